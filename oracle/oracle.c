@@ -1,0 +1,392 @@
+/*
+ * oracle/oracle.c -- float64 CPU oracle of the coarse-grid Dirac operator.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load, call or link this code.  It shares no
+ * code, header, table or helper with the CUDA library (paper_1612_07873_b200/csrc), and
+ * the CUDA library never calls it.
+ *
+ * What it computes (§3.4 Eq. 3, read as DESIGN.md R1-R10):
+ *
+ *   y(x) = X(x) v(x) + sum_{mu=0..3} [ L_{2mu}(x) v(x+mu) + L_{2mu+1}(x) v(x-mu) ]
+ *
+ * on a periodic 4-D lattice, each L_k(x) a dense N x N complex matrix, N = 2*Nvec
+ * (coarse spin 2 x Nvec colours).  Layouts:
+ *   site  s = ((x3*L2 + x2)*L1 + x1)*L0 + x0         (Listing 2: x0 fastest)
+ *   dof   i = sigma*Nvec + c                         (Listing 3: spin slower)
+ *   hop   k = 2*mu + dir, dir 0 = +mu, dir 1 = -mu   (§6.3 "mu*2+dir"); k = 8: X
+ *   links[((s*9 + k)*N + i)*N + j], v[s*N + i]       complex double, interleaved re/im
+ *
+ * Every function is the plain definition written out: no blocking, no fusion, fixed
+ * term order (X first, then k = 0..7), OpenMP only over independent output sites
+ * (the paper's own CPU path is "rudimentary OpenMP").
+ *
+ * Pins (tests/test_oracle_*.py): plane-wave closed form, unit impulse,
+ * shift == numpy.roll, block-diagonal == numpy.matmul, identity, L=1 self hops,
+ * tau3-hermiticity adjoint identity + negative control, <w,Dv> == <D^H w,v>,
+ * dense assembly, partition emulation, face slicing == numpy slicing, fp16 quantiser
+ * == numpy float16 cast.  No function here is "parity unpinned".
+ */
+#include <complex.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <math.h>
+
+typedef double complex cplx;
+
+#define MAXN 128
+
+/* ---------------------------------------------------------------- geometry */
+
+/* PAPER.md:197 (§6.1, Listing 2): x[0] fastest, x[3] slowest. */
+static int64_t site_of(const int L[4], const int x[4])
+{
+    return (((int64_t)x[3] * L[2] + x[2]) * L[1] + x[1]) * L[0] + x[0];
+}
+
+static void coords_of(const int L[4], int64_t s, int x[4])
+{
+    x[0] = (int)(s % L[0]); s /= L[0];
+    x[1] = (int)(s % L[1]); s /= L[1];
+    x[2] = (int)(s % L[2]); s /= L[2];
+    x[3] = (int)s;
+}
+
+static int64_t volume_of(const int L[4])
+{
+    return (int64_t)L[0] * L[1] * L[2] * L[3];
+}
+
+/* Periodic neighbour x + step*mu_hat (R10: periodic in all four dims). */
+static int64_t hop(const int L[4], const int x[4], int mu, int step)
+{
+    int y[4] = {x[0], x[1], x[2], x[3]};
+    y[mu] = ((y[mu] + step) % L[mu] + L[mu]) % L[mu];
+    return site_of(L, y);
+}
+
+/* Neighbour site index for each hop k = 0..8 of site s (k = 8: the site itself). */
+void oracle_neighbours(const int L[4], int64_t s, int64_t out[9])
+{
+    int x[4];
+    coords_of(L, s, x);
+    for (int mu = 0; mu < 4; mu++) {
+        out[2 * mu] = hop(L, x, mu, +1);
+        out[2 * mu + 1] = hop(L, x, mu, -1);
+    }
+    out[8] = s;
+}
+
+/* ---------------------------------------------------------------- operator */
+
+/* acc[i] += sum_j M[i][j] * u[j] */
+static void matvec_acc(int N, const cplx *M, const cplx *u, cplx *acc)
+{
+    for (int i = 0; i < N; i++) {
+        cplx a = 0;
+        for (int j = 0; j < N; j++) a += M[(int64_t)i * N + j] * u[j];
+        acc[i] += a;
+    }
+}
+
+/* acc[i] += sum_j conj(M[j][i]) * u[j]    (M^H u) */
+static void matvec_h_acc(int N, const cplx *M, const cplx *u, cplx *acc)
+{
+    for (int i = 0; i < N; i++) {
+        cplx a = 0;
+        for (int j = 0; j < N; j++) a += conj(M[(int64_t)j * N + i]) * u[j];
+        acc[i] += a;
+    }
+}
+
+/* One output site from its 9 link matrices and the 9 vectors they multiply
+ * (links9[k], vn[k] = v(nbr_k(x)), k = 8 the diagonal).  Term order: X, then k = 0..7. */
+void oracle_site_apply(int N, const double *links9, const double *vn, double *y)
+{
+    const cplx *Lk = (const cplx *)links9;
+    const cplx *u = (const cplx *)vn;
+    cplx acc[MAXN];
+    for (int i = 0; i < N; i++) acc[i] = 0;
+    matvec_acc(N, Lk + (int64_t)8 * N * N, u + (int64_t)8 * N, acc);
+    for (int k = 0; k < 8; k++) matvec_acc(N, Lk + (int64_t)k * N * N, u + (int64_t)k * N, acc);
+    memcpy(y, acc, sizeof(cplx) * N);
+}
+
+/* y = D v  (Eq. 3 as read in DESIGN.md R1-R3: all nine matrices stored at x, oriented). */
+void oracle_apply(const int L[4], int N, const double *links_, const double *v_, double *y_)
+{
+    const cplx *links = (const cplx *)links_;
+    const cplx *v = (const cplx *)v_;
+    cplx *y = (cplx *)y_;
+    const int64_t V = volume_of(L);
+    const int64_t NN = (int64_t)N * N;
+#pragma omp parallel for schedule(static)
+    for (int64_t s = 0; s < V; s++) {
+        int x[4];
+        coords_of(L, s, x);
+        cplx acc[MAXN];
+        for (int i = 0; i < N; i++) acc[i] = 0;
+        matvec_acc(N, links + (s * 9 + 8) * NN, v + s * N, acc);                  /* X(x) v(x)        */
+        for (int mu = 0; mu < 4; mu++) {
+            int64_t sf = hop(L, x, mu, +1), sb = hop(L, x, mu, -1);
+            matvec_acc(N, links + (s * 9 + 2 * mu) * NN, v + sf * N, acc);         /* L_{2mu} v(x+mu)   */
+            matvec_acc(N, links + (s * 9 + 2 * mu + 1) * NN, v + sb * N, acc);     /* L_{2mu+1} v(x-mu) */
+        }
+        for (int i = 0; i < N; i++) y[s * N + i] = acc[i];
+    }
+}
+
+/* tau3 = diag(+1 x Nvec, -1 x Nvec) (PAPER.md:121 footnote 1; R5/R6). */
+static void tau3(int64_t V, int N, const cplx *in, cplx *out)
+{
+    for (int64_t s = 0; s < V; s++)
+        for (int i = 0; i < N; i++)
+            out[s * N + i] = (i < N / 2) ? in[s * N + i] : -in[s * N + i];
+}
+
+/* y = tau3 D tau3 w: the library's "dagger" (R5).  Equal to D^H w iff the links
+ * are tau3-hermitian (coarse gamma5-hermiticity, PAPER.md:121 footnote 1). */
+void oracle_apply_dagger_tau3(const int L[4], int N, const double *links, const double *w_, double *y_)
+{
+    const int64_t V = volume_of(L);
+    cplx *t = (cplx *)malloc(sizeof(cplx) * V * N);
+    cplx *u = (cplx *)malloc(sizeof(cplx) * V * N);
+    tau3(V, N, (const cplx *)w_, t);
+    oracle_apply(L, N, links, (const double *)t, (double *)u);
+    tau3(V, N, u, (cplx *)y_);
+    free(t);
+    free(u);
+}
+
+/* y = D^H w, the true adjoint, from its definition:
+ *   (D^H w)(x) = X(x)^H w(x) + sum_mu [ L_{2mu}(x-mu)^H w(x-mu) + L_{2mu+1}(x+mu)^H w(x+mu) ]
+ * (block (x', x) of D is L_{2mu}(x') when x = x'+mu and L_{2mu+1}(x') when x = x'-mu). */
+void oracle_adjoint(const int L[4], int N, const double *links_, const double *w_, double *y_)
+{
+    const cplx *links = (const cplx *)links_;
+    const cplx *w = (const cplx *)w_;
+    cplx *y = (cplx *)y_;
+    const int64_t V = volume_of(L);
+    const int64_t NN = (int64_t)N * N;
+#pragma omp parallel for schedule(static)
+    for (int64_t s = 0; s < V; s++) {
+        int x[4];
+        coords_of(L, s, x);
+        cplx acc[MAXN];
+        for (int i = 0; i < N; i++) acc[i] = 0;
+        matvec_h_acc(N, links + (s * 9 + 8) * NN, w + s * N, acc);
+        for (int mu = 0; mu < 4; mu++) {
+            int64_t sb = hop(L, x, mu, -1), sf = hop(L, x, mu, +1);
+            matvec_h_acc(N, links + (sb * 9 + 2 * mu) * NN, w + sb * N, acc);
+            matvec_h_acc(N, links + (sf * 9 + 2 * mu + 1) * NN, w + sf * N, acc);
+        }
+        for (int i = 0; i < N; i++) y[s * N + i] = acc[i];
+    }
+}
+
+/* Dense D in C^{VN x VN} (row-major), assembled with += so that the L_mu = 1, 2 cases,
+ * where several hops land on the same block, keep every term (R10). */
+void oracle_dense(const int L[4], int N, const double *links_, double *D_)
+{
+    const cplx *links = (const cplx *)links_;
+    cplx *D = (cplx *)D_;
+    const int64_t V = volume_of(L);
+    const int64_t NN = (int64_t)N * N, VN = V * N;
+    memset(D, 0, sizeof(cplx) * VN * VN);
+    for (int64_t s = 0; s < V; s++) {
+        int64_t nb[9];
+        oracle_neighbours(L, s, nb);
+        for (int k = 0; k < 9; k++)
+            for (int i = 0; i < N; i++)
+                for (int j = 0; j < N; j++)
+                    D[(s * N + i) * VN + nb[k] * N + j] += links[(s * 9 + k) * NN + (int64_t)i * N + j];
+    }
+}
+
+/* ---------------------------------------------------------------- halo (multi-rank) */
+
+/* Canonical face order (R13, "a single packing kernel ... for all
+ * exchange dimensions"): for each split dim mu ascending: block A = the face sent to the
+ * +mu neighbour (local x_mu = Lloc_mu - 1), then block B = the face sent to the -mu
+ * neighbour (x_mu = 0).  Inside a face, sites are lexicographic over the other three
+ * coordinates, lowest mu fastest.  Each block holds the site records (rec_bytes each)
+ * followed, if scales != NULL, by that block's per-site scales (scale_bytes each).
+ * Returns the number of bytes written (out may be NULL to query the size). */
+size_t oracle_pack_halo(const int Lloc[4], const int split[4], const void *payload, size_t rec_bytes,
+                        const void *scales, size_t scale_bytes, void *out)
+{
+    const unsigned char *p = (const unsigned char *)payload;
+    const unsigned char *sc = (const unsigned char *)scales;
+    unsigned char *o = (unsigned char *)out;
+    size_t off = 0;
+    for (int mu = 0; mu < 4; mu++) {
+        if (!split[mu]) continue;
+        int o3[3], n = 0;
+        for (int nu = 0; nu < 4; nu++)
+            if (nu != mu) o3[n++] = nu;
+        int64_t F = (int64_t)Lloc[o3[0]] * Lloc[o3[1]] * Lloc[o3[2]];
+        for (int blk = 0; blk < 2; blk++) {
+            int xmu = (blk == 0) ? Lloc[mu] - 1 : 0;
+            for (int pass = 0; pass < (sc ? 2 : 1); pass++) {
+                size_t rb = pass == 0 ? rec_bytes : scale_bytes;
+                const unsigned char *src = pass == 0 ? p : sc;
+                for (int64_t f = 0; f < F; f++) {
+                    int x[4];
+                    int64_t t = f;
+                    x[o3[0]] = (int)(t % Lloc[o3[0]]); t /= Lloc[o3[0]];
+                    x[o3[1]] = (int)(t % Lloc[o3[1]]); t /= Lloc[o3[1]];
+                    x[o3[2]] = (int)t;
+                    x[mu] = xmu;
+                    int64_t s = site_of(Lloc, x);
+                    if (o) memcpy(o + off, src + (size_t)s * rb, rb);
+                    off += rb;
+                }
+            }
+        }
+    }
+    return off;
+}
+
+/* Emulate an apply distributed over a P[0] x P[1] x P[2] x P[3] process grid with explicit
+ * halo buffers: every rank packs its faces (oracle_pack_halo), the blocks are delivered
+ * (block A of rank r -> block A of rank r+mu, block B -> rank r-mu), and every rank applies
+ * the stencil reading remote neighbours from its receive buffer.  Same term order as
+ * oracle_apply, so the result must be bit-identical to it (pin P10).
+ * Rank layout: lexicographic like sites, rank = ((c3*P2 + c2)*P1 + c1)*P0 + c0. */
+void oracle_partitioned_apply(const int Lg[4], const int P[4], int N, const double *links_,
+                              const double *v_, double *y_)
+{
+    const cplx *links = (const cplx *)links_;
+    const cplx *v = (const cplx *)v_;
+    cplx *y = (cplx *)y_;
+    int Ll[4], split[4];
+    for (int mu = 0; mu < 4; mu++) {
+        Ll[mu] = Lg[mu] / P[mu];
+        split[mu] = P[mu] > 1;
+    }
+    const int nranks = P[0] * P[1] * P[2] * P[3];
+    const int64_t Vl = volume_of(Ll);
+    const int64_t NN = (int64_t)N * N;
+    const size_t rec = sizeof(cplx) * N;
+    const size_t hbytes = oracle_pack_halo(Ll, split, NULL, rec, NULL, 0, NULL);
+    cplx **vloc = (cplx **)calloc(nranks, sizeof(cplx *));
+    unsigned char **send = (unsigned char **)calloc(nranks, sizeof(void *));
+    unsigned char **recv = (unsigned char **)calloc(nranks, sizeof(void *));
+    int (*rc)[4] = calloc(nranks, sizeof(*rc));
+    /* scatter the global field into per-rank local fields, and pack */
+    for (int r = 0; r < nranks; r++) {
+        int t = r;
+        for (int mu = 0; mu < 4; mu++) { rc[r][mu] = t % P[mu]; t /= P[mu]; }
+        vloc[r] = (cplx *)malloc(rec * Vl);
+        for (int64_t sl = 0; sl < Vl; sl++) {
+            int xl[4], xg[4];
+            coords_of(Ll, sl, xl);
+            for (int mu = 0; mu < 4; mu++) xg[mu] = rc[r][mu] * Ll[mu] + xl[mu];
+            memcpy(vloc[r] + sl * N, v + site_of(Lg, xg) * N, rec);
+        }
+        send[r] = (unsigned char *)malloc(hbytes ? hbytes : 1);
+        recv[r] = (unsigned char *)malloc(hbytes ? hbytes : 1);
+        oracle_pack_halo(Ll, split, vloc[r], rec, NULL, 0, send[r]);
+    }
+    /* deliver: block A (to +mu) lands in the +mu neighbour's block A, block B in the -mu one's */
+    for (int r = 0; r < nranks; r++) {
+        size_t off = 0;
+        for (int mu = 0; mu < 4; mu++) {
+            if (!split[mu]) continue;
+            size_t fb = rec * (size_t)(Vl / Ll[mu]);
+            for (int blk = 0; blk < 2; blk++) {
+                int c[4] = {rc[r][0], rc[r][1], rc[r][2], rc[r][3]};
+                c[mu] = (c[mu] + (blk == 0 ? 1 : -1) + P[mu]) % P[mu];
+                int dst = ((c[3] * P[2] + c[2]) * P[1] + c[1]) * P[0] + c[0];
+                memcpy(recv[dst] + off, send[r] + off, fb);
+                off += fb;
+            }
+        }
+    }
+    /* local apply; remote neighbours are read from the receive buffer */
+    for (int r = 0; r < nranks; r++) {
+        for (int64_t sl = 0; sl < Vl; sl++) {
+            int xl[4], xg[4];
+            coords_of(Ll, sl, xl);
+            for (int mu = 0; mu < 4; mu++) xg[mu] = rc[r][mu] * Ll[mu] + xl[mu];
+            int64_t sg = site_of(Lg, xg);
+            const cplx *nbv[9];
+            for (int mu = 0; mu < 4; mu++) {
+                for (int dir = 0; dir < 2; dir++) {
+                    int step = dir == 0 ? +1 : -1;
+                    int edge = dir == 0 ? (xl[mu] == Ll[mu] - 1) : (xl[mu] == 0);
+                    if (split[mu] && edge) {
+                        /* +mu hop reads block B (sent by the +mu neighbour), -mu hop block A */
+                        size_t off = 0;
+                        for (int nu = 0; nu < mu; nu++)
+                            if (split[nu]) off += 2 * rec * (size_t)(Vl / Ll[nu]);
+                        if (dir == 0) off += rec * (size_t)(Vl / Ll[mu]);
+                        int o3[3], n = 0;
+                        for (int nu = 0; nu < 4; nu++)
+                            if (nu != mu) o3[n++] = nu;
+                        int64_t f = ((int64_t)xl[o3[2]] * Ll[o3[1]] + xl[o3[1]]) * Ll[o3[0]] + xl[o3[0]];
+                        nbv[2 * mu + dir] = (const cplx *)(recv[r] + off + (size_t)f * rec);
+                    } else {
+                        nbv[2 * mu + dir] = vloc[r] + hop(Ll, xl, mu, step) * N;
+                    }
+                }
+            }
+            nbv[8] = vloc[r] + sl * N;
+            cplx acc[MAXN];
+            for (int i = 0; i < N; i++) acc[i] = 0;
+            matvec_acc(N, links + (sg * 9 + 8) * NN, nbv[8], acc);
+            for (int k = 0; k < 8; k++) matvec_acc(N, links + (sg * 9 + k) * NN, nbv[k], acc);
+            for (int i = 0; i < N; i++) y[sg * N + i] = acc[i];
+        }
+    }
+    for (int r = 0; r < nranks; r++) {
+        free(vloc[r]);
+        free(send[r]);
+        free(recv[r]);
+    }
+    free(vloc);
+    free(send);
+    free(recv);
+    free(rc);
+}
+
+/* ---------------------------------------------------------------- 16-bit storage */
+
+/* Half-precision storage ("custom 16-bit ... storage format" with a scale;
+ * DESIGN.md R12): per record (a site's vector, or one (site, k) matrix):
+ *   xf = fp32_rn(x);  s = max |xf|  (over all re and im parts);
+ *   q  = fp16_rn(xf / s)   (correctly rounded fp32 division, then round-to-nearest-even);
+ *   s == 0 -> every q = +0.
+ * Both roundings are IEEE: C's double->float cast and _Float16 conversion (x86-64 SSE). */
+void oracle_quantise_fp16(int64_t nrec, int64_t reals_per_rec, const double *x, uint16_t *q, float *scale)
+{
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < nrec; r++) {
+        const double *xr = x + r * reals_per_rec;
+        float s = 0.0f;
+        for (int64_t e = 0; e < reals_per_rec; e++) {
+            float a = fabsf((float)xr[e]);
+            if (a > s) s = a;
+        }
+        scale[r] = s;
+        for (int64_t e = 0; e < reals_per_rec; e++) {
+            _Float16 h = (s == 0.0f) ? (_Float16)0.0f : (_Float16)((float)xr[e] / s);
+            uint16_t bits;
+            memcpy(&bits, &h, 2);
+            q[r * reals_per_rec + e] = bits;
+        }
+    }
+}
+
+/* x' = float(q) * s, returned in double (exact). */
+void oracle_dequantise_fp16(int64_t nrec, int64_t reals_per_rec, const uint16_t *q, const float *scale,
+                            double *x)
+{
+    for (int64_t r = 0; r < nrec; r++)
+        for (int64_t e = 0; e < reals_per_rec; e++) {
+            _Float16 h;
+            memcpy(&h, q + r * reals_per_rec + e, 2);
+            x[r * reals_per_rec + e] = (double)((float)h * scale[r]);
+        }
+}
