@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""Benchmark of the coarse-grid Dirac operator apply (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--prec fp32|fp16]
+
+A "step" is one apply y = D v of the whole local lattice (all hot-path rows of SURVEY §8(a):
+decode, link streaming, neighbour gather, dot products, reductions, store; for N > 1 also the
+halo pack, NCCL exchange and halo-term kernel).  Steps are chained (v -> y -> v ...), as in a
+coarse-grid solver.  N = 1 workload: the 8^4, Nvec = 24 lattice the north_star target is quoted
+on (BASELINE.json configs[2]).  N > 1: weak scaling, every rank holds an 8^4 block of a
+8 x 8 x 8 x (8N) lattice split along T, with the NCCL halo exchange.
+
+Rank 0 prints ONE JSON line.  Inputs are synthetic (device generator, links
+scaled by 2^-4), resident in HBM; the link field (680 MB) is larger than L2 (126 MB), so no L2
+flush is needed between steps.  Timing: CUDA events on the launching stream, barrier +
+synchronize on both sides, max over ranks.  `e2e` is the same metric through the public API
+with host buffers: pinned-host -> device import of v, apply, device -> pinned-host export of y,
+every step.  `cpu_baseline` / --impl reference: the float64 oracle (oracle/) timed on this
+host's cores on a bounded periodic sub-lattice of the same Nvec (per-site work is identical).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = {
+    "dims": (8, 8, 8, 8),
+    "nvec": 24,
+    "name": "coarse lattice 8^4, Nvec=24 (48^3x96 fine lattice blocked 6^3x12)",
+}
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+# ------------------------------------------------------------------ clocks (nvidia-smi during timing)
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.device), "-lms", "20"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ oracle timing (CPU baseline)
+SAMPLE_LADDER = [(2, 2, 2, 2), (4, 2, 2, 2), (4, 4, 2, 2), (4, 4, 4, 2), (4, 4, 4, 4), (8, 4, 4, 4), (8, 8, 4, 4),
+                 (8, 8, 8, 2), (8, 8, 8, 4), (8, 8, 8, 8)]
+
+
+def _oracle_setup(nvec):
+    cores = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    import oracle
+    import synth
+    return oracle, synth, int(os.environ["OMP_NUM_THREADS"])
+
+
+def oracle_time_per_site(nvec, dims=(4, 4, 4, 4)):
+    oracle, synth, cores = _oracle_setup(nvec)
+    N = 2 * nvec
+    L = synth.links(dims, N, scale_log2=-4)
+    v = synth.vector(dims, N)
+    oracle.apply(dims, L, v)
+    t0 = time.perf_counter()
+    oracle.apply(dims, L, v)
+    return (time.perf_counter() - t0) / (dims[0] * dims[1] * dims[2] * dims[3])
+
+
+def cpu_baseline(nvec, budget_s=15.0, dims=(8, 8, 8, 2)):
+    """float64 oracle apply on a periodic sub-lattice, repeated for ~budget_s seconds."""
+    from paper_1612_07873_b200 import perfmodel  # model only; no library call
+    oracle, synth, cores = _oracle_setup(nvec)
+    N = 2 * nvec
+    L = synth.links(dims, N, scale_log2=-4)
+    v = synth.vector(dims, N)
+    oracle.apply(dims, L, v)   # warm-up
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        v = oracle.apply(dims, L, v)
+        reps += 1
+        el = time.perf_counter() - t0
+        if (el >= budget_s and reps >= 3) or reps >= 1000:
+            break
+    V = dims[0] * dims[1] * dims[2] * dims[3]
+    gflops = perfmodel.flops_per_site(nvec) * V * reps / el / 1e9
+    return {"value": round(gflops, 3), "unit": "GFLOPS", "cores": cores, "kind": "oracle",
+            "sample": f"{reps} float64 oracle applies on a periodic {'x'.join(map(str, dims))} sub-lattice "
+                      f"({V} sites, Nvec={nvec}; same per-site work as the 8^4 workload), {el:.1f} s",
+            "gbs_fp64": round(perfmodel.metric_bytes_per_site(nvec, 'fp64') * V * reps / el / 1e9, 3)}
+
+
+# ------------------------------------------------------------------ distributed plumbing
+def dist_setup():
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if os.environ.get("CD_BENCH_BACKEND", "nccl") == "nccl" else "gloo"
+        dist.init_process_group(backend)
+    return world, rank, local
+
+
+def dist_max(x: float, world: int, device=None) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def measured_peak():
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs: 1 Gi bf16 copy, read+write)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(prec):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel from the
+    committed ncu --set full capture (profiles/ncu_traffic.json), or None."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        return t.get(f"8^4_nvec24_{prec}")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    import paper_1612_07873_b200 as cd
+    from paper_1612_07873_b200 import perfmodel
+
+    L0, L1, L2, L3 = WORKLOAD["dims"]
+    nvec = WORKLOAD["nvec"]
+    gdims = (L0, L1, L2, L3 * world)
+    pgrid = (1, 1, 1, world)
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist
+        obj = [cd.cd_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    ctx = cd.Context(gdims, nvec, pgrid, device=local, nranks=world, rank=rank, nccl_id=nccl_id)
+    prec = args.prec
+    stream = torch.cuda.current_stream()
+    links = ctx.links_generate(prec, kind="general", seed=0x1612, scale_log2=-4)
+    a, b = ctx.field(prec), ctx.field(prec)
+    a.generate(seed=0x7873, tag=2)
+    torch.cuda.synchronize()
+
+    def steps(n):
+        x, y = a, b
+        for _ in range(n):
+            links.apply(y, x, stream)
+            x, y = y, x
+
+    # warm-up (the first call autotunes; excluded, as the paper excludes its tuning solve)
+    steps(max(args.warmup, 3))
+    torch.cuda.synchronize()
+    t_end = time.perf_counter() + 0.5       # settle clocks under load before the timed region
+    while time.perf_counter() < t_end:
+        steps(50)
+        torch.cuda.synchronize()
+    a.generate(seed=0x7873, tag=2)
+    barrier(world)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.05)
+    n0 = cd.cd_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    steps(args.steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    sampler.stop()
+    launches = cd.cd_launch_count() - n0
+    ms_local = e0.elapsed_time(e1) / args.steps
+    barrier(world)
+    ms = dist_max(ms_local, world, device=f"cuda:{local}")
+    clocks = sampler.summary()
+
+    V_local = L0 * L1 * L2 * L3
+    V_glob = V_local * world
+    flops = perfmodel.flops_per_site(nvec) * V_glob
+    gflops = flops / (ms * 1e-3) / 1e9
+    gbs_local = perfmodel.metric_bytes_per_site(nvec, prec) * V_local / (ms * 1e-3) / 1e9
+    peak, peak_src = measured_peak()
+
+    # ---- e2e through the public API with pinned host buffers (h2d of v, d2h of y, every step)
+    N = 2 * nvec
+    cdt = torch.complex64
+    hv = torch.empty((V_local, N), dtype=cdt).pin_memory()
+    hy = torch.empty((V_local, N), dtype=cdt).pin_memory()
+    a.export(hv, stream=stream)
+    k_e2e = max(10, min(args.steps, 500))
+    for _ in range(3):
+        a.import_(hv, stream)
+        links.apply(b, a, stream)
+        b.export(hy, stream=stream, sync=False)
+    barrier(world)
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(k_e2e):
+        a.import_(hv, stream)
+        links.apply(b, a, stream)
+        b.export(hy, stream=stream, sync=False)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = dist_max(f0.elapsed_time(f1) / k_e2e, world, device=f"cuda:{local}")
+    e2e_val = flops / (ms_e2e * 1e-3) / 1e9
+
+    # ---- cpu baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(nvec, budget_s=args.cpu_budget)
+
+    if rank == 0:
+        variant = ctx.variants(prec)[ctx.chosen_variant(prec)]
+        traffic = ncu_traffic(prec)
+        out = {
+            "metric": "coarse-Dslash GFLOPS and HBM GB/s (% of B200 roofline)",
+            "value": round(gflops, 2),
+            "unit": "GFLOPS",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms, 6),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32" if prec == "fp32" else "f16-storage/f32-accumulate",
+            "data": "synthetic (device splitmix64 generator, links x 2^-4; DESIGN.md §3)",
+            "config": {"workload": WORKLOAD["name"] if world == 1 else
+                       f"coarse lattice 8x8x8x{8 * world} (8^4 per GPU, T-partitioned), Nvec=24",
+                       "global_dims": list(gdims), "proc_grid": list(pgrid), "nvec": nvec, "storage": prec,
+                       "op": "apply (D v), chained v->y->v", "variant": variant,
+                       "l2": "inputs larger than L2: links %.1f MB per GPU vs 126 MB L2" %
+                             (V_local * 9 * (N * N * (8 if prec == 'fp32' else 4)) / 1e6),
+                       "parallelism": f"T-split x{world}" if world > 1 else "single GPU"},
+            "gbs": round(gbs_local * world, 1),
+            "gbs_per_gpu": round(gbs_local, 1),
+            "pct_of_8tbs_per_gpu": round(100 * gbs_local / 8000.0, 2),
+            "roofline": {"bound": "hbm", "achieved": round(gbs_local, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(gbs_local / peak, 4), "traffic": traffic,
+                         "kernel": variant, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": perfmodel.metric_bytes_per_site(nvec, prec) * V_local},
+            "e2e": {"value": round(e2e_val, 2), "unit": "GFLOPS", "ms_per_step": round(ms_e2e, 5),
+                    "h2d_bytes_per_step": V_local * N * 8, "d2h_bytes_per_step": V_local * N * 8},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ reference arm (the oracle)
+def run_reference(args):
+    world, rank = env_int("WORLD_SIZE", 1), env_int("RANK", 0)
+    if rank != 0:
+        return
+    from paper_1612_07873_b200 import perfmodel  # model only
+    nvec = WORKLOAD["nvec"]
+    oracle, synth, cores = _oracle_setup(nvec)
+    N = 2 * nvec
+    budget = args.ref_budget
+    t_site = oracle_time_per_site(nvec)
+    dims = SAMPLE_LADDER[0]
+    for d in SAMPLE_LADDER:
+        V = d[0] * d[1] * d[2] * d[3]
+        if V * t_site * (args.steps + args.warmup) <= budget:
+            dims = d
+    V = dims[0] * dims[1] * dims[2] * dims[3]
+    L = synth.links(dims, N, scale_log2=-4)
+    v = synth.vector(dims, N)
+    for _ in range(args.warmup):
+        v = oracle.apply(dims, L, v)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v = oracle.apply(dims, L, v)
+    el = time.perf_counter() - t0
+    ms = el / args.steps * 1e3
+    gflops = perfmodel.flops_per_site(nvec) * V / (ms * 1e-3) / 1e9
+    sample = f"each step: one float64 oracle apply on a periodic {'x'.join(map(str, dims))} sub-lattice " \
+             f"({V} of the workload's sites per step, Nvec={nvec}, same per-site work)"
+    out = {
+        "impl": "reference",
+        "metric": "coarse-Dslash GFLOPS and HBM GB/s (% of B200 roofline)",
+        "value": round(gflops, 3), "unit": "GFLOPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (synth/ splitmix64 generator, links x 2^-4)",
+        "config": {"workload": WORKLOAD["name"], "nvec": nvec, "sample_dims": list(dims)},
+        "cpu_baseline": {"value": round(gflops, 3), "unit": "GFLOPS", "cores": cores, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(gflops, 3), "unit": "GFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--prec", choices=["fp32", "fp16"], default="fp32")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--ref-budget", type=float, default=90.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

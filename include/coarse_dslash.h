@@ -1,0 +1,216 @@
+/*
+ * coarse_dslash.h -- C ABI of the B200-native coarse-grid Dirac operator.
+ *
+ * The operator (§3.4 Eq. 3, read as DESIGN.md R1-R10):
+ *
+ *     y(x) = X(x) v(x) + sum_{mu=0..3} [ L_{2mu}(x) v(x+mu) + L_{2mu+1}(x) v(x-mu) ]
+ *
+ * on a periodic 4-D coarse lattice; every L_k(x) is a dense N x N complex matrix with
+ * N = 2*Nvec (coarse spin 2 x Nvec colours).  The dagger is
+ * tau3 D tau3 (R5; PAPER.md:121 footnote 1).
+ *
+ * CANONICAL LAYOUTS (what import/export/upload read and write):
+ *   site   s = ((x3*L2 + x2)*L1 + x1)*L0 + x0     x0 fastest (Listing 2)
+ *   dof    i = sigma*Nvec + c                     spin slower (Listing 3)
+ *   hop    k = 2*mu + dir; dir 0 -> +mu, dir 1 -> -mu; k = 8 -> X   (§6.3)
+ *   vector   v[s][i]          complex, interleaved {re, im}
+ *   links    L[s][k][i][j]    complex, row-major: y_i += L[i][j] v_j
+ * With nranks > 1 every rank passes its LOCAL block (local dims = global / proc_grid),
+ * indexed with local coordinates; rank r owns the block at grid coordinates
+ * c = (r % P0, (r / P0) % P1, ...) (lexicographic like sites).
+ *
+ * STORAGE PRECISION (a run-time attribute of every field / link set):
+ *   CD_FP32  fp32 payload.
+ *   CD_FP16  IEEE binary16 payload normalised by an fp32 scale, one scale per site
+ *            for vectors and one per (site, k) matrix for links (R12, the
+ *            paper's "16-bit ... storage format" with a scale).
+ *   Arithmetic is always fp32 (R11).
+ *
+ * CONVENTIONS
+ *   - Every function returns a cd_status; on failure cd_last_error() gives a
+ *     thread-local message.  No C++ exception and no abort() crosses this ABI.
+ *   - Argument errors are detected synchronously and nothing is enqueued.
+ *   - Data calls are asynchronous and stream-ordered on the caller's cudaStream_t
+ *     (passed as void*; NULL = legacy default stream).  They never synchronise the
+ *     host, except coarse_links_upload / *_read_stored from host memory, which return
+ *     once the host source (destination) has been consumed (filled).
+ *   - Asynchronous CUDA / NCCL faults surface at the next call that observes them.
+ *   - Pointers are borrowed for the duration of the stream-ordered work only; the
+ *     library never keeps a caller pointer except caller-provided field memory
+ *     (coarse_field_alloc with device_mem != NULL), which stays caller-owned.
+ *   - apply / apply_dagger are COLLECTIVE when nranks > 1: every rank calls them in
+ *     the same order.  They are CUDA-graph capturable once the (volume, Nvec,
+ *     precision, op, partition) key has been tuned (first call; or CD_TUNE=0).
+ */
+#ifndef COARSE_DSLASH_H
+#define COARSE_DSLASH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+typedef enum {
+    CD_OK = 0,
+    CD_ERR_INVALID = -1,      /* bad argument (NULL, size, alias, range)               */
+    CD_ERR_UNSUPPORTED = -2,  /* valid but not implemented (e.g. Nvec not in {24, 32}) */
+    CD_ERR_OOM = -3,          /* device or host allocation failed                      */
+    CD_ERR_CUDA = -4,         /* CUDA runtime error (message has cudaGetErrorString)   */
+    CD_ERR_NCCL = -5,         /* NCCL error or libnccl.so.2 not loadable               */
+    CD_ERR_MISMATCH = -6      /* objects from different contexts / precisions          */
+} cd_status;
+
+typedef enum { CD_FP32 = 0, CD_FP16 = 1 } cd_precision;    /* storage; arithmetic is fp32   */
+typedef enum { CD_C64 = 0, CD_C128 = 1 } cd_host_dtype;     /* canonical complex element type */
+
+typedef enum {                 /* synthetic link recipes   */
+    CD_LINKS_GENERAL = 0,      /* L_k(x) = G(x, k)                                          */
+    CD_LINKS_HERMITIAN = 1,    /* tau3-hermitian: L_{2mu+1}(x) = tau3 G(x-mu,2mu)^H tau3, X = (G+tau3 G^H tau3)/2 */
+    CD_LINKS_TI_GENERAL = 2,   /* translation invariant (gsite := 0, tag 4)                 */
+    CD_LINKS_TI_HERMITIAN = 3
+} cd_links_kind;
+
+typedef enum {
+    CD_OPT_VARIANT = 0,        /* force a kernel variant id (>= 0), -1 = autotune (default) */
+    CD_OPT_TUNE = 1,           /* 1 = autotune on first call of a key (default), 0 = heuristic */
+    CD_OPT_HALO_SELF_MASK = 2, /* bit mu: route dim mu through the halo path even when P_mu = 1
+                                  (self exchange; exercises pack/exchange/halo kernels on 1 GPU).
+                                  Only valid before the first apply. */
+    CD_OPT_PDL = 3             /* 1 = programmatic dependent launch between kernels (default 1) */
+} cd_option;
+
+typedef struct {
+    int32_t global_dims[4];    /* L0..L3 (x0 fastest, x3 = T); each >= 1                     */
+    int32_t nvec;              /* Nvec; N = 2*Nvec; supported: 24, 32 (CD_ERR_UNSUPPORTED)   */
+    int32_t proc_grid[4];      /* P0..P3; prod == nranks; global_dims[mu] % P[mu] == 0       */
+} cd_geometry;
+
+typedef struct cd_context cd_context;
+typedef struct cd_field cd_field;
+typedef struct cd_links cd_links;
+
+/* ------------------------------------------------------------------ context */
+
+/* Library version string (static storage). */
+const char *cd_version(void);
+
+/* Thread-local message of the last failed call on this thread ("" if none). */
+const char *cd_last_error(void);
+
+/* NCCL unique id for a multi-rank context (rank 0 calls it and broadcasts the 128 bytes,
+ * e.g. with torch.distributed).  CD_ERR_NCCL if libnccl.so.2 cannot be loaded. */
+int cd_get_unique_id(uint8_t out_id[128]);
+
+/* Create a context on CUDA device `device` for rank `rank` of `nranks`.
+ * nccl_id: NULL iff nranks == 1; else the 128-byte id from cd_get_unique_id (collective:
+ * all ranks call this concurrently).  Allocates halo/scratch buffers (device memory).
+ * Errors: CD_ERR_INVALID (geometry), CD_ERR_UNSUPPORTED (nvec), CD_ERR_CUDA, CD_ERR_NCCL. */
+int cd_context_create(const cd_geometry *geom, int device, int nranks, int rank, const uint8_t *nccl_id,
+                      cd_context **out);
+
+/* Destroy a context (synchronises its device; fields/links of it must be freed first). */
+int cd_context_destroy(cd_context *ctx);
+
+/* Set a cd_option (see the enum).  CD_ERR_INVALID for an unknown option or bad value. */
+int cd_context_set_option(cd_context *ctx, int option, int64_t value);
+
+/* Local geometry: local dims (4 ints), local volume, rank grid coordinates (4 ints). */
+int cd_context_local(const cd_context *ctx, int32_t local_dims[4], int64_t *local_volume,
+                     int32_t grid_coords[4]);
+
+/* Number of kernel variants for a precision, and the name of variant `id`
+ * (static storage; NULL if out of range). */
+int cd_variant_count(const cd_context *ctx, cd_precision prec);
+const char *cd_variant_name(const cd_context *ctx, cd_precision prec, int id);
+
+/* Variant chosen for (prec, dagger) by the tuner / heuristic for this context's geometry
+ * (-1 if that key has not been resolved yet). */
+int cd_context_chosen_variant(const cd_context *ctx, cd_precision prec, int dagger);
+
+/* Total kernels launched by this process through this library (for launch accounting). */
+uint64_t cd_launch_count(void);
+
+/* ------------------------------------------------------------------ fields */
+
+/* Device bytes needed for one field of this context's local volume in `prec`
+ * (internal stored representation; 256-byte aligned allocation unit). */
+size_t coarse_field_bytes(const cd_context *ctx, cd_precision prec);
+
+/* Create a field.  device_mem == NULL: the library allocates (cudaMalloc) and frees it.
+ * Else device_mem (>= 256-byte aligned, >= coarse_field_bytes) is caller-owned and must
+ * outlive the field.  Contents are undefined until imported / generated / computed. */
+int coarse_field_alloc(cd_context *ctx, cd_precision prec, void *device_mem, size_t bytes, cd_field **out);
+
+/* Free a field handle (and its memory iff library-owned). */
+int coarse_field_free(cd_field *f);
+
+/* Import the canonical LOCAL vector v[s][i] (V_local * N complex of `dtype`) from host
+ * (src_on_device = 0; pinned memory gives an asynchronous copy) or device memory.
+ * fp16 fields quantise per site (R12).  stream-ordered. */
+int coarse_field_import(cd_field *f, const void *src, int src_on_device, cd_host_dtype dtype, void *stream);
+
+/* Export the field as a canonical LOCAL vector (fp16: dequantised x = float(q) * s). */
+int coarse_field_export(const cd_field *f, void *dst, int dst_on_device, cd_host_dtype dtype, void *stream);
+
+/* Fill with the synthetic vector of seed/tag over GLOBAL site indices,
+ * values scaled by 2^scale_log2.  fp16 fields are quantised as by import. */
+int coarse_field_generate(cd_field *f, uint64_t seed, uint32_t tag, int32_t scale_log2, void *stream);
+
+/* Raw stored representation, for bit-exact layout checks: canonical-order payload
+ * (V * N complex of float (fp32) or binary16 (fp16)) followed, for fp16, by V float
+ * scales.  *_stored_bytes gives the size.  read copies to host or device memory. */
+size_t coarse_field_stored_bytes(const cd_field *f);
+int coarse_field_read_stored(const cd_field *f, void *dst, int dst_on_device, void *stream);
+
+/* ------------------------------------------------------------------ links */
+
+/* Upload the canonical LOCAL link block L[s][k][i][j] (V_local * 9 * N * N complex of
+ * `dtype`) from host or device memory into a new, immutable links object in `prec`
+ * (fp16: quantised per (s, k) matrix, R12).  Host sources are staged through
+ * a bounded device buffer; the call returns when the source has been consumed. */
+int coarse_links_upload(cd_context *ctx, cd_precision prec, const void *links, int src_on_device,
+                        cd_host_dtype dtype, void *stream, cd_links **out);
+
+/* Generate a synthetic links object on the device (recipe `kind`, GLOBAL indices, so the
+ * operator is the same for every partition), values scaled by 2^scale_log2. */
+int coarse_links_generate(cd_context *ctx, cd_precision prec, int kind, uint64_t seed, int32_t scale_log2,
+                          void *stream, cd_links **out);
+
+/* Raw stored links: canonical payload (V*9*N*N complex float / binary16) then, for fp16,
+ * V*9 float scales. */
+size_t coarse_links_stored_bytes(const cd_links *l);
+int coarse_links_read_stored(const cd_links *l, void *dst, int dst_on_device, void *stream);
+
+int coarse_links_free(cd_links *l);
+
+/* ------------------------------------------------------------------ operator */
+
+/* out = D in  (Eq. 3).  in, out, links: same context and precision (else CD_ERR_MISMATCH);
+ * out must not alias in (CD_ERR_INVALID).  Collective for nranks > 1 (halo exchange of
+ * `in` over NCCL, overlapped with the interior).  The first call for a key autotunes
+ * (several trial launches on `stream`, excluded from any timing). */
+int coarse_dslash_apply(const cd_links *links, cd_field *out, const cd_field *in, void *stream);
+
+/* out = tau3 D tau3 in  (= D^H in for tau3-hermitian links; R5). */
+int coarse_dslash_apply_dagger(const cd_links *links, cd_field *out, const cd_field *in, void *stream);
+
+/* Halo send buffer of `in` in the canonical wire order (R13): packs on `stream`
+ * and copies to dst (host or device).  *bytes receives the size; dst may be NULL to query. */
+int coarse_halo_pack(cd_context *ctx, const cd_field *in, void *dst, int dst_on_device, size_t *bytes,
+                     void *stream);
+
+/* Write the L2-flush scratch (bench utility): a kernel writing `bytes` of device memory. */
+int cd_flush_l2(cd_context *ctx, size_t bytes, void *stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* COARSE_DSLASH_H */

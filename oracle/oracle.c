@@ -211,7 +211,8 @@ void oracle_dense(const int L[4], int N, const double *links_, double *D_)
  * +mu neighbour (local x_mu = Lloc_mu - 1), then block B = the face sent to the -mu
  * neighbour (x_mu = 0).  Inside a face, sites are lexicographic over the other three
  * coordinates, lowest mu fastest.  Each block holds the site records (rec_bytes each)
- * followed, if scales != NULL, by that block's per-site scales (scale_bytes each).
+ * followed, if scales != NULL, by that block's per-site scales (scale_bytes each); every
+ * block is zero-padded to a multiple of 16 bytes (so 128-bit loads of any block are aligned).
  * Returns the number of bytes written (out may be NULL to query the size). */
 size_t oracle_pack_halo(const int Lloc[4], const int split[4], const void *payload, size_t rec_bytes,
                         const void *scales, size_t scale_bytes, void *out)
@@ -242,6 +243,10 @@ size_t oracle_pack_halo(const int Lloc[4], const int split[4], const void *paylo
                     if (o) memcpy(o + off, src + (size_t)s * rb, rb);
                     off += rb;
                 }
+            }
+            while (off % 16) {
+                if (o) o[off] = 0;
+                off++;
             }
         }
     }

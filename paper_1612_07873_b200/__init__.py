@@ -1,0 +1,371 @@
+"""B200-native coarse-grid Dirac operator (arXiv:1612.07873) -- Python binding.
+
+A thin ctypes layer over the C ABI in ``include/coarse_dslash.h`` (library
+``libcoarse_dslash.so``, built in-tree by ``paper_1612_07873_b200.build``).  Every step of
+the operator runs in the library's sm_100a kernels; this module only marshals arguments.
+PyTorch, when used, supplies device memory (``torch.empty(..., device="cuda")``), streams
+(``torch.cuda.current_stream().cuda_stream``) and process groups (NCCL-id broadcast).
+
+There is no CPU fallback: if the library is missing this import fails loudly.
+
+Function names mirror the C ABI (``coarse_field_alloc``, ``coarse_links_upload``,
+``coarse_dslash_apply``, ``coarse_dslash_apply_dagger``, ...); the classes ``Context``,
+``Field`` and ``Links`` are conveniences over them.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcoarse_dslash.so")
+
+CD_OK, CD_ERR_INVALID, CD_ERR_UNSUPPORTED, CD_ERR_OOM, CD_ERR_CUDA, CD_ERR_NCCL, CD_ERR_MISMATCH = 0, -1, -2, -3, -4, -5, -6
+CD_FP32, CD_FP16 = 0, 1
+CD_C64, CD_C128 = 0, 1
+CD_LINKS_GENERAL, CD_LINKS_HERMITIAN, CD_LINKS_TI_GENERAL, CD_LINKS_TI_HERMITIAN = 0, 1, 2, 3
+CD_OPT_VARIANT, CD_OPT_TUNE, CD_OPT_HALO_SELF_MASK, CD_OPT_PDL = 0, 1, 2, 3
+
+PREC = {"fp32": CD_FP32, "fp16": CD_FP16, CD_FP32: CD_FP32, CD_FP16: CD_FP16}
+LINK_KIND = {"general": 0, "hermitian": 1, "ti_general": 2, "ti_hermitian": 3}
+
+# Every symbol include/coarse_dslash.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "cd_version", "cd_last_error", "cd_get_unique_id", "cd_context_create", "cd_context_destroy",
+    "cd_context_set_option", "cd_context_local", "cd_variant_count", "cd_variant_name",
+    "cd_context_chosen_variant", "cd_launch_count", "coarse_field_bytes", "coarse_field_alloc",
+    "coarse_field_free", "coarse_field_import", "coarse_field_export", "coarse_field_generate",
+    "coarse_field_stored_bytes", "coarse_field_read_stored", "coarse_links_upload", "coarse_links_generate",
+    "coarse_links_stored_bytes", "coarse_links_read_stored", "coarse_links_free", "coarse_dslash_apply",
+    "coarse_dslash_apply_dagger", "coarse_halo_pack", "cd_flush_l2",
+)
+
+
+class CDError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[cd status {code}] {msg}")
+        self.code = code
+
+
+class _Geometry(ctypes.Structure):
+    _fields_ = [("global_dims", ctypes.c_int32 * 4), ("nvec", ctypes.c_int32), ("proc_grid", ctypes.c_int32 * 4)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1612_07873_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I, I64, SZ, U64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_size_t, ctypes.c_uint64
+    PP = ctypes.POINTER(ctypes.c_void_p)
+    sig = {
+        "cd_version": ([], ctypes.c_char_p),
+        "cd_last_error": ([], ctypes.c_char_p),
+        "cd_get_unique_id": ([P], I),
+        "cd_context_create": ([ctypes.POINTER(_Geometry), I, I, I, P, PP], I),
+        "cd_context_destroy": ([P], I),
+        "cd_context_set_option": ([P, I, I64], I),
+        "cd_context_local": ([P, P, P, P], I),
+        "cd_variant_count": ([P, I], I),
+        "cd_variant_name": ([P, I, I], ctypes.c_char_p),
+        "cd_context_chosen_variant": ([P, I, I], I),
+        "cd_launch_count": ([], U64),
+        "coarse_field_bytes": ([P, I], SZ),
+        "coarse_field_alloc": ([P, I, P, SZ, PP], I),
+        "coarse_field_free": ([P], I),
+        "coarse_field_import": ([P, P, I, I, P], I),
+        "coarse_field_export": ([P, P, I, I, P], I),
+        "coarse_field_generate": ([P, U64, ctypes.c_uint32, ctypes.c_int32, P], I),
+        "coarse_field_stored_bytes": ([P], SZ),
+        "coarse_field_read_stored": ([P, P, I, P], I),
+        "coarse_links_upload": ([P, I, P, I, I, P, PP], I),
+        "coarse_links_generate": ([P, I, I, U64, ctypes.c_int32, P, PP], I),
+        "coarse_links_stored_bytes": ([P], SZ),
+        "coarse_links_read_stored": ([P, P, I, P], I),
+        "coarse_links_free": ([P], I),
+        "coarse_dslash_apply": ([P, P, P, P], I),
+        "coarse_dslash_apply_dagger": ([P, P, P, P], I),
+        "coarse_halo_pack": ([P, P, P, I, ctypes.POINTER(SZ), P], I),
+        "cd_flush_l2": ([P, SZ, P], I),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    return lib
+
+
+lib = _load()
+
+
+def _check(rc):
+    if rc != CD_OK:
+        raise CDError(rc, lib.cd_last_error().decode())
+    return rc
+
+
+def default_stream():
+    """The current torch CUDA stream handle (0 = legacy default stream if torch is unusable)."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.cuda.current_stream().cuda_stream
+    except Exception:
+        pass
+    return 0
+
+
+def _stream(s):
+    if s is None:
+        return ctypes.c_void_p(default_stream())
+    if hasattr(s, "cuda_stream"):
+        return ctypes.c_void_p(s.cuda_stream)
+    return ctypes.c_void_p(int(s))
+
+
+def _ptr(x):
+    """(pointer, on_device, keepalive) for numpy arrays, torch tensors or raw ints."""
+    if isinstance(x, np.ndarray):
+        if not x.flags.c_contiguous:
+            raise ValueError("array must be C-contiguous")
+        return x.ctypes.data, 0, x
+    try:
+        import torch
+        if isinstance(x, torch.Tensor):
+            if not x.is_contiguous():
+                raise ValueError("tensor must be contiguous")
+            return x.data_ptr(), 1 if x.is_cuda else 0, x
+    except ImportError:
+        pass
+    return int(x), 1, None
+
+
+# ------------------------------------------------------------------ C-ABI-named functions
+def cd_version() -> str:
+    return lib.cd_version().decode()
+
+
+def cd_launch_count() -> int:
+    return int(lib.cd_launch_count())
+
+
+def cd_get_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib.cd_get_unique_id(buf))
+    return bytes(buf)
+
+
+def cd_context_create(global_dims, nvec, proc_grid=(1, 1, 1, 1), device=0, nranks=1, rank=0, nccl_id=None):
+    g = _Geometry((ctypes.c_int32 * 4)(*global_dims), nvec, (ctypes.c_int32 * 4)(*proc_grid))
+    out = ctypes.c_void_p()
+    idb = None if nccl_id is None else (ctypes.c_uint8 * 128)(*nccl_id)
+    _check(lib.cd_context_create(ctypes.byref(g), device, nranks, rank, idb, ctypes.byref(out)))
+    return out
+
+
+def coarse_field_alloc(ctx, prec, device_mem=None, nbytes=0):
+    out = ctypes.c_void_p()
+    _check(lib.coarse_field_alloc(ctx, PREC[prec], device_mem, nbytes, ctypes.byref(out)))
+    return out
+
+
+def coarse_links_upload(ctx, prec, links, stream=None):
+    """links: canonical LOCAL [V, 9, N, N] complex128/complex64 (numpy or torch)."""
+    p, dev, keep = _ptr(links)
+    out = ctypes.c_void_p()
+    _check(lib.coarse_links_upload(ctx, PREC[prec], p, dev, CD_C128 if _is_c128(links) else CD_C64,
+                                   _stream(stream), ctypes.byref(out)))
+    del keep
+    return out
+
+
+def _is_c128(x):
+    if isinstance(x, np.ndarray):
+        if x.dtype == np.complex128:
+            return True
+        if x.dtype == np.complex64:
+            return False
+        raise TypeError(f"expected complex64/complex128, got {x.dtype}")
+    import torch
+    if x.dtype == torch.complex128:
+        return True
+    if x.dtype == torch.complex64:
+        return False
+    raise TypeError(f"expected complex64/complex128, got {x.dtype}")
+
+
+def coarse_links_generate(ctx, prec, kind="general", seed=0x1612, scale_log2=0, stream=None):
+    out = ctypes.c_void_p()
+    k = LINK_KIND[kind] if isinstance(kind, str) else int(kind)
+    _check(lib.coarse_links_generate(ctx, PREC[prec], k, seed, scale_log2, _stream(stream), ctypes.byref(out)))
+    return out
+
+
+def coarse_dslash_apply(links, out, in_, stream=None):
+    _check(lib.coarse_dslash_apply(links, out, in_, _stream(stream)))
+
+
+def coarse_dslash_apply_dagger(links, out, in_, stream=None):
+    _check(lib.coarse_dslash_apply_dagger(links, out, in_, _stream(stream)))
+
+
+# ------------------------------------------------------------------ classes
+class Context:
+    """A lattice geometry on one GPU (one rank of a process grid)."""
+
+    def __init__(self, global_dims, nvec, proc_grid=(1, 1, 1, 1), device=0, nranks=1, rank=0, nccl_id=None):
+        self.global_dims = tuple(int(x) for x in global_dims)
+        self.nvec = int(nvec)
+        self.N = 2 * self.nvec
+        self.proc_grid = tuple(int(x) for x in proc_grid)
+        self.handle = cd_context_create(self.global_dims, self.nvec, self.proc_grid, device, nranks, rank, nccl_id)
+        ld = (ctypes.c_int32 * 4)()
+        gc = (ctypes.c_int32 * 4)()
+        vol = ctypes.c_int64()
+        _check(lib.cd_context_local(self.handle, ld, ctypes.byref(vol), gc))
+        self.local_dims = tuple(ld)
+        self.grid_coords = tuple(gc)
+        self.V = int(vol.value)
+        self._objs = []
+
+    def set_option(self, option, value):
+        _check(lib.cd_context_set_option(self.handle, option, int(value)))
+
+    def variants(self, prec):
+        p = PREC[prec]
+        return [lib.cd_variant_name(self.handle, p, i).decode() for i in range(lib.cd_variant_count(self.handle, p))]
+
+    def chosen_variant(self, prec, dagger=False):
+        return lib.cd_context_chosen_variant(self.handle, PREC[prec], int(bool(dagger)))
+
+    def field(self, prec="fp32", torch_memory=True):
+        return Field(self, prec, torch_memory)
+
+    def links_upload(self, links, prec="fp32", stream=None):
+        return Links(self, prec, coarse_links_upload(self.handle, prec, np.ascontiguousarray(links)
+                                                     if isinstance(links, np.ndarray) else links, stream))
+
+    def links_generate(self, prec="fp32", kind="general", seed=0x1612, scale_log2=0, stream=None):
+        return Links(self, prec, coarse_links_generate(self.handle, prec, kind, seed, scale_log2, stream))
+
+    def halo_pack(self, field, stream=None) -> bytes:
+        n = ctypes.c_size_t()
+        _check(lib.coarse_halo_pack(self.handle, field.handle, None, 0, ctypes.byref(n), _stream(stream)))
+        buf = np.zeros(max(n.value, 1), np.uint8)
+        if n.value:
+            _check(lib.coarse_halo_pack(self.handle, field.handle, buf.ctypes.data, 0, ctypes.byref(n),
+                                        _stream(stream)))
+        return buf[:n.value].tobytes()
+
+    def flush_l2(self, nbytes=512 << 20, stream=None):
+        _check(lib.cd_flush_l2(self.handle, nbytes, _stream(stream)))
+
+    def close(self):
+        if self.handle:
+            _check(lib.cd_context_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Field:
+    """A colour-spinor field in the library's stored layout (device memory from torch)."""
+
+    def __init__(self, ctx: Context, prec="fp32", torch_memory=True):
+        self.ctx = ctx
+        self.prec = PREC[prec]
+        self.nbytes = int(lib.coarse_field_bytes(ctx.handle, self.prec))
+        self._mem = None
+        if torch_memory:
+            import torch
+            self._mem = torch.empty(self.nbytes, dtype=torch.uint8, device="cuda")
+            self.handle = coarse_field_alloc(ctx.handle, self.prec, self._mem.data_ptr(), self.nbytes)
+        else:
+            self.handle = coarse_field_alloc(ctx.handle, self.prec)
+
+    def import_(self, v, stream=None):
+        """v: canonical LOCAL [V, N] complex64/complex128 (numpy host or torch host/device)."""
+        p, dev, keep = _ptr(v)
+        _check(lib.coarse_field_import(self.handle, p, dev, CD_C128 if _is_c128(v) else CD_C64, _stream(stream)))
+        return keep
+
+    def export(self, dst=None, dtype=np.complex128, stream=None, sync=True):
+        if dst is None:
+            dst = np.empty((self.ctx.V, self.ctx.N), dtype)
+        p, dev, _ = _ptr(dst)
+        _check(lib.coarse_field_export(self.handle, p, dev, CD_C128 if _is_c128(dst) else CD_C64, _stream(stream)))
+        if sync:
+            _sync(stream)
+        return dst
+
+    def generate(self, seed=0x7873, tag=2, scale_log2=0, stream=None):
+        _check(lib.coarse_field_generate(self.handle, seed, tag, scale_log2, _stream(stream)))
+
+    def read_stored(self, stream=None) -> bytes:
+        n = int(lib.coarse_field_stored_bytes(self.handle))
+        buf = np.empty(n, np.uint8)
+        _check(lib.coarse_field_read_stored(self.handle, buf.ctypes.data, 0, _stream(stream)))
+        return buf.tobytes()
+
+    def close(self):
+        if self.handle:
+            _check(lib.coarse_field_free(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Links:
+    """An immutable link set (9 matrices per site) in the library's stored layout."""
+
+    def __init__(self, ctx: Context, prec, handle):
+        self.ctx = ctx
+        self.prec = PREC[prec]
+        self.handle = handle
+
+    def apply(self, out: Field, in_: Field, stream=None):
+        coarse_dslash_apply(self.handle, out.handle, in_.handle, stream)
+
+    def apply_dagger(self, out: Field, in_: Field, stream=None):
+        coarse_dslash_apply_dagger(self.handle, out.handle, in_.handle, stream)
+
+    def read_stored(self, stream=None) -> bytes:
+        n = int(lib.coarse_links_stored_bytes(self.handle))
+        buf = np.empty(n, np.uint8)
+        _check(lib.coarse_links_read_stored(self.handle, buf.ctypes.data, 0, _stream(stream)))
+        return buf.tobytes()
+
+    def close(self):
+        if self.handle:
+            _check(lib.coarse_links_free(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _sync(stream=None):
+    try:
+        import torch
+        if torch.cuda.is_available():
+            if stream is None:
+                torch.cuda.current_stream().synchronize()
+            elif hasattr(stream, "synchronize"):
+                stream.synchronize()
+            else:
+                torch.cuda.synchronize()
+    except ImportError:
+        pass

@@ -1,0 +1,884 @@
+// api.cpp -- C ABI of the coarse-Dslash library (include/coarse_dslash.h): argument
+// validation, object lifetimes, halo layout, autotuning + tune cache, apply dispatch.
+//
+// Every entry point catches everything: no C++ exception crosses the ABI; failures return a
+// cd_status and set a thread-local message (cd_last_error).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "cd_internal.h"
+#include "comm.h"
+
+namespace cd {
+cudaError_t launch_dslash_f32_24(int, const ApplyArgs &, cudaStream_t, bool, int);
+cudaError_t launch_dslash_f32_32(int, const ApplyArgs &, cudaStream_t, bool, int);
+cudaError_t launch_dslash_f16_24(int, const ApplyArgs &, cudaStream_t, bool, int);
+cudaError_t launch_dslash_f16_32(int, const ApplyArgs &, cudaStream_t, bool, int);
+cudaError_t launch_halo_f32_24(const ApplyArgs &, cudaStream_t);
+cudaError_t launch_halo_f32_32(const ApplyArgs &, cudaStream_t);
+cudaError_t launch_halo_f16_24(const ApplyArgs &, cudaStream_t);
+cudaError_t launch_halo_f16_32(const ApplyArgs &, cudaStream_t);
+cudaError_t launch_pack_f32_24(const void *, void *, const KGeom &, cudaStream_t);
+cudaError_t launch_pack_f32_32(const void *, void *, const KGeom &, cudaStream_t);
+cudaError_t launch_pack_f16_24(const void *, void *, const KGeom &, cudaStream_t);
+cudaError_t launch_pack_f16_32(const void *, void *, const KGeom &, cudaStream_t);
+int variant_count_f32_24();
+int variant_count_f32_32();
+int variant_count_f16_24();
+int variant_count_f16_32();
+const char *variant_name_f32_24(int);
+const char *variant_name_f32_32(int);
+const char *variant_name_f16_24(int);
+const char *variant_name_f16_32(int);
+int variant_kind_f32_24(int, int *, int *);
+int variant_kind_f32_32(int, int *, int *);
+int variant_kind_f16_24(int, int *, int *);
+int variant_kind_f16_32(int, int *, int *);
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch(int n) { g_launches += (uint64_t)n; }
+
+#define PICK(p, nv, f32_24, f32_32, f16_24, f16_32) \
+    ((p) == CD_FP32 ? ((nv) == 24 ? (f32_24) : (f32_32)) : ((nv) == 24 ? (f16_24) : (f16_32)))
+
+int variant_count(cd_precision p, int nv)
+{
+    return PICK(p, nv, variant_count_f32_24(), variant_count_f32_32(), variant_count_f16_24(), variant_count_f16_32());
+}
+const char *variant_name(cd_precision p, int nv, int id)
+{
+    return PICK(p, nv, variant_name_f32_24(id), variant_name_f32_32(id), variant_name_f16_24(id),
+                variant_name_f16_32(id));
+}
+static int variant_kind(cd_precision p, int nv, int id, int *kw, int *wr)
+{
+    return PICK(p, nv, variant_kind_f32_24(id, kw, wr), variant_kind_f32_32(id, kw, wr),
+                variant_kind_f16_24(id, kw, wr), variant_kind_f16_32(id, kw, wr));
+}
+bool variant_valid(cd_precision p, int nv, int id, const KGeom &) { return id >= 0 && id < variant_count(p, nv); }
+
+// Heuristic when tuning is off (or the stream is being captured before a key was tuned):
+// the persistent TMA ring once there are several sites per SM, else the fine-grained kernel
+// with the most CTAs per site that still keeps warps busy.
+int variant_heuristic(cd_precision p, int nv, const KGeom &g, int num_sms)
+{
+    if (g.V >= 4 * num_sms) return 0;
+    int best = -1, best_score = -1;
+    for (int id = 0; id < variant_count(p, nv); id++) {
+        int kw = 0, wr = 0;
+        if (variant_kind(p, nv, id, &kw, &wr) != 1) continue;
+        const int R = (p == CD_FP32) ? 4 : 8;
+        const int nrb = 2 * nv / (wr * R);
+        const int64_t ctas = (int64_t)g.V * nrb;
+        // prefer >= 2 CTAs per SM, then fewer hops per warp (shorter dependent chains)
+        const int score = (ctas >= 2 * num_sms ? 1000 : (int)(ctas * 500 / (2 * num_sms))) - kw * 10 + wr;
+        if (score > best_score) best_score = score, best = id;
+    }
+    return best < 0 ? 0 : best;
+}
+
+cudaError_t launch_dslash(cd_precision p, int id, const ApplyArgs &a, cudaStream_t s, bool pdl, int sms)
+{
+    return PICK(p, a.nvec, launch_dslash_f32_24(id, a, s, pdl, sms), launch_dslash_f32_32(id, a, s, pdl, sms),
+                launch_dslash_f16_24(id, a, s, pdl, sms), launch_dslash_f16_32(id, a, s, pdl, sms));
+}
+cudaError_t launch_halo(cd_precision p, const ApplyArgs &a, cudaStream_t s)
+{
+    return PICK(p, a.nvec, launch_halo_f32_24(a, s), launch_halo_f32_32(a, s), launch_halo_f16_24(a, s),
+                launch_halo_f16_32(a, s));
+}
+cudaError_t launch_pack(cd_precision p, int nv, const void *f, void *d, const KGeom &g, cudaStream_t s)
+{
+    return PICK(p, nv, launch_pack_f32_24(f, d, g, s), launch_pack_f32_32(f, d, g, s), launch_pack_f16_24(f, d, g, s),
+                launch_pack_f16_32(f, d, g, s));
+}
+
+}  // namespace cd
+
+using namespace cd;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string t_err;
+
+static int fail(int code, const std::string &msg)
+{
+    t_err = msg;
+    return code;
+}
+static int cuda_fail(cudaError_t e, const char *what)
+{
+    return fail(CD_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CUDA_TRY(expr, what)                         \
+    do {                                             \
+        cudaError_t e_ = (expr);                     \
+        if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+    } while (0)
+
+#define API_BEGIN try {
+#define API_END                                                          \
+    }                                                                    \
+    catch (const std::exception &ex) { return fail(CD_ERR_INVALID, ex.what()); } \
+    catch (...) { return fail(CD_ERR_INVALID, "unknown C++ exception"); }
+
+static cudaStream_t S(void *s) { return static_cast<cudaStream_t>(s); }
+
+// ------------------------------------------------------------------ halo layout
+// Wire order (R13): split dims ascending; per dim block A (face sent to +mu, x_mu =
+// L-1) then block B (face sent to -mu, x_mu = 0); each block = F payload records then
+// (fp16) F float scales.
+static KGeom halo_geom(const cd_context *c, cd_precision p)
+{
+    KGeom g = c->kg;
+    const size_t prec_rec = (p == CD_FP32) ? 8 * (size_t)c->N : 4 * (size_t)c->N;
+    const size_t sc = (p == CD_FP32) ? 0 : 4;
+    int64_t off = 0;
+    for (int mu = 0; mu < 4; mu++) {
+        g.F[mu] = (int)(c->V / c->local[mu]);
+        if (!((g.split >> mu) & 1)) {
+            g.blk_off[mu][0] = g.blk_off[mu][1] = 0;
+            continue;
+        }
+        for (int b = 0; b < 2; b++) {
+            g.blk_off[mu][b] = off;
+            off += (int64_t)g.F[mu] * (prec_rec + sc);
+            off = (off + 15) & ~int64_t(15);
+        }
+    }
+    return g;
+}
+static size_t halo_bytes(const cd_context *c, cd_precision p)
+{
+    KGeom g = halo_geom(c, p);
+    size_t mx = 0;
+    const size_t prec_rec = (p == CD_FP32) ? 8 * (size_t)c->N : 4 * (size_t)c->N;
+    const size_t sc = (p == CD_FP32) ? 0 : 4;
+    for (int mu = 0; mu < 4; mu++)
+        if ((g.split >> mu) & 1) mx = std::max(mx, (size_t)g.blk_off[mu][1] + (((size_t)g.F[mu] * (prec_rec + sc) + 15) & ~size_t(15)));
+    return mx;
+}
+
+static int setup_halo(cd_context *c)
+{
+    if (c->halo_ready || c->kg.split == 0) return CD_OK;
+    CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
+    const size_t cap = align256(std::max(halo_bytes(c, CD_FP32), halo_bytes(c, CD_FP16)) + 16);
+    CUDA_TRY(cudaMalloc(&c->send_buf, cap), "cudaMalloc(send)");
+    CUDA_TRY(cudaMalloc(&c->recv_buf, cap), "cudaMalloc(recv)");
+    CUDA_TRY(cudaMemset(c->send_buf, 0, cap), "memset");
+    CUDA_TRY(cudaMemset(c->recv_buf, 0, cap), "memset");
+    c->halo_cap = cap;
+    CUDA_TRY(cudaMalloc(&c->face_scratch, sizeof(float2) * c->V * c->N), "cudaMalloc(scratch)");
+    std::vector<int> faces;
+    for (int64_t s = 0; s < c->V; s++) {
+        int64_t t = s;
+        int x[4];
+        for (int mu = 0; mu < 4; mu++) {
+            x[mu] = (int)(t % c->local[mu]);
+            t /= c->local[mu];
+        }
+        bool face = false;
+        for (int mu = 0; mu < 4; mu++)
+            if (((c->kg.split >> mu) & 1) && (x[mu] == 0 || x[mu] == c->local[mu] - 1)) face = true;
+        if (face) faces.push_back((int)s);
+    }
+    c->n_face = (int)faces.size();
+    CUDA_TRY(cudaMalloc(&c->face_sites, sizeof(int) * std::max<size_t>(1, faces.size())), "cudaMalloc(faces)");
+    if (!faces.empty())
+        CUDA_TRY(cudaMemcpy(c->face_sites, faces.data(), sizeof(int) * faces.size(), cudaMemcpyHostToDevice),
+                 "cudaMemcpy(faces)");
+    if (!c->comm_stream) CUDA_TRY(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking), "stream");
+    if (!c->ev_in) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming), "event");
+    if (!c->ev_halo) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming), "event");
+    c->halo_ready = true;
+    return CD_OK;
+}
+
+// ------------------------------------------------------------------ tune cache (file)
+static std::string tune_key_str(const cd_context *c, int prec, int dag)
+{
+    std::ostringstream o;
+    o << "v1 nvec=" << c->nvec << " prec=" << prec << " dag=" << dag << " L=" << c->local[0] << "," << c->local[1]
+      << "," << c->local[2] << "," << c->local[3] << " split=" << c->kg.split << " sms=" << c->num_sms;
+    return o.str();
+}
+static std::mutex g_tune_mu;
+static int tune_file_lookup(const std::string &key)
+{
+    const char *path = getenv("CD_TUNE_CACHE");
+    if (!path || !*path) return -1;
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    std::ifstream f(path);
+    std::string line;
+    int found = -1;
+    while (std::getline(f, line)) {
+        const size_t bar = line.find(" | ");
+        if (bar != std::string::npos && line.substr(0, bar) == key) found = atoi(line.c_str() + bar + 3);
+    }
+    return found;
+}
+static void tune_file_store(const std::string &key, int id, const char *name, float us)
+{
+    const char *path = getenv("CD_TUNE_CACHE");
+    if (!path || !*path) return;
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    std::ofstream f(path, std::ios::app);
+    f << key << " | " << id << " | " << (name ? name : "?") << " | " << us << " us\n";
+}
+
+// ------------------------------------------------------------------ context
+extern "C" {
+
+const char *cd_version(void) { return "coarse_dslash 0.1 (sm_100a)"; }
+const char *cd_last_error(void) { return t_err.c_str(); }
+uint64_t cd_launch_count(void) { return g_launches.load(); }
+
+int cd_get_unique_id(uint8_t out_id[128])
+{
+    API_BEGIN
+    if (!out_id) return fail(CD_ERR_INVALID, "out_id is NULL");
+    std::string err;
+    int r = nccl_unique_id(out_id, err);
+    if (r != CD_OK) return fail(r, err);
+    return CD_OK;
+    API_END
+}
+
+int cd_context_create(const cd_geometry *geom, int device, int nranks, int rank, const uint8_t *nccl_id,
+                      cd_context **out)
+{
+    API_BEGIN
+    if (!geom || !out) return fail(CD_ERR_INVALID, "geom/out is NULL");
+    *out = nullptr;
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(CD_ERR_INVALID, "bad nranks/rank");
+    if ((nranks > 1) != (nccl_id != nullptr)) return fail(CD_ERR_INVALID, "nccl_id must be given iff nranks > 1");
+    int64_t prodP = 1;
+    for (int mu = 0; mu < 4; mu++) {
+        if (geom->global_dims[mu] < 1) return fail(CD_ERR_INVALID, "global_dims must be >= 1");
+        if (geom->proc_grid[mu] < 1) return fail(CD_ERR_INVALID, "proc_grid must be >= 1");
+        if (geom->global_dims[mu] % geom->proc_grid[mu]) return fail(CD_ERR_INVALID, "global_dims % proc_grid != 0");
+        prodP *= geom->proc_grid[mu];
+    }
+    if (prodP != nranks) return fail(CD_ERR_INVALID, "prod(proc_grid) != nranks");
+    if (geom->nvec != 24 && geom->nvec != 32) return fail(CD_ERR_UNSUPPORTED, "nvec must be 24 or 32");
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) return fail(CD_ERR_INVALID, "bad device");
+    CUDA_TRY(cudaSetDevice(device), "cudaSetDevice");
+
+    cd_context *c = new cd_context();
+    c->geom = *geom;
+    c->device = device;
+    c->nranks = nranks;
+    c->rank = rank;
+    c->nvec = geom->nvec;
+    c->N = 2 * geom->nvec;
+    int t = rank;
+    int64_t V = 1;
+    for (int mu = 0; mu < 4; mu++) {
+        c->coords[mu] = t % geom->proc_grid[mu];
+        t /= geom->proc_grid[mu];
+        c->local[mu] = geom->global_dims[mu] / geom->proc_grid[mu];
+        V *= c->local[mu];
+    }
+    if (V >= (int64_t(1) << 31) / 9) {
+        delete c;
+        return fail(CD_ERR_UNSUPPORTED, "local volume too large");
+    }
+    c->V = V;
+    for (int mu = 0; mu < 4; mu++) {
+        for (int dir = 0; dir < 2; dir++) {
+            int cc[4] = {c->coords[0], c->coords[1], c->coords[2], c->coords[3]};
+            const int P = geom->proc_grid[mu];
+            cc[mu] = (cc[mu] + (dir == 0 ? 1 : -1) + P) % P;
+            c->nbr_rank[mu][dir] = ((cc[3] * geom->proc_grid[2] + cc[2]) * geom->proc_grid[1] + cc[1]) *
+                                       geom->proc_grid[0] + cc[0];
+        }
+    }
+    KGeom &g = c->kg;
+    for (int mu = 0; mu < 4; mu++) g.L[mu] = c->local[mu];
+    g.V = (int)V;
+    for (int i = 0; i < 3; i++) g.fd[i] = make_fastdiv((uint32_t)c->local[i]);
+    g.split = 0;
+    for (int mu = 0; mu < 4; mu++)
+        if (geom->proc_grid[mu] > 1) g.split |= (1 << mu);
+    cudaDeviceProp prop;
+    cudaError_t e = cudaGetDeviceProperties(&prop, device);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_fail(e, "cudaGetDeviceProperties");
+    }
+    c->num_sms = prop.multiProcessorCount;
+    if (const char *ev = getenv("CD_TUNE")) c->tune = atoi(ev) ? 1 : 0;
+    if (const char *ev = getenv("CD_VARIANT")) c->force_variant = atoi(ev);
+    if (const char *ev = getenv("CD_PDL")) c->pdl = atoi(ev) ? 1 : 0;
+    if (nranks > 1) {
+        std::string err;
+        int r = comm_create(nccl_id, nranks, rank, &c->comm, err);
+        if (r != CD_OK) {
+            delete c;
+            return fail(r, err);
+        }
+    }
+    int r = setup_halo(c);
+    if (r != CD_OK) {
+        delete c;
+        return r;
+    }
+    *out = c;
+    return CD_OK;
+    API_END
+}
+
+int cd_context_destroy(cd_context *c)
+{
+    API_BEGIN
+    if (!c) return fail(CD_ERR_INVALID, "ctx is NULL");
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    if (c->send_buf) cudaFree(c->send_buf);
+    if (c->recv_buf) cudaFree(c->recv_buf);
+    if (c->face_scratch) cudaFree(c->face_scratch);
+    if (c->face_sites) cudaFree(c->face_sites);
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    if (c->ev_in) cudaEventDestroy(c->ev_in);
+    if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+    comm_destroy(c->comm);
+    delete c;
+    return CD_OK;
+    API_END
+}
+
+int cd_context_set_option(cd_context *c, int option, int64_t value)
+{
+    API_BEGIN
+    if (!c) return fail(CD_ERR_INVALID, "ctx is NULL");
+    std::lock_guard<std::mutex> lk(c->mu);
+    switch (option) {
+    case CD_OPT_VARIANT:
+        if (value < -1) return fail(CD_ERR_INVALID, "variant must be >= -1");
+        c->force_variant = (int)value;
+        return CD_OK;
+    case CD_OPT_TUNE:
+        c->tune = value ? 1 : 0;
+        return CD_OK;
+    case CD_OPT_PDL:
+        c->pdl = value ? 1 : 0;
+        return CD_OK;
+    case CD_OPT_HALO_SELF_MASK: {
+        if (value < 0 || value > 15) return fail(CD_ERR_INVALID, "mask must be in [0, 15]");
+        if (c->applied) return fail(CD_ERR_INVALID, "HALO_SELF_MASK must be set before the first apply");
+        for (int mu = 0; mu < 4; mu++)
+            if (((value >> mu) & 1) && c->geom.proc_grid[mu] != 1)
+                return fail(CD_ERR_INVALID, "HALO_SELF_MASK dims must have proc_grid == 1");
+        if (c->halo_ready) {
+            cudaFree(c->send_buf);
+            cudaFree(c->recv_buf);
+            cudaFree(c->face_scratch);
+            cudaFree(c->face_sites);
+            c->send_buf = c->recv_buf = nullptr;
+            c->face_scratch = nullptr;
+            c->face_sites = nullptr;
+            c->halo_ready = false;
+        }
+        c->halo_self_mask = (int)value;
+        int split = 0;
+        for (int mu = 0; mu < 4; mu++)
+            if (c->geom.proc_grid[mu] > 1) split |= (1 << mu);
+        c->kg.split = split | (int)value;
+        c->chosen.clear();
+        return setup_halo(c);
+    }
+    default:
+        return fail(CD_ERR_INVALID, "unknown option");
+    }
+    API_END
+}
+
+int cd_context_local(const cd_context *c, int32_t local_dims[4], int64_t *local_volume, int32_t grid_coords[4])
+{
+    if (!c) return fail(CD_ERR_INVALID, "ctx is NULL");
+    for (int mu = 0; mu < 4; mu++) {
+        if (local_dims) local_dims[mu] = c->local[mu];
+        if (grid_coords) grid_coords[mu] = c->coords[mu];
+    }
+    if (local_volume) *local_volume = c->V;
+    return CD_OK;
+}
+
+int cd_variant_count(const cd_context *c, cd_precision p)
+{
+    if (!c || (p != CD_FP32 && p != CD_FP16)) return 0;
+    return variant_count(p, c->nvec);
+}
+const char *cd_variant_name(const cd_context *c, cd_precision p, int id)
+{
+    if (!c || (p != CD_FP32 && p != CD_FP16)) return nullptr;
+    return variant_name(p, c->nvec, id);
+}
+int cd_context_chosen_variant(const cd_context *c, cd_precision p, int dagger)
+{
+    if (!c) return -1;
+    auto *cc = const_cast<cd_context *>(c);
+    std::lock_guard<std::mutex> lk(cc->mu);
+    auto it = c->chosen.find(TuneKey{(int)p, dagger ? 1 : 0});
+    return it == c->chosen.end() ? -1 : it->second;
+}
+
+// ------------------------------------------------------------------ fields
+size_t coarse_field_bytes(const cd_context *c, cd_precision p)
+{
+    if (!c || (p != CD_FP32 && p != CD_FP16)) return 0;
+    return align256(vec_rec_bytes(c->N, p) * (size_t)c->V);
+}
+
+int coarse_field_alloc(cd_context *c, cd_precision p, void *mem, size_t bytes, cd_field **out)
+{
+    API_BEGIN
+    if (!c || !out) return fail(CD_ERR_INVALID, "ctx/out is NULL");
+    if (p != CD_FP32 && p != CD_FP16) return fail(CD_ERR_INVALID, "bad precision");
+    const size_t need = coarse_field_bytes(c, p);
+    bool owned = false;
+    if (!mem) {
+        CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
+        cudaError_t e = cudaMalloc(&mem, need);
+        if (e != cudaSuccess) return fail(CD_ERR_OOM, std::string("cudaMalloc(field): ") + cudaGetErrorString(e));
+        bytes = need;
+        owned = true;
+    } else {
+        if (reinterpret_cast<uintptr_t>(mem) % 256) return fail(CD_ERR_INVALID, "device_mem must be 256-B aligned");
+        if (bytes < need) return fail(CD_ERR_INVALID, "device_mem too small (need coarse_field_bytes)");
+    }
+    *out = new cd_field{c, p, mem, bytes, owned};
+    return CD_OK;
+    API_END
+}
+
+int coarse_field_free(cd_field *f)
+{
+    API_BEGIN
+    if (!f) return fail(CD_ERR_INVALID, "field is NULL");
+    if (f->owned) cudaFree(f->base);
+    delete f;
+    return CD_OK;
+    API_END
+}
+
+// Bounded device staging for host <-> device transfers of canonical data.
+static int staged_h2d(void *dst_dev, const void *src_host, size_t bytes, cudaStream_t s)
+{
+    CUDA_TRY(cudaMemcpyAsync(dst_dev, src_host, bytes, cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(H2D)");
+    return CD_OK;
+}
+
+int coarse_field_import(cd_field *f, const void *src, int src_on_device, cd_host_dtype dt, void *stream)
+{
+    API_BEGIN
+    if (!f || !src) return fail(CD_ERR_INVALID, "field/src is NULL");
+    if (dt != CD_C64 && dt != CD_C128) return fail(CD_ERR_INVALID, "bad dtype");
+    cd_context *c = f->ctx;
+    const size_t elem = dt == CD_C128 ? 16 : 8;
+    const size_t bytes = elem * c->N * (size_t)c->V;
+    cudaStream_t s = S(stream);
+    if (f->prec == CD_FP32 && dt == CD_C64) {   // stored layout == canonical layout
+        CUDA_TRY(cudaMemcpyAsync(f->base, src, bytes, src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                 s), "cudaMemcpyAsync(import)");
+        return CD_OK;
+    }
+    const void *dsrc = src;
+    void *stage = nullptr;
+    if (!src_on_device) {
+        CUDA_TRY(cudaMallocAsync(&stage, bytes, s), "cudaMallocAsync(stage)");
+        int r = staged_h2d(stage, src, bytes, s);
+        if (r != CD_OK) return r;
+        dsrc = stage;
+    }
+    CUDA_TRY(launch_import(f->prec, c->nvec, c->V, dsrc, dt == CD_C128, f->base, s), "import kernel");
+    if (stage) CUDA_TRY(cudaFreeAsync(stage, s), "cudaFreeAsync");
+    return CD_OK;
+    API_END
+}
+
+int coarse_field_export(const cd_field *f, void *dst, int dst_on_device, cd_host_dtype dt, void *stream)
+{
+    API_BEGIN
+    if (!f || !dst) return fail(CD_ERR_INVALID, "field/dst is NULL");
+    if (dt != CD_C64 && dt != CD_C128) return fail(CD_ERR_INVALID, "bad dtype");
+    cd_context *c = f->ctx;
+    const size_t elem = dt == CD_C128 ? 16 : 8;
+    const size_t bytes = elem * c->N * (size_t)c->V;
+    cudaStream_t s = S(stream);
+    if (f->prec == CD_FP32 && dt == CD_C64) {
+        CUDA_TRY(cudaMemcpyAsync(dst, f->base, bytes, dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                 s), "cudaMemcpyAsync(export)");
+        return CD_OK;
+    }
+    void *ddst = dst;
+    void *stage = nullptr;
+    if (!dst_on_device) {
+        CUDA_TRY(cudaMallocAsync(&stage, bytes, s), "cudaMallocAsync(stage)");
+        ddst = stage;
+    }
+    CUDA_TRY(launch_export(f->prec, c->nvec, c->V, f->base, ddst, dt == CD_C128, s), "export kernel");
+    if (stage) {
+        CUDA_TRY(cudaMemcpyAsync(dst, stage, bytes, cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(D2H)");
+        CUDA_TRY(cudaFreeAsync(stage, s), "cudaFreeAsync");
+    }
+    return CD_OK;
+    API_END
+}
+
+int coarse_field_generate(cd_field *f, uint64_t seed, uint32_t tag, int32_t scale_log2, void *stream)
+{
+    API_BEGIN
+    if (!f) return fail(CD_ERR_INVALID, "field is NULL");
+    if (scale_log2 < -60 || scale_log2 > 60) return fail(CD_ERR_INVALID, "scale_log2 out of range");
+    CUDA_TRY(launch_field_generate(f->prec, f->ctx->nvec, f->ctx, seed, tag, scale_log2, f->base, S(stream)),
+             "field generate");
+    return CD_OK;
+    API_END
+}
+
+size_t coarse_field_stored_bytes(const cd_field *f)
+{
+    if (!f) return 0;
+    const size_t n = (size_t)f->ctx->V * f->ctx->N;
+    return f->prec == CD_FP32 ? 8 * n : 4 * n + 4 * (size_t)f->ctx->V;
+}
+
+// internal records -> canonical raw (payloads contiguous, then scales), via the host
+static int read_stored(const void *base, int64_t nrec, size_t payload, size_t rec, bool f16, void *dst,
+                       int dst_on_device, cudaStream_t s)
+{
+    std::vector<unsigned char> h(rec * nrec);
+    CUDA_TRY(cudaMemcpyAsync(h.data(), base, h.size(), cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(read)");
+    CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    std::vector<unsigned char> o(payload * nrec + (f16 ? 4 * nrec : 0));
+    for (int64_t r = 0; r < nrec; r++) {
+        memcpy(o.data() + payload * r, h.data() + rec * r, payload);
+        if (f16) memcpy(o.data() + payload * nrec + 4 * r, h.data() + rec * r + payload, 4);
+    }
+    if (dst_on_device) {
+        CUDA_TRY(cudaMemcpy(dst, o.data(), o.size(), cudaMemcpyHostToDevice), "cudaMemcpy(read)");
+    } else {
+        memcpy(dst, o.data(), o.size());
+    }
+    return CD_OK;
+}
+
+int coarse_field_read_stored(const cd_field *f, void *dst, int dst_on_device, void *stream)
+{
+    API_BEGIN
+    if (!f || !dst) return fail(CD_ERR_INVALID, "field/dst is NULL");
+    const int N = f->ctx->N;
+    const bool f16 = f->prec == CD_FP16;
+    return read_stored(f->base, f->ctx->V, f16 ? 4 * N : 8 * N, vec_rec_bytes(N, f->prec), f16, dst, dst_on_device,
+                       S(stream));
+    API_END
+}
+
+// ------------------------------------------------------------------ links
+static int links_new(cd_context *c, cd_precision p, cd_links **out)
+{
+    const size_t bytes = align256(mat_rec_bytes(c->N, p) * 9 * (size_t)c->V);
+    void *mem = nullptr;
+    CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
+    cudaError_t e = cudaMalloc(&mem, bytes);
+    if (e != cudaSuccess) return fail(CD_ERR_OOM, std::string("cudaMalloc(links): ") + cudaGetErrorString(e));
+    *out = new cd_links{c, p, mem, bytes};
+    return CD_OK;
+}
+
+int coarse_links_upload(cd_context *c, cd_precision p, const void *src, int src_on_device, cd_host_dtype dt,
+                        void *stream, cd_links **out)
+{
+    API_BEGIN
+    if (!c || !src || !out) return fail(CD_ERR_INVALID, "ctx/src/out is NULL");
+    if (p != CD_FP32 && p != CD_FP16) return fail(CD_ERR_INVALID, "bad precision");
+    if (dt != CD_C64 && dt != CD_C128) return fail(CD_ERR_INVALID, "bad dtype");
+    cd_links *l = nullptr;
+    int r = links_new(c, p, &l);
+    if (r != CD_OK) return r;
+    cudaStream_t s = S(stream);
+    const size_t elem = dt == CD_C128 ? 16 : 8;
+    const size_t mat_src = elem * c->N * c->N;
+    const int64_t nmats = 9 * c->V;
+    if (src_on_device) {
+        cudaError_t e = launch_links_convert(p, c->nvec, nmats, src, dt == CD_C128, l->base, s, 0);
+        if (e != cudaSuccess) {
+            cudaFree(l->base);
+            delete l;
+            return cuda_fail(e, "links convert");
+        }
+    } else {
+        // stage through a bounded device buffer (<= 64 MB of source per chunk)
+        const int64_t chunk = std::max<int64_t>(1, (int64_t)((64u << 20) / mat_src));
+        void *stage = nullptr;
+        cudaError_t e = cudaMalloc(&stage, (size_t)std::min<int64_t>(chunk, nmats) * mat_src);
+        if (e != cudaSuccess) {
+            cudaFree(l->base);
+            delete l;
+            return fail(CD_ERR_OOM, "cudaMalloc(stage)");
+        }
+        for (int64_t m0 = 0; m0 < nmats && e == cudaSuccess; m0 += chunk) {
+            const int64_t n = std::min(chunk, nmats - m0);
+            e = cudaMemcpyAsync(stage, static_cast<const unsigned char *>(src) + m0 * mat_src, n * mat_src,
+                                cudaMemcpyHostToDevice, s);
+            if (e == cudaSuccess) e = launch_links_convert(p, c->nvec, n, stage, dt == CD_C128, l->base, s, m0);
+        }
+        cudaError_t e2 = cudaStreamSynchronize(s);
+        cudaFree(stage);
+        if (e == cudaSuccess) e = e2;
+        if (e != cudaSuccess) {
+            cudaFree(l->base);
+            delete l;
+            return cuda_fail(e, "links upload");
+        }
+    }
+    *out = l;
+    return CD_OK;
+    API_END
+}
+
+int coarse_links_generate(cd_context *c, cd_precision p, int kind, uint64_t seed, int32_t scale_log2, void *stream,
+                          cd_links **out)
+{
+    API_BEGIN
+    if (!c || !out) return fail(CD_ERR_INVALID, "ctx/out is NULL");
+    if (p != CD_FP32 && p != CD_FP16) return fail(CD_ERR_INVALID, "bad precision");
+    if (kind < 0 || kind > 3) return fail(CD_ERR_INVALID, "bad links kind");
+    if (scale_log2 < -60 || scale_log2 > 60) return fail(CD_ERR_INVALID, "scale_log2 out of range");
+    cd_links *l = nullptr;
+    int r = links_new(c, p, &l);
+    if (r != CD_OK) return r;
+    cudaError_t e = launch_links_generate(p, c->nvec, c, kind, seed, scale_log2, l->base, S(stream));
+    if (e != cudaSuccess) {
+        cudaFree(l->base);
+        delete l;
+        return cuda_fail(e, "links generate");
+    }
+    *out = l;
+    return CD_OK;
+    API_END
+}
+
+size_t coarse_links_stored_bytes(const cd_links *l)
+{
+    if (!l) return 0;
+    const size_t nm = 9 * (size_t)l->ctx->V;
+    const size_t NN = (size_t)l->ctx->N * l->ctx->N;
+    return l->prec == CD_FP32 ? 8 * NN * nm : 4 * NN * nm + 4 * nm;
+}
+
+int coarse_links_read_stored(const cd_links *l, void *dst, int dst_on_device, void *stream)
+{
+    API_BEGIN
+    if (!l || !dst) return fail(CD_ERR_INVALID, "links/dst is NULL");
+    const size_t NN = (size_t)l->ctx->N * l->ctx->N;
+    const bool f16 = l->prec == CD_FP16;
+    return read_stored(l->base, 9 * l->ctx->V, f16 ? 4 * NN : 8 * NN, mat_rec_bytes(l->ctx->N, l->prec), f16, dst,
+                       dst_on_device, S(stream));
+    API_END
+}
+
+int coarse_links_free(cd_links *l)
+{
+    API_BEGIN
+    if (!l) return fail(CD_ERR_INVALID, "links is NULL");
+    cudaFree(l->base);
+    delete l;
+    return CD_OK;
+    API_END
+}
+
+// ------------------------------------------------------------------ apply
+static int check_objs(const cd_links *l, const cd_field *out, const cd_field *in)
+{
+    if (!l || !out || !in) return fail(CD_ERR_INVALID, "links/out/in is NULL");
+    if (l->ctx != out->ctx || l->ctx != in->ctx) return fail(CD_ERR_MISMATCH, "objects from different contexts");
+    if (l->prec != out->prec || l->prec != in->prec) return fail(CD_ERR_MISMATCH, "precision mismatch");
+    if (out->base == in->base) return fail(CD_ERR_INVALID, "out must not alias in");
+    const char *ob = static_cast<const char *>(out->base), *ib = static_cast<const char *>(in->base);
+    const size_t need = coarse_field_bytes(l->ctx, l->prec);
+    if (ob < ib + need && ib < ob + need) return fail(CD_ERR_INVALID, "out overlaps in");
+    return CD_OK;
+}
+
+// Pick the kernel variant for (prec, dagger): forced > cached > tuned > heuristic.
+// Tuning (first call of a key, "auto-tuned upon first call and cached") times
+// every variant with CUDA events on the caller's stream; trial launches write `out` only.
+static int resolve_variant(cd_context *c, cd_precision p, int dag, const ApplyArgs &a, cudaStream_t s, int *id)
+{
+    const int nvar = variant_count(p, c->nvec);
+    if (c->force_variant >= 0) {
+        if (c->force_variant >= nvar) return fail(CD_ERR_INVALID, "forced variant out of range for this precision");
+        *id = c->force_variant;
+        return CD_OK;
+    }
+    TuneKey key{(int)p, dag};
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        auto it = c->chosen.find(key);
+        if (it != c->chosen.end()) {
+            *id = it->second;
+            return CD_OK;
+        }
+    }
+    const std::string ks = tune_key_str(c, (int)p, dag);
+    int v = tune_file_lookup(ks);
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cap);
+    if (v < 0 || v >= nvar) {
+        v = variant_heuristic(p, c->nvec, a.g, c->num_sms);
+        if (c->tune && cap == cudaStreamCaptureStatusNone) {
+            cudaEvent_t e0, e1;
+            CUDA_TRY(cudaEventCreate(&e0), "event");
+            CUDA_TRY(cudaEventCreate(&e1), "event");
+            float best = 1e30f;
+            const int reps = c->V >= 2048 ? 3 : 20;
+            for (int id2 = 0; id2 < nvar; id2++) {
+                cudaError_t e = cudaSuccess;
+                for (int w = 0; w < 2 && e == cudaSuccess; w++) e = launch_dslash(p, id2, a, s, false, c->num_sms);
+                if (e != cudaSuccess) {
+                    cudaGetLastError();
+                    continue;
+                }
+                cudaEventRecord(e0, s);
+                for (int rr = 0; rr < reps && e == cudaSuccess; rr++) e = launch_dslash(p, id2, a, s, false, c->num_sms);
+                cudaEventRecord(e1, s);
+                if (e != cudaSuccess || cudaEventSynchronize(e1) != cudaSuccess) {
+                    cudaGetLastError();
+                    continue;
+                }
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, e0, e1);
+                ms /= reps;
+                if (ms < best) best = ms, v = id2;
+            }
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+            tune_file_store(ks, v, variant_name(p, c->nvec, v), best * 1000.f);
+        }
+    }
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->chosen[key] = v;
+    }
+    *id = v;
+    return CD_OK;
+}
+
+static int do_apply(const cd_links *l, cd_field *out, const cd_field *in, void *stream, int dag)
+{
+    int r = check_objs(l, out, in);
+    if (r != CD_OK) return r;
+    cd_context *c = l->ctx;
+    cudaStream_t s = S(stream);
+    c->applied = true;
+    if (c->comm) {
+        std::string err;
+        r = comm_check(c->comm, err);
+        if (r != CD_OK) return fail(r, err);
+    }
+    ApplyArgs a{};
+    a.links = l->base;
+    a.in = in->base;
+    a.out = out->base;
+    a.nvec = c->nvec;
+    a.dagger = dag;
+    const bool halo = c->kg.split != 0;
+    a.g = halo ? halo_geom(c, l->prec) : c->kg;
+    a.halo = halo ? 1 : 0;
+    a.scratch = c->face_scratch;
+    a.recv = c->recv_buf;
+    a.face_sites = c->face_sites;
+    a.n_face = c->n_face;
+    int id = 0;
+    r = resolve_variant(c, l->prec, dag, a, s, &id);
+    if (r != CD_OK) return r;
+    if (!halo) {
+        CUDA_TRY(launch_dslash(l->prec, id, a, s, c->pdl != 0, c->num_sms), "dslash launch");
+        return CD_OK;
+    }
+    // multi-rank: pack + exchange on the comm stream, interior on the caller's stream,
+    // then the halo-term kernel once the exchange has landed (overlap).
+    CUDA_TRY(cudaEventRecord(c->ev_in, s), "cudaEventRecord");
+    CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->ev_in, 0), "cudaStreamWaitEvent");
+    CUDA_TRY(launch_pack(l->prec, c->nvec, in->base, c->send_buf, a.g, c->comm_stream), "halo pack");
+    {
+        std::string err;
+        const size_t prec_rec = l->prec == CD_FP32 ? 8 * (size_t)c->N : 4 * (size_t)c->N;
+        r = halo_exchange(c, a.g, prec_rec, l->prec == CD_FP32 ? 0 : 4, c->comm_stream, err);
+        if (r != CD_OK) return fail(r, err);
+    }
+    CUDA_TRY(cudaEventRecord(c->ev_halo, c->comm_stream), "cudaEventRecord");
+    CUDA_TRY(launch_dslash(l->prec, id, a, s, false, c->num_sms), "dslash interior launch");
+    CUDA_TRY(cudaStreamWaitEvent(s, c->ev_halo, 0), "cudaStreamWaitEvent");
+    CUDA_TRY(launch_halo(l->prec, a, s), "halo kernel");
+    return CD_OK;
+}
+
+int coarse_dslash_apply(const cd_links *l, cd_field *out, const cd_field *in, void *stream)
+{
+    API_BEGIN
+    return do_apply(l, out, in, stream, 0);
+    API_END
+}
+
+int coarse_dslash_apply_dagger(const cd_links *l, cd_field *out, const cd_field *in, void *stream)
+{
+    API_BEGIN
+    return do_apply(l, out, in, stream, 1);
+    API_END
+}
+
+int coarse_halo_pack(cd_context *c, const cd_field *in, void *dst, int dst_on_device, size_t *bytes, void *stream)
+{
+    API_BEGIN
+    if (!c || !in || !bytes) return fail(CD_ERR_INVALID, "ctx/in/bytes is NULL");
+    if (in->ctx != c) return fail(CD_ERR_MISMATCH, "field from another context");
+    if (c->kg.split == 0) {
+        *bytes = 0;
+        return CD_OK;
+    }
+    const size_t n = halo_bytes(c, in->prec);
+    *bytes = n;
+    if (!dst) return CD_OK;
+    cudaStream_t s = S(stream);
+    KGeom g = halo_geom(c, in->prec);
+    CUDA_TRY(launch_pack(in->prec, c->nvec, in->base, c->send_buf, g, s), "halo pack");
+    CUDA_TRY(cudaMemcpyAsync(dst, c->send_buf, n, dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s),
+             "cudaMemcpyAsync(pack)");
+    if (!dst_on_device) CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    return CD_OK;
+    API_END
+}
+
+int cd_flush_l2(cd_context *c, size_t bytes, void *stream)
+{
+    API_BEGIN
+    if (!c) return fail(CD_ERR_INVALID, "ctx is NULL");
+    static void *buf = nullptr;
+    static size_t cap = 0;
+    if (bytes > cap) {
+        if (buf) cudaFree(buf);
+        buf = nullptr;
+        cap = 0;
+        CUDA_TRY(cudaMalloc(&buf, bytes), "cudaMalloc(flush)");
+        cap = bytes;
+    }
+    CUDA_TRY(launch_flush(buf, bytes, S(stream)), "flush kernel");
+    return CD_OK;
+    API_END
+}
+
+}  // extern "C"

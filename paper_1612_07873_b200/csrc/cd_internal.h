@@ -1,0 +1,157 @@
+// cd_internal.h -- host runtime structures of the coarse-Dslash library (not part of the ABI).
+//
+// Internal stored records (DESIGN.md §5 "Data layout in HBM"):
+//   fp32 vector record  : N float2                              (8N bytes)
+//   fp16 vector record  : N half2 {re,im} + float scale + 12 B  (4N + 16 bytes)
+//   fp32 matrix record  : N*N float2, row-major                 (8N^2 bytes)
+//   fp16 matrix record  : N*N half2 + float scale + 12 B        (4N^2 + 16 bytes)
+//   field  = V records, site-major (canonical site order)
+//   links  = V * 9 matrix records, [site][k]   -> one site's 9 matrices are contiguous
+// Every record is a multiple of 16 bytes, so every record can be moved by one
+// cp.async.bulk (TMA 1-D) and read with 128-bit loads.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+#include <map>
+#include <mutex>
+
+#include "../../include/coarse_dslash.h"
+
+namespace cd {
+
+inline size_t vec_rec_bytes(int N, cd_precision p) { return p == CD_FP32 ? size_t(8) * N : size_t(4) * N + 16; }
+inline size_t mat_rec_bytes(int N, cd_precision p) { return p == CD_FP32 ? size_t(8) * N * N : size_t(4) * N * N + 16; }
+inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+// Integer division by a run-time constant via a multiply-high (the "integer division magic
+// numbers computed on the host" the paper proposes for the index decode).
+// Valid for 0 <= n < 2^31, 1 <= d < 2^31:  q = (umulhi(n, m) + n) >> s.
+struct FastDiv {
+    uint32_t d, m, s;
+};
+inline FastDiv make_fastdiv(uint32_t d)
+{
+    FastDiv f{d, 0, 0};
+    uint32_t s = 0;
+    while ((uint64_t(1) << s) < d) s++;
+    f.s = s;
+    f.m = uint32_t(((uint64_t(1) << 32) * ((uint64_t(1) << s) - d)) / d + 1);
+    return f;
+}
+inline uint32_t fastdiv_host(uint32_t n, const FastDiv &f)
+{
+    uint64_t hi = (uint64_t(n) * f.m) >> 32;
+    return uint32_t((hi + n) >> f.s);
+}
+
+// Kernel-visible geometry of the local lattice + halo description.
+struct KGeom {
+    int L[4];
+    int V;
+    FastDiv fd[3];          // divisions by L0, L1, L2 for the site decode
+    int split;              // bit mu: dim mu goes through the halo path
+    // halo wire format (R13): for split dim mu, block A then block B,
+    // each F[mu] payload records of prec_rec bytes then (fp16) F[mu] float scales.
+    int64_t blk_off[4][2];  // byte offset of block (mu, A/B) in the send / recv buffer
+    int F[4];               // face sites of dim mu
+};
+
+struct Comm;  // comm.cpp
+
+struct TuneKey {
+    int prec, dagger;
+    bool operator<(const TuneKey &o) const { return prec != o.prec ? prec < o.prec : dagger < o.dagger; }
+};
+
+}  // namespace cd
+
+struct cd_context {
+    cd_geometry geom{};
+    int device = 0, nranks = 1, rank = 0;
+    int coords[4] = {0, 0, 0, 0};
+    int local[4] = {1, 1, 1, 1};
+    int64_t V = 0;
+    int N = 0, nvec = 0;
+    int nbr_rank[4][2] = {};      // [mu][0] = rank at +mu, [mu][1] = rank at -mu
+    cd::KGeom kg{};
+    // halo resources (allocated lazily on first partitioned apply)
+    void *send_buf = nullptr, *recv_buf = nullptr;
+    size_t halo_cap = 0;
+    float2 *face_scratch = nullptr;   // fp32 partial y for face sites [V][N]
+    int *face_sites = nullptr;        // device list of face site indices
+    int n_face = 0;
+    bool halo_ready = false;
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_halo = nullptr;
+    cd::Comm *comm = nullptr;
+    // options
+    int force_variant = -1;
+    int tune = 1;
+    int halo_self_mask = 0;
+    int pdl = 1;
+    bool applied = false;
+    int num_sms = 148;
+    // tuning results per (prec, dagger)
+    std::map<cd::TuneKey, int> chosen;
+    std::mutex mu;
+};
+
+struct cd_field {
+    cd_context *ctx;
+    cd_precision prec;
+    void *base;
+    size_t bytes;
+    bool owned;
+};
+
+struct cd_links {
+    cd_context *ctx;
+    cd_precision prec;
+    void *base;
+    size_t bytes;
+};
+
+namespace cd {
+
+// ---- launchers implemented in .cu files (return cudaError_t of the launch)
+struct ApplyArgs {
+    const void *links;
+    const void *in;
+    void *out;
+    float2 *scratch;       // face-site fp32 partials (halo mode) or nullptr
+    const void *recv;      // halo receive buffer (halo kernel)
+    const int *face_sites; // halo kernel site list
+    int n_face;
+    KGeom g;
+    int nvec;
+    int dagger;
+    int halo;              // 1: skip remote hops, face sites -> scratch
+};
+
+int variant_count(cd_precision p, int nvec);
+const char *variant_name(cd_precision p, int nvec, int id);
+bool variant_valid(cd_precision p, int nvec, int id, const KGeom &g);
+int variant_heuristic(cd_precision p, int nvec, const KGeom &g, int num_sms);
+cudaError_t launch_dslash(cd_precision p, int id, const ApplyArgs &a, cudaStream_t s, bool pdl, int num_sms);
+cudaError_t launch_halo(cd_precision p, const ApplyArgs &a, cudaStream_t s);
+cudaError_t launch_pack(cd_precision p, int nvec, const void *field, void *send, const KGeom &g, cudaStream_t s);
+
+cudaError_t launch_import(cd_precision p, int nvec, int64_t nsites, const void *src, int src_c128, void *dst,
+                          cudaStream_t s);
+cudaError_t launch_export(cd_precision p, int nvec, int64_t nsites, const void *src, void *dst, int dst_c128,
+                          cudaStream_t s);
+cudaError_t launch_links_convert(cd_precision p, int nvec, int64_t nmats, const void *src, int src_c128, void *dst,
+                                 cudaStream_t s, int64_t mat0);
+cudaError_t launch_links_generate(cd_precision p, int nvec, const cd_context *ctx, int kind, uint64_t seed,
+                                  int scale_log2, void *dst, cudaStream_t s);
+cudaError_t launch_field_generate(cd_precision p, int nvec, const cd_context *ctx, uint64_t seed, uint32_t tag,
+                                  int scale_log2, void *dst, cudaStream_t s);
+cudaError_t launch_flush(void *buf, size_t bytes, cudaStream_t s);
+
+void count_launch(int n = 1);
+
+}  // namespace cd

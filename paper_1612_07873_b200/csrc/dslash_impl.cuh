@@ -1,0 +1,595 @@
+// dslash_impl.cuh -- sm_100a kernels of the coarse-grid Dirac operator (Eq. 3).
+//
+//   y(x) = X(x) v(x) + sum_mu [ L_{2mu}(x) v(x+mu) + L_{2mu+1}(x) v(x-mu) ]      (R1-R10)
+//
+// Two kernel families, both instantiated per (storage precision, Nvec):
+//
+//  * RING (large lattices): persistent, one CTA per SM.  One producer thread streams each
+//    site's nine link matrices -- and next to each the neighbour vector it multiplies -- into a
+//    multi-stage shared-memory ring with cp.async.bulk (TMA 1-D, SASS UBLKCP) completed on
+//    mbarriers; N/R consumer warps each own R output rows of the site for all nine hops, so the
+//    hop ("stencil direction") sum stays in registers (direction splitting is
+//    detrimental on large grids).  Lanes split each row dot product D ways (PAPER.md:227-245,
+//    Listing 4) and reduce with xor-shuffles.
+//
+//  * FG (fine-grained, small lattices): a CTA per (site, row block); warps split the nine hops
+//    (KW hops per warp) and the rows (WR row-warps); lanes split the dot product.  All link
+//    loads (input independent) are issued before griddepcontrol.wait (PDL), the nine neighbour
+//    records are staged once per CTA in shared memory, hop partials are reduced through shared
+//    memory by one owner thread per row (§6.2-6.4 mapped onto CTAs: grid parallelism
+//    x colour-spin x direction x dot-product split, no integer division in the decode).
+//
+// Dagger (tau3 D tau3, R5): sign flips of input chunks j >= Nvec and output rows
+// i >= Nvec, no extra pass.  fp16 storage: FHFMA (fp16 x fp16 + fp32) on the raw half2 words,
+// one multiply by s_L * s_v per (row, hop), and a whole-site max-abs before re-quantising y.
+#pragma once
+
+#include "device_common.cuh"
+
+namespace cd {
+
+// ------------------------------------------------------------------ shared pieces
+template <cd_precision P, int NV>
+__device__ __forceinline__ bool is_face(const KGeom &g, const int x[4])
+{
+#pragma unroll
+    for (int mu = 0; mu < 4; mu++)
+        if (((g.split >> mu) & 1) && (x[mu] == 0 || x[mu] == g.L[mu] - 1)) return true;
+    return false;
+}
+
+// Store one site's finished rows.  Called by ALL threads of a group of `nthr` threads (named
+// barrier `bar_id`, or __syncthreads when bar_id < 0); thread t < N owns row t (fp16 needs the
+// whole site for its scale, R12).  fp32: plain store.
+template <cd_precision P, int NV>
+__device__ __forceinline__ void store_site(unsigned char *out, int site, int row, bool owner, float re, float im,
+                                           float *red, int nthr, int bar_id)
+{
+    using Q = Cfg<P, NV>;
+    if constexpr (P == CD_FP32) {
+        if (owner) reinterpret_cast<float2 *>(out + (size_t)site * Q::VREC)[row] = make_float2(re, im);
+    } else {
+        float m = owner ? fmaxf(fabsf(re), fabsf(im)) : 0.0f;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, shfl_xor(m, o));
+        const int warp = (threadIdx.x >> 5), lane = threadIdx.x & 31;
+        const int nw = nthr >> 5;
+        const int w0 = (bar_id < 0) ? 0 : warp;  // caller passes warp-relative ids via red layout
+        (void)w0;
+        if (lane == 0) red[warp] = m;
+        if (bar_id < 0) __syncthreads(); else bar_named(bar_id, nthr);
+        float s = 0.0f;
+        for (int w = 0; w < nw; w++) s = fmaxf(s, red[w]);
+        if (owner) {
+            __half2 q;
+            if (s > 0.0f) q = __halves2half2(__float2half_rn(__fdiv_rn(re, s)), __float2half_rn(__fdiv_rn(im, s)));
+            else q = __halves2half2(__float2half_rn(0.0f), __float2half_rn(0.0f));
+            reinterpret_cast<__half2 *>(out + (size_t)site * Q::VREC)[row] = q;
+            if (row == 0) *reinterpret_cast<float *>(out + (size_t)site * Q::VREC + Q::VSCALE) = s;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ RING variant
+template <cd_precision P, int NV>
+struct RingCfg {
+    using Q = Cfg<P, NV>;
+    static constexpr int NCW = Q::N / Q::R;                         // consumer warps
+    static constexpr int THREADS = 32 * (NCW + 1);
+    static constexpr int STAGE = ((Q::MREC + Q::VREC) + 127) / 128 * 128;
+    static constexpr int HDR = 1024;                                // barriers + reduction scratch
+    static constexpr int MAXS = 32;
+};
+
+template <cd_precision P, int NV>
+__global__ void __launch_bounds__(RingCfg<P, NV>::THREADS, 1) dslash_ring(ApplyArgs a, int S)
+{
+    using Q = Cfg<P, NV>;
+    using RC = RingCfg<P, NV>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem);
+    uint64_t *empty = full + RC::MAXS;
+    float *red = reinterpret_cast<float *>(smem + 16 * RC::MAXS);   // 2 x 32 floats
+    unsigned char *stages = smem + RC::HDR;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned char *links = static_cast<const unsigned char *>(a.links);
+    const unsigned char *in = static_cast<const unsigned char *>(a.in);
+    unsigned char *out = static_cast<unsigned char *>(a.out);
+    const int V = a.g.V;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], RC::NCW);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    pdl_trigger();
+
+    if (warp == RC::NCW) {
+        // ===== producer: one elected lane streams (matrix, vector) records into the ring
+        if (lane == 0) {
+            pdl_wait();   // `in` is written by the previous kernel in the stream
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int site = blockIdx.x; site < V; site += gridDim.x) {
+                int x[4];
+                decode(a.g, site, x);
+                const unsigned char *lsite = links + (size_t)site * 9 * Q::MREC;
+                for (int i = 0; i < 9; i++) {
+                    const int k = kseq(i);
+                    if (a.halo && remote_hop(a.g, x, k)) continue;
+                    const int nb = neighbour(a.g, x, site, k);
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    unsigned char *st = stages + (size_t)stage * RC::STAGE;
+                    mbar_arrive_expect_tx(&full[stage], Q::MREC + Q::VREC);
+                    bulk_g2s(st, lsite + (size_t)k * Q::MREC, Q::MREC, &full[stage]);
+                    bulk_g2s(st + Q::MREC, in + (size_t)nb * Q::VREC, Q::VREC, &full[stage]);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+        return;
+    }
+
+    // ===== consumers: warp w owns rows [w*R, w*R + R) of the current site, all nine hops
+    pdl_wait();   // order our stores after the previous kernel (it may still read `out`)
+    const int r = lane / Q::D, d = lane % Q::D;
+    const int row = warp * Q::R + r;
+    constexpr bool ROT = (Q::ROWB % 128 == 0) && (Q::D * 16 < 128);   // fp16 N=64: avoid 2-way bank conflict
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int site = blockIdx.x; site < V; site += gridDim.x, ++it) {
+        int x[4];
+        decode(a.g, site, x);
+        float re = 0.0f, im = 0.0f;
+        for (int i = 0; i < 9; i++) {
+            const int k = kseq(i);
+            if (a.halo && remote_hop(a.g, x, k)) continue;
+            mbar_wait(&full[stage], phase);
+            const unsigned char *st = stages + (size_t)stage * RC::STAGE;
+            const unsigned char *mrow = st + row * Q::ROWB;
+            const unsigned char *vrec = st + Q::MREC;
+            if constexpr (P == CD_FP32) {
+                float pr[Q::C], pi[Q::C];
+#pragma unroll
+                for (int c = 0; c < Q::C; c++) {
+                    pr[c] = 0.0f;
+                    pi[c] = 0.0f;
+                    const int q = d + Q::D * c;
+                    uint4 vq = lds128(vrec + q * 16);
+                    if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<false>(vq);
+                    cmac2(lds128(mrow + q * 16), vq, pr[c], pi[c]);
+                }
+#pragma unroll
+                for (int c = 0; c < Q::C; c++) { re += pr[c]; im += pi[c]; }
+            } else {
+                float ra = 0.f, rb = 0.f, ia = 0.f, ib = 0.f;
+#pragma unroll
+                for (int c = 0; c < Q::C; c++) {
+                    const int cc = ROT ? ((c + (r & 1)) % Q::C) : c;
+                    const int q = d + Q::D * cc;
+                    uint4 vq = lds128(vrec + q * 16);
+                    if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<true>(vq);
+                    hmac4(lds128(mrow + q * 16), vq, ra, rb, ia, ib);
+                }
+                const float sc = *reinterpret_cast<const float *>(st + Q::MSCALE) *
+                                 *reinterpret_cast<const float *>(vrec + Q::VSCALE);
+                re = fmaf(ra - rb, sc, re);
+                im = fmaf(ia + ib, sc, im);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+#pragma unroll
+        for (int m = Q::D / 2; m >= 1; m >>= 1) {
+            re += shfl_xor(re, m);
+            im += shfl_xor(im, m);
+        }
+        const bool owner = (d == 0);
+        if (a.halo && is_face<P, NV>(a.g, x)) {
+            if (owner) a.scratch[(size_t)site * Q::N + row] = make_float2(re, im);
+        } else {
+            const float sg = (a.dagger && row >= NV) ? -1.0f : 1.0f;
+            store_site<P, NV>(out, site, row, owner, sg * re, sg * im, red + 32 * (it & 1), 32 * RC::NCW, 1);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ FG variant
+template <cd_precision P, int NV, int KW, int WR>
+struct FgCfg {
+    using Q = Cfg<P, NV>;
+    static constexpr int WK = 9 / KW;
+    static constexpr int NW = WK * WR;
+    static constexpr int THREADS = 32 * NW;
+    static constexpr int ROWS = WR * Q::R;
+    static constexpr int NRB = Q::N / ROWS;
+    static_assert(WK * KW == 9, "KW must divide 9");
+    static_assert(NRB * ROWS == Q::N, "row blocks must tile N");
+    static_assert(P == CD_FP32 || NRB == 1, "fp16 output needs the whole site in one CTA");
+    static_assert(NW <= 32, "too many warps");
+};
+
+template <cd_precision P, int NV, int KW, int WR>
+__global__ void __launch_bounds__(FgCfg<P, NV, KW, WR>::THREADS) dslash_fg(ApplyArgs a)
+{
+    using Q = Cfg<P, NV>;
+    using F = FgCfg<P, NV, KW, WR>;
+    __shared__ __align__(16) unsigned char vs[9 * Q::VREC];
+    __shared__ float2 part[F::WK][F::ROWS];
+    __shared__ float red[32];
+
+    const int site = blockIdx.x / F::NRB, rb = blockIdx.x - site * F::NRB;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wk = warp / WR, wr = warp - wk * WR;
+    const int r = lane / Q::D, d = lane % Q::D;
+    const int rowl = wr * Q::R + r, row = rb * F::ROWS + rowl;
+    const unsigned char *links = static_cast<const unsigned char *>(a.links);
+    const unsigned char *in = static_cast<const unsigned char *>(a.in);
+    unsigned char *out = static_cast<unsigned char *>(a.out);
+
+    int x[4];
+    decode(a.g, site, x);
+
+    // 1. link rows: input independent -> issued before the PDL wait
+    uint4 Lc[KW][Q::C];
+    float sl[KW];
+    bool on[KW];
+#pragma unroll
+    for (int kk = 0; kk < KW; kk++) {
+        const int k = kseq(wk * KW + kk);
+        on[kk] = !(a.halo && remote_hop(a.g, x, k));
+        const unsigned char *m = links + ((size_t)site * 9 + k) * Q::MREC;
+#pragma unroll
+        for (int c = 0; c < Q::C; c++)
+            Lc[kk][c] = on[kk] ? ld_stream(m + row * Q::ROWB + (d + Q::D * c) * 16) : make_uint4(0, 0, 0, 0);
+        sl[kk] = (Q::F16 && on[kk]) ? ld_nc_f32(m + Q::MSCALE) : 0.0f;
+    }
+    pdl_trigger();
+    pdl_wait();
+
+    // 2. the nine neighbour records -> shared memory (one 16-B chunk per thread-step)
+    for (int t = threadIdx.x; t < 9 * Q::VCH; t += F::THREADS) {
+        const int k = t / Q::VCH, e = t - k * Q::VCH;
+        if (a.halo && remote_hop(a.g, x, k)) continue;
+        const int nb = neighbour(a.g, x, site, k);
+        *reinterpret_cast<uint4 *>(vs + k * Q::VREC + e * 16) = ld_nc(in + (size_t)nb * Q::VREC + e * 16);
+    }
+    __syncthreads();
+
+    // 3. dot products (ILP: one accumulator pair per chunk, Listing 5)
+    float re = 0.0f, im = 0.0f;
+#pragma unroll
+    for (int kk = 0; kk < KW; kk++) {
+        if (!on[kk]) continue;
+        const int k = kseq(wk * KW + kk);
+        const unsigned char *vrec = vs + k * Q::VREC;
+        if constexpr (P == CD_FP32) {
+            float pr[Q::C], pi[Q::C];
+#pragma unroll
+            for (int c = 0; c < Q::C; c++) {
+                pr[c] = 0.0f;
+                pi[c] = 0.0f;
+                const int q = d + Q::D * c;
+                uint4 vq = lds128(vrec + q * 16);
+                if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<false>(vq);
+                cmac2(Lc[kk][c], vq, pr[c], pi[c]);
+            }
+#pragma unroll
+            for (int c = 0; c < Q::C; c++) { re += pr[c]; im += pi[c]; }
+        } else {
+            float ra = 0.f, rb2 = 0.f, ia = 0.f, ib = 0.f;
+#pragma unroll
+            for (int c = 0; c < Q::C; c++) {
+                const int q = d + Q::D * c;
+                uint4 vq = lds128(vrec + q * 16);
+                if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<true>(vq);
+                hmac4(Lc[kk][c], vq, ra, rb2, ia, ib);
+            }
+            const float sc = sl[kk] * *reinterpret_cast<const float *>(vrec + Q::VSCALE);
+            re = fmaf(ra - rb2, sc, re);
+            im = fmaf(ia + ib, sc, im);
+        }
+    }
+    // 4. dot-product split: xor-shuffle over the D lanes of a row
+#pragma unroll
+    for (int m = Q::D / 2; m >= 1; m >>= 1) {
+        re += shfl_xor(re, m);
+        im += shfl_xor(im, m);
+    }
+    // 5. direction split: hop-group partials through shared memory, one owner per row
+    if (d == 0) part[wk][rowl] = make_float2(re, im);
+    __syncthreads();
+    const int t = threadIdx.x;
+    const bool owner = t < F::ROWS;
+    float yr = 0.0f, yi = 0.0f;
+    if (owner) {
+#pragma unroll
+        for (int w = 0; w < F::WK; w++) {
+            yr += part[w][t].x;
+            yi += part[w][t].y;
+        }
+    }
+    const int orow = rb * F::ROWS + (owner ? t : 0);
+    if (a.halo && is_face<P, NV>(a.g, x)) {
+        if (owner) a.scratch[(size_t)site * Q::N + orow] = make_float2(yr, yi);
+        return;
+    }
+    const float sg = (a.dagger && orow >= NV) ? -1.0f : 1.0f;
+    store_site<P, NV>(out, site, orow, owner, sg * yr, sg * yi, red, F::THREADS, -1);
+}
+
+// ------------------------------------------------------------------ halo term (multi-rank)
+// One CTA per face site: y(x) = partial(x) + sum over remote hops L_k(x) v_halo, then the
+// final store (fp16: whole-site re-quantisation).  Neighbour records come from the receive
+// buffer in the wire order of DESIGN.md R13: a +mu hop reads block B of mu (sent by the +mu
+// neighbour from its x_mu = 0 face), a -mu hop reads block A.
+template <cd_precision P, int NV>
+__global__ void __launch_bounds__(32 * (2 * NV / Cfg<P, NV>::R)) dslash_halo(ApplyArgs a)
+{
+    using Q = Cfg<P, NV>;
+    constexpr int NWARP = Q::N / Q::R;
+    constexpr int PREC = Q::F16 ? 4 * Q::N : 8 * Q::N;   // wire payload record
+    __shared__ float red[32];
+    const int site = a.face_sites[blockIdx.x];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r = lane / Q::D, d = lane % Q::D;
+    const int row = warp * Q::R + r;
+    const unsigned char *links = static_cast<const unsigned char *>(a.links);
+    const unsigned char *recv = static_cast<const unsigned char *>(a.recv);
+    int x[4];
+    decode(a.g, site, x);
+    float re = 0.0f, im = 0.0f;
+    for (int k = 0; k < 8; k++) {
+        if (!remote_hop(a.g, x, k)) continue;
+        const int mu = k >> 1;
+        const int blk = (k & 1) ? 0 : 1;
+        int o3[3], n = 0;
+        for (int nu = 0; nu < 4; nu++)
+            if (nu != mu) o3[n++] = nu;
+        const int f = (x[o3[2]] * a.g.L[o3[1]] + x[o3[1]]) * a.g.L[o3[0]] + x[o3[0]];
+        const unsigned char *vrec = recv + a.g.blk_off[mu][blk] + (size_t)f * PREC;
+        const unsigned char *m = links + ((size_t)site * 9 + k) * Q::MREC;
+        if constexpr (P == CD_FP32) {
+#pragma unroll
+            for (int c = 0; c < Q::C; c++) {
+                const int q = d + Q::D * c;
+                uint4 vq = ld_nc(vrec + q * 16);
+                if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<false>(vq);
+                cmac2(ld_nc(m + row * Q::ROWB + q * 16), vq, re, im);
+            }
+        } else {
+            float ra = 0.f, rb = 0.f, ia = 0.f, ib = 0.f;
+#pragma unroll
+            for (int c = 0; c < Q::C; c++) {
+                const int q = d + Q::D * c;
+                uint4 vq = ld_nc(vrec + q * 16);
+                if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<true>(vq);
+                hmac4(ld_nc(m + row * Q::ROWB + q * 16), vq, ra, rb, ia, ib);
+            }
+            const float sv = *reinterpret_cast<const float *>(recv + a.g.blk_off[mu][blk] + (size_t)a.g.F[mu] * PREC +
+                                                              (size_t)f * 4);
+            const float sc = ld_nc_f32(m + Q::MSCALE) * sv;
+            re = fmaf(ra - rb, sc, re);
+            im = fmaf(ia + ib, sc, im);
+        }
+    }
+#pragma unroll
+    for (int m = Q::D / 2; m >= 1; m >>= 1) {
+        re += shfl_xor(re, m);
+        im += shfl_xor(im, m);
+    }
+    const bool owner = (d == 0);
+    if (owner) {
+        const float2 p = a.scratch[(size_t)site * Q::N + row];
+        re += p.x;
+        im += p.y;
+    }
+    const float sg = (a.dagger && row >= NV) ? -1.0f : 1.0f;
+    store_site<P, NV>(static_cast<unsigned char *>(a.out), site, row, owner, sg * re, sg * im, red, 32 * NWARP, -1);
+}
+
+// ------------------------------------------------------------------ halo pack
+// One launch for all split dims: blockIdx.y = (mu, block) pair index,
+// threads over the face's 16-B payload chunks and then its scales (fp16).
+template <cd_precision P, int NV>
+__global__ void halo_pack(const unsigned char *field, unsigned char *send, KGeom g, int4 pairs)
+{
+    using Q = Cfg<P, NV>;
+    constexpr int PREC = Q::F16 ? 4 * Q::N : 8 * Q::N;
+    constexpr int CPR = PREC / 16;
+    const int pid = (&pairs.x)[blockIdx.y >> 1];
+    const int mu = pid, blk = blockIdx.y & 1;
+    const int F = g.F[mu];
+    int o3[3], n = 0;
+    for (int nu = 0; nu < 4; nu++)
+        if (nu != mu) o3[n++] = nu;
+    unsigned char *dst = send + g.blk_off[mu][blk];
+    const int total = F * CPR + (Q::F16 ? F : 0);
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        const bool sc = e >= F * CPR;
+        const int f = sc ? e - F * CPR : e / CPR;
+        const int ch = sc ? 0 : e - f * CPR;
+        int x[4];
+        int t = f;
+        x[o3[0]] = t % g.L[o3[0]];
+        t /= g.L[o3[0]];
+        x[o3[1]] = t % g.L[o3[1]];
+        x[o3[2]] = t / g.L[o3[1]];
+        x[mu] = blk == 0 ? g.L[mu] - 1 : 0;
+        const unsigned char *rec = field + (size_t)encode(g, x) * Q::VREC;
+        if (!sc) *reinterpret_cast<uint4 *>(dst + (size_t)f * PREC + ch * 16) = *reinterpret_cast<const uint4 *>(rec + ch * 16);
+        else *reinterpret_cast<float *>(dst + (size_t)F * PREC + (size_t)f * 4) = *reinterpret_cast<const float *>(rec + Q::VSCALE);
+    }
+}
+
+// ------------------------------------------------------------------ variant table
+struct VDesc {
+    int kind;  // 0 = ring, 1 = fg
+    int kw, wr;
+};
+
+template <cd_precision P, int NV>
+struct Variants;
+template <>
+struct Variants<CD_FP32, 24> {
+    static constexpr int n = 10;
+    static constexpr VDesc v[n] = {{0, 0, 0}, {1, 1, 1}, {1, 1, 2}, {1, 1, 3}, {1, 3, 2},
+                                   {1, 3, 4}, {1, 3, 6}, {1, 9, 3}, {1, 9, 6}, {1, 9, 12}};
+};
+template <>
+struct Variants<CD_FP32, 32> {
+    static constexpr int n = 9;
+    static constexpr VDesc v[n] = {{0, 0, 0}, {1, 1, 1}, {1, 1, 2}, {1, 3, 2}, {1, 3, 4},
+                                   {1, 3, 8}, {1, 9, 4}, {1, 9, 8}, {1, 9, 16}};
+};
+template <>
+struct Variants<CD_FP16, 24> {
+    static constexpr int n = 3;
+    static constexpr VDesc v[n] = {{0, 0, 0}, {1, 3, 6}, {1, 9, 6}};
+};
+template <>
+struct Variants<CD_FP16, 32> {
+    static constexpr int n = 3;
+    static constexpr VDesc v[n] = {{0, 0, 0}, {1, 3, 8}, {1, 9, 8}};
+};
+
+template <cd_precision P, int NV>
+inline const char *variant_name_t(int id)
+{
+    static char names[16][48];
+    static bool init = false;
+    if (!init) {
+        for (int i = 0; i < Variants<P, NV>::n; i++) {
+            const VDesc &v = Variants<P, NV>::v[i];
+            if (v.kind == 0) snprintf(names[i], 48, "ring_tma_%s_nv%d", P == CD_FP32 ? "f32" : "f16", NV);
+            else snprintf(names[i], 48, "fg_kw%d_wr%d_%s_nv%d", v.kw, v.wr, P == CD_FP32 ? "f32" : "f16", NV);
+        }
+        init = true;
+    }
+    return (id >= 0 && id < Variants<P, NV>::n) ? names[id] : nullptr;
+}
+
+inline cudaError_t launch_ex(const void *fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl, void **args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    count_launch();
+    return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+template <cd_precision P, int NV>
+inline int ring_stages()
+{
+    using RC = RingCfg<P, NV>;
+    int s = (227 * 1024 - RC::HDR) / RC::STAGE;
+    return s > RC::MAXS ? RC::MAXS : s;
+}
+
+template <cd_precision P, int NV>
+cudaError_t launch_ring(const ApplyArgs &a, cudaStream_t s, bool pdl, int num_sms)
+{
+    using RC = RingCfg<P, NV>;
+    static bool attr = false;
+    const int S = ring_stages<P, NV>();
+    const size_t smem = RC::HDR + (size_t)S * RC::STAGE;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(dslash_ring<P, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    int grid = a.g.V < num_sms ? a.g.V : num_sms;
+    ApplyArgs aa = a;
+    int SS = S;
+    void *args[] = {&aa, &SS};
+    return launch_ex((const void *)dslash_ring<P, NV>, dim3(grid), dim3(RC::THREADS), smem, s, pdl, args);
+}
+
+template <cd_precision P, int NV, int KW, int WR>
+cudaError_t launch_fg(const ApplyArgs &a, cudaStream_t s, bool pdl)
+{
+    using F = FgCfg<P, NV, KW, WR>;
+    ApplyArgs aa = a;
+    void *args[] = {&aa};
+    return launch_ex((const void *)dslash_fg<P, NV, KW, WR>, dim3((unsigned)(a.g.V * F::NRB)), dim3(F::THREADS), 0, s,
+                     pdl, args);
+}
+
+template <cd_precision P, int NV, int I>
+cudaError_t dispatch_variant(int id, const ApplyArgs &a, cudaStream_t s, bool pdl, int num_sms)
+{
+    if constexpr (I >= Variants<P, NV>::n) {
+        return cudaErrorInvalidValue;
+    } else {
+        if (id == I) {
+            constexpr VDesc v = Variants<P, NV>::v[I];
+            if constexpr (v.kind == 0) return launch_ring<P, NV>(a, s, pdl, num_sms);
+            else return launch_fg<P, NV, v.kw, v.wr>(a, s, pdl);
+        }
+        return dispatch_variant<P, NV, I + 1>(id, a, s, pdl, num_sms);
+    }
+}
+
+template <cd_precision P, int NV>
+cudaError_t launch_halo_t(const ApplyArgs &a, cudaStream_t s)
+{
+    if (a.n_face == 0) return cudaSuccess;
+    using Q = Cfg<P, NV>;
+    ApplyArgs aa = a;
+    void *args[] = {&aa};
+    return launch_ex((const void *)dslash_halo<P, NV>, dim3(a.n_face), dim3(32 * (Q::N / Q::R)), 0, s, false, args);
+}
+
+template <cd_precision P, int NV>
+cudaError_t launch_pack_t(const void *field, void *send, const KGeom &g, cudaStream_t s)
+{
+    int4 pairs = make_int4(0, 0, 0, 0);
+    int np = 0;
+    int *pp = &pairs.x;
+    for (int mu = 0; mu < 4; mu++)
+        if ((g.split >> mu) & 1) pp[np++] = mu;
+    if (np == 0) return cudaSuccess;
+    const unsigned char *f = static_cast<const unsigned char *>(field);
+    unsigned char *d = static_cast<unsigned char *>(send);
+    KGeom gg = g;
+    void *args[] = {&f, &d, &gg, &pairs};
+    return launch_ex((const void *)halo_pack<P, NV>, dim3(16, 2 * np), dim3(256), 0, s, false, args);
+}
+
+}  // namespace cd
+
+// Per-(P, NV) entry points, defined in the instantiation units.
+#define CD_INSTANTIATE(P, NV, TAG)                                                                                 \
+    namespace cd {                                                                                                \
+    cudaError_t launch_dslash_##TAG(int id, const ApplyArgs &a, cudaStream_t s, bool pdl, int sms)                \
+    {                                                                                                             \
+        return dispatch_variant<P, NV, 0>(id, a, s, pdl, sms);                                                    \
+    }                                                                                                             \
+    cudaError_t launch_halo_##TAG(const ApplyArgs &a, cudaStream_t s) { return launch_halo_t<P, NV>(a, s); }      \
+    cudaError_t launch_pack_##TAG(const void *f, void *d, const KGeom &g, cudaStream_t s)                         \
+    {                                                                                                             \
+        return launch_pack_t<P, NV>(f, d, g, s);                                                                  \
+    }                                                                                                             \
+    int variant_count_##TAG() { return Variants<P, NV>::n; }                                                      \
+    const char *variant_name_##TAG(int id) { return variant_name_t<P, NV>(id); }                                  \
+    int variant_kind_##TAG(int id, int *kw, int *wr)                                                              \
+    {                                                                                                             \
+        if (id < 0 || id >= Variants<P, NV>::n) return -1;                                                        \
+        *kw = Variants<P, NV>::v[id].kw;                                                                          \
+        *wr = Variants<P, NV>::v[id].wr;                                                                          \
+        return Variants<P, NV>::v[id].kind;                                                                       \
+    }                                                                                                             \
+    }
