@@ -207,6 +207,34 @@ int coarse_halo_pack(cd_context *ctx, const cd_field *in, void *dst, int dst_on_
 /* Write the L2-flush scratch (bench utility): a kernel writing `bytes` of device memory. */
 int cd_flush_l2(cd_context *ctx, size_t bytes, void *stream);
 
+/* ------------------------------------------------------------------ halo plan (host only) */
+
+/* The domain decomposition and halo wire layout of one rank (R13), computed on the
+ * host without touching a GPU; the library's own pack / exchange / halo-term path uses exactly
+ * this plan.  Exchange schedule for every split dim mu: send block A to nbr_rank[mu][0] (+mu)
+ * and block B to nbr_rank[mu][1] (-mu); receive block A from nbr_rank[mu][1] and block B from
+ * nbr_rank[mu][0], into the same offsets of the receive buffer.  A +mu hop of a face site reads
+ * block B, a -mu hop block A; record f of a block is the face site with the other three
+ * coordinates lexicographic (lowest mu fastest). */
+typedef struct {
+    int32_t local_dims[4];
+    int32_t grid_coords[4];
+    int64_t local_volume;
+    int32_t split_mask;          /* bit mu: dim mu exchanged (P_mu > 1, or forced by self_mask) */
+    int32_t nbr_rank[4][2];      /* [mu][0] = rank at +mu, [mu][1] = rank at -mu (periodic)    */
+    int64_t face_sites[4];       /* sites of one face of dim mu (= V / L_mu)                    */
+    int64_t record_bytes;        /* wire payload bytes per site (fp32: 8N, fp16: 4N)            */
+    int64_t scale_bytes;         /* wire scale bytes per site (fp32: 0, fp16: 4)                */
+    int64_t block_offset[4][2];  /* byte offset of block A / B of dim mu (0 if not split)       */
+    int64_t block_bytes[4];      /* bytes of one block of dim mu, zero-padded to 16             */
+    int64_t total_bytes;         /* send (= receive) buffer size                                */
+} cd_halo_plan;
+
+/* Fill *out for `rank` of the process grid in geom (self_mask as CD_OPT_HALO_SELF_MASK).
+ * CD_ERR_INVALID / CD_ERR_UNSUPPORTED as cd_context_create's geometry checks. */
+int cd_halo_plan_create(const cd_geometry *geom, int nranks, int rank, cd_precision prec, int32_t self_mask,
+                        cd_halo_plan *out);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

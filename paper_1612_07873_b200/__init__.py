@@ -39,7 +39,7 @@ EXPORTS = (
     "coarse_field_free", "coarse_field_import", "coarse_field_export", "coarse_field_generate",
     "coarse_field_stored_bytes", "coarse_field_read_stored", "coarse_links_upload", "coarse_links_generate",
     "coarse_links_stored_bytes", "coarse_links_read_stored", "coarse_links_free", "coarse_dslash_apply",
-    "coarse_dslash_apply_dagger", "coarse_halo_pack", "cd_flush_l2",
+    "coarse_dslash_apply_dagger", "coarse_halo_pack", "cd_flush_l2", "cd_halo_plan_create",
 )
 
 
@@ -51,6 +51,16 @@ class CDError(RuntimeError):
 
 class _Geometry(ctypes.Structure):
     _fields_ = [("global_dims", ctypes.c_int32 * 4), ("nvec", ctypes.c_int32), ("proc_grid", ctypes.c_int32 * 4)]
+
+
+class HaloPlan(ctypes.Structure):
+    """cd_halo_plan (include/coarse_dslash.h): decomposition + halo wire layout of one rank."""
+    _fields_ = [("local_dims", ctypes.c_int32 * 4), ("grid_coords", ctypes.c_int32 * 4),
+                ("local_volume", ctypes.c_int64), ("split_mask", ctypes.c_int32),
+                ("nbr_rank", (ctypes.c_int32 * 2) * 4), ("face_sites", ctypes.c_int64 * 4),
+                ("record_bytes", ctypes.c_int64), ("scale_bytes", ctypes.c_int64),
+                ("block_offset", (ctypes.c_int64 * 2) * 4), ("block_bytes", ctypes.c_int64 * 4),
+                ("total_bytes", ctypes.c_int64)]
 
 
 def _load():
@@ -89,6 +99,7 @@ def _load():
         "coarse_dslash_apply_dagger": ([P, P, P, P], I),
         "coarse_halo_pack": ([P, P, P, I, ctypes.POINTER(SZ), P], I),
         "cd_flush_l2": ([P, SZ, P], I),
+        "cd_halo_plan_create": ([ctypes.POINTER(_Geometry), I, I, I, ctypes.c_int32, ctypes.POINTER(HaloPlan)], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -162,6 +173,15 @@ def cd_context_create(global_dims, nvec, proc_grid=(1, 1, 1, 1), device=0, nrank
     out = ctypes.c_void_p()
     idb = None if nccl_id is None else (ctypes.c_uint8 * 128)(*nccl_id)
     _check(lib.cd_context_create(ctypes.byref(g), device, nranks, rank, idb, ctypes.byref(out)))
+    return out
+
+
+def cd_halo_plan_create(global_dims, nvec, proc_grid, rank, prec="fp32", self_mask=0) -> HaloPlan:
+    """Host-only decomposition + halo layout of `rank` (no GPU needed)."""
+    g = _Geometry((ctypes.c_int32 * 4)(*global_dims), nvec, (ctypes.c_int32 * 4)(*proc_grid))
+    nranks = int(np.prod(proc_grid))
+    out = HaloPlan()
+    _check(lib.cd_halo_plan_create(ctypes.byref(g), nranks, rank, PREC[prec], self_mask, ctypes.byref(out)))
     return out
 
 

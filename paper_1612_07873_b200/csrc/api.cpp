@@ -132,40 +132,85 @@ static int cuda_fail(cudaError_t e, const char *what)
 
 static cudaStream_t S(void *s) { return static_cast<cudaStream_t>(s); }
 
-// ------------------------------------------------------------------ halo layout
-// Wire order (R13): split dims ascending; per dim block A (face sent to +mu, x_mu =
-// L-1) then block B (face sent to -mu, x_mu = 0); each block = F payload records then
-// (fp16) F float scales.
+// ------------------------------------------------------------------ decomposition + halo plan
+// Geometry checks shared by cd_context_create and cd_halo_plan_create.
+static int check_geometry(const cd_geometry *geom, int nranks, int rank)
+{
+    if (!geom) return fail(CD_ERR_INVALID, "geom is NULL");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(CD_ERR_INVALID, "bad nranks/rank");
+    int64_t prodP = 1, V = 1;
+    for (int mu = 0; mu < 4; mu++) {
+        if (geom->global_dims[mu] < 1) return fail(CD_ERR_INVALID, "global_dims must be >= 1");
+        if (geom->proc_grid[mu] < 1) return fail(CD_ERR_INVALID, "proc_grid must be >= 1");
+        if (geom->global_dims[mu] % geom->proc_grid[mu]) return fail(CD_ERR_INVALID, "global_dims % proc_grid != 0");
+        prodP *= geom->proc_grid[mu];
+        V *= geom->global_dims[mu] / geom->proc_grid[mu];
+    }
+    if (prodP != nranks) return fail(CD_ERR_INVALID, "prod(proc_grid) != nranks");
+    if (geom->nvec != 24 && geom->nvec != 32) return fail(CD_ERR_UNSUPPORTED, "nvec must be 24 or 32");
+    if (V >= (int64_t(1) << 31) / 9) return fail(CD_ERR_UNSUPPORTED, "local volume too large");
+    return CD_OK;
+}
+
+// Rank grid (lexicographic like sites), local block, periodic neighbour ranks, and the wire
+// layout of DESIGN.md R13: split dims ascending; per dim block A (face sent to +mu, x_mu =
+// L-1) then block B (face sent to -mu, x_mu = 0); each block = F payload records then (fp16)
+// F float scales, zero-padded to 16 bytes.
+static void make_plan(const cd_geometry *geom, int rank, cd_precision p, int self_mask, cd_halo_plan *o)
+{
+    memset(o, 0, sizeof(*o));
+    const int N = 2 * geom->nvec;
+    int t = rank;
+    o->local_volume = 1;
+    for (int mu = 0; mu < 4; mu++) {
+        o->grid_coords[mu] = t % geom->proc_grid[mu];
+        t /= geom->proc_grid[mu];
+        o->local_dims[mu] = geom->global_dims[mu] / geom->proc_grid[mu];
+        o->local_volume *= o->local_dims[mu];
+        if (geom->proc_grid[mu] > 1 || ((self_mask >> mu) & 1)) o->split_mask |= 1 << mu;
+    }
+    for (int mu = 0; mu < 4; mu++)
+        for (int dir = 0; dir < 2; dir++) {
+            int cc[4] = {o->grid_coords[0], o->grid_coords[1], o->grid_coords[2], o->grid_coords[3]};
+            const int P = geom->proc_grid[mu];
+            cc[mu] = (cc[mu] + (dir == 0 ? 1 : -1) + P) % P;
+            o->nbr_rank[mu][dir] = ((cc[3] * geom->proc_grid[2] + cc[2]) * geom->proc_grid[1] + cc[1]) *
+                                       geom->proc_grid[0] + cc[0];
+        }
+    o->record_bytes = (p == CD_FP32) ? 8 * (int64_t)N : 4 * (int64_t)N;
+    o->scale_bytes = (p == CD_FP32) ? 0 : 4;
+    int64_t off = 0;
+    for (int mu = 0; mu < 4; mu++) {
+        o->face_sites[mu] = o->local_volume / o->local_dims[mu];
+        if (!((o->split_mask >> mu) & 1)) continue;
+        o->block_bytes[mu] = (o->face_sites[mu] * (o->record_bytes + o->scale_bytes) + 15) & ~int64_t(15);
+        for (int b = 0; b < 2; b++) {
+            o->block_offset[mu][b] = off;
+            off += o->block_bytes[mu];
+        }
+    }
+    o->total_bytes = off;
+}
+
+static cd_halo_plan ctx_plan(const cd_context *c, cd_precision p)
+{
+    cd_halo_plan o;
+    make_plan(&c->geom, c->rank, p, c->halo_self_mask, &o);
+    return o;
+}
+
 static KGeom halo_geom(const cd_context *c, cd_precision p)
 {
     KGeom g = c->kg;
-    const size_t prec_rec = (p == CD_FP32) ? 8 * (size_t)c->N : 4 * (size_t)c->N;
-    const size_t sc = (p == CD_FP32) ? 0 : 4;
-    int64_t off = 0;
+    const cd_halo_plan pl = ctx_plan(c, p);
     for (int mu = 0; mu < 4; mu++) {
-        g.F[mu] = (int)(c->V / c->local[mu]);
-        if (!((g.split >> mu) & 1)) {
-            g.blk_off[mu][0] = g.blk_off[mu][1] = 0;
-            continue;
-        }
-        for (int b = 0; b < 2; b++) {
-            g.blk_off[mu][b] = off;
-            off += (int64_t)g.F[mu] * (prec_rec + sc);
-            off = (off + 15) & ~int64_t(15);
-        }
+        g.F[mu] = (int)pl.face_sites[mu];
+        g.blk_off[mu][0] = pl.block_offset[mu][0];
+        g.blk_off[mu][1] = pl.block_offset[mu][1];
     }
     return g;
 }
-static size_t halo_bytes(const cd_context *c, cd_precision p)
-{
-    KGeom g = halo_geom(c, p);
-    size_t mx = 0;
-    const size_t prec_rec = (p == CD_FP32) ? 8 * (size_t)c->N : 4 * (size_t)c->N;
-    const size_t sc = (p == CD_FP32) ? 0 : 4;
-    for (int mu = 0; mu < 4; mu++)
-        if ((g.split >> mu) & 1) mx = std::max(mx, (size_t)g.blk_off[mu][1] + (((size_t)g.F[mu] * (prec_rec + sc) + 15) & ~size_t(15)));
-    return mx;
-}
+static size_t halo_bytes(const cd_context *c, cd_precision p) { return (size_t)ctx_plan(c, p).total_bytes; }
 
 static int setup_halo(cd_context *c)
 {
@@ -259,17 +304,9 @@ int cd_context_create(const cd_geometry *geom, int device, int nranks, int rank,
     API_BEGIN
     if (!geom || !out) return fail(CD_ERR_INVALID, "geom/out is NULL");
     *out = nullptr;
-    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(CD_ERR_INVALID, "bad nranks/rank");
+    int r0 = check_geometry(geom, nranks, rank);
+    if (r0 != CD_OK) return r0;
     if ((nranks > 1) != (nccl_id != nullptr)) return fail(CD_ERR_INVALID, "nccl_id must be given iff nranks > 1");
-    int64_t prodP = 1;
-    for (int mu = 0; mu < 4; mu++) {
-        if (geom->global_dims[mu] < 1) return fail(CD_ERR_INVALID, "global_dims must be >= 1");
-        if (geom->proc_grid[mu] < 1) return fail(CD_ERR_INVALID, "proc_grid must be >= 1");
-        if (geom->global_dims[mu] % geom->proc_grid[mu]) return fail(CD_ERR_INVALID, "global_dims % proc_grid != 0");
-        prodP *= geom->proc_grid[mu];
-    }
-    if (prodP != nranks) return fail(CD_ERR_INVALID, "prod(proc_grid) != nranks");
-    if (geom->nvec != 24 && geom->nvec != 32) return fail(CD_ERR_UNSUPPORTED, "nvec must be 24 or 32");
     int ndev = 0;
     CUDA_TRY(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
     if (device < 0 || device >= ndev) return fail(CD_ERR_INVALID, "bad device");
@@ -282,35 +319,20 @@ int cd_context_create(const cd_geometry *geom, int device, int nranks, int rank,
     c->rank = rank;
     c->nvec = geom->nvec;
     c->N = 2 * geom->nvec;
-    int t = rank;
-    int64_t V = 1;
+    cd_halo_plan pl;
+    make_plan(geom, rank, CD_FP32, 0, &pl);
     for (int mu = 0; mu < 4; mu++) {
-        c->coords[mu] = t % geom->proc_grid[mu];
-        t /= geom->proc_grid[mu];
-        c->local[mu] = geom->global_dims[mu] / geom->proc_grid[mu];
-        V *= c->local[mu];
+        c->coords[mu] = pl.grid_coords[mu];
+        c->local[mu] = pl.local_dims[mu];
+        c->nbr_rank[mu][0] = pl.nbr_rank[mu][0];
+        c->nbr_rank[mu][1] = pl.nbr_rank[mu][1];
     }
-    if (V >= (int64_t(1) << 31) / 9) {
-        delete c;
-        return fail(CD_ERR_UNSUPPORTED, "local volume too large");
-    }
-    c->V = V;
-    for (int mu = 0; mu < 4; mu++) {
-        for (int dir = 0; dir < 2; dir++) {
-            int cc[4] = {c->coords[0], c->coords[1], c->coords[2], c->coords[3]};
-            const int P = geom->proc_grid[mu];
-            cc[mu] = (cc[mu] + (dir == 0 ? 1 : -1) + P) % P;
-            c->nbr_rank[mu][dir] = ((cc[3] * geom->proc_grid[2] + cc[2]) * geom->proc_grid[1] + cc[1]) *
-                                       geom->proc_grid[0] + cc[0];
-        }
-    }
+    c->V = pl.local_volume;
     KGeom &g = c->kg;
     for (int mu = 0; mu < 4; mu++) g.L[mu] = c->local[mu];
-    g.V = (int)V;
+    g.V = (int)c->V;
     for (int i = 0; i < 3; i++) g.fd[i] = make_fastdiv((uint32_t)c->local[i]);
-    g.split = 0;
-    for (int mu = 0; mu < 4; mu++)
-        if (geom->proc_grid[mu] > 1) g.split |= (1 << mu);
+    g.split = pl.split_mask;
     cudaDeviceProp prop;
     cudaError_t e = cudaGetDeviceProperties(&prop, device);
     if (e != cudaSuccess) {
@@ -318,6 +340,12 @@ int cd_context_create(const cd_geometry *geom, int device, int nranks, int rank,
         return cuda_fail(e, "cudaGetDeviceProperties");
     }
     c->num_sms = prop.multiProcessorCount;
+    e = cudaMalloc(&c->work, 2 * sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(c->work, 0, 2 * sizeof(int));
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_fail(e, "cudaMalloc(work)");
+    }
     if (const char *ev = getenv("CD_TUNE")) c->tune = atoi(ev) ? 1 : 0;
     if (const char *ev = getenv("CD_VARIANT")) c->force_variant = atoi(ev);
     if (const char *ev = getenv("CD_PDL")) c->pdl = atoi(ev) ? 1 : 0;
@@ -349,6 +377,7 @@ int cd_context_destroy(cd_context *c)
     if (c->recv_buf) cudaFree(c->recv_buf);
     if (c->face_scratch) cudaFree(c->face_scratch);
     if (c->face_sites) cudaFree(c->face_sites);
+    if (c->work) cudaFree(c->work);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->ev_in) cudaEventDestroy(c->ev_in);
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
@@ -802,6 +831,7 @@ static int do_apply(const cd_links *l, cd_field *out, const cd_field *in, void *
     a.recv = c->recv_buf;
     a.face_sites = c->face_sites;
     a.n_face = c->n_face;
+    a.work = c->work;
     int id = 0;
     r = resolve_variant(c, l->prec, dag, a, s, &id);
     if (r != CD_OK) return r;
@@ -816,8 +846,7 @@ static int do_apply(const cd_links *l, cd_field *out, const cd_field *in, void *
     CUDA_TRY(launch_pack(l->prec, c->nvec, in->base, c->send_buf, a.g, c->comm_stream), "halo pack");
     {
         std::string err;
-        const size_t prec_rec = l->prec == CD_FP32 ? 8 * (size_t)c->N : 4 * (size_t)c->N;
-        r = halo_exchange(c, a.g, prec_rec, l->prec == CD_FP32 ? 0 : 4, c->comm_stream, err);
+        r = halo_exchange(c, ctx_plan(c, l->prec), c->comm_stream, err);
         if (r != CD_OK) return fail(r, err);
     }
     CUDA_TRY(cudaEventRecord(c->ev_halo, c->comm_stream), "cudaEventRecord");
@@ -859,6 +888,23 @@ int coarse_halo_pack(cd_context *c, const cd_field *in, void *dst, int dst_on_de
     CUDA_TRY(cudaMemcpyAsync(dst, c->send_buf, n, dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s),
              "cudaMemcpyAsync(pack)");
     if (!dst_on_device) CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    return CD_OK;
+    API_END
+}
+
+int cd_halo_plan_create(const cd_geometry *geom, int nranks, int rank, cd_precision prec, int32_t self_mask,
+                        cd_halo_plan *out)
+{
+    API_BEGIN
+    if (!out) return fail(CD_ERR_INVALID, "out is NULL");
+    int r = check_geometry(geom, nranks, rank);
+    if (r != CD_OK) return r;
+    if (prec != CD_FP32 && prec != CD_FP16) return fail(CD_ERR_INVALID, "bad precision");
+    if (self_mask < 0 || self_mask > 15) return fail(CD_ERR_INVALID, "self_mask must be in [0, 15]");
+    for (int mu = 0; mu < 4; mu++)
+        if (((self_mask >> mu) & 1) && geom->proc_grid[mu] != 1)
+            return fail(CD_ERR_INVALID, "self_mask dims must have proc_grid == 1");
+    make_plan(geom, rank, prec, self_mask, out);
     return CD_OK;
     API_END
 }

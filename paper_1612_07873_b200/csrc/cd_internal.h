@@ -83,6 +83,8 @@ struct cd_context {
     size_t halo_cap = 0;
     float2 *face_scratch = nullptr;   // fp32 partial y for face sites [V][N]
     int *face_sites = nullptr;        // device list of face site indices
+    int *work = nullptr;              // ring kernel ticket counters (2 ints, zero between launches);
+                                      // applies on one context must be stream-ordered
     int n_face = 0;
     bool halo_ready = false;
     cudaStream_t comm_stream = nullptr;
@@ -126,6 +128,7 @@ struct ApplyArgs {
     const void *recv;      // halo receive buffer (halo kernel)
     const int *face_sites; // halo kernel site list
     int n_face;
+    int *work;             // ring: [0] site tickets, [1] finished CTAs (reset by the last CTA)
     KGeom g;
     int nvec;
     int dagger;

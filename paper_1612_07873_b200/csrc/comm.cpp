@@ -114,19 +114,18 @@ int comm_check(Comm *c, std::string &err)
 // Exchange the packed faces (R13): block A of every split dim goes to the +mu
 // neighbour's block A, block B to the -mu neighbour's block B.  Dims whose neighbours are
 // this rank itself (P_mu = 1, forced through the halo path) are copied device-to-device.
-int halo_exchange(cd_context *ctx, const KGeom &g, size_t prec_rec, size_t scale_rec, cudaStream_t s,
-                  std::string &err)
+int halo_exchange(cd_context *ctx, const cd_halo_plan &pl, cudaStream_t s, std::string &err)
 {
     const unsigned char *send = static_cast<const unsigned char *>(ctx->send_buf);
     unsigned char *recv = static_cast<unsigned char *>(ctx->recv_buf);
     bool group = false;
     for (int mu = 0; mu < 4; mu++) {
-        if (!((g.split >> mu) & 1)) continue;
-        const size_t blk = ((size_t)g.F[mu] * (prec_rec + scale_rec) + 15) & ~size_t(15);   // R13: 16-B padded blocks
-        const int up = ctx->nbr_rank[mu][0], dn = ctx->nbr_rank[mu][1];
+        if (!((pl.split_mask >> mu) & 1)) continue;
+        const size_t blk = (size_t)pl.block_bytes[mu];
+        const int64_t offA = pl.block_offset[mu][0], offB = pl.block_offset[mu][1];
+        const int up = pl.nbr_rank[mu][0], dn = pl.nbr_rank[mu][1];
         if (up == ctx->rank && dn == ctx->rank) {
-            cudaError_t e = cudaMemcpyAsync(recv + g.blk_off[mu][0], send + g.blk_off[mu][0], 2 * blk,
-                                            cudaMemcpyDeviceToDevice, s);
+            cudaError_t e = cudaMemcpyAsync(recv + offA, send + offA, 2 * blk, cudaMemcpyDeviceToDevice, s);
             if (e != cudaSuccess) {
                 err = std::string("halo self copy: ") + cudaGetErrorString(e);
                 return CD_ERR_CUDA;
@@ -143,10 +142,10 @@ int halo_exchange(cd_context *ctx, const KGeom &g, size_t prec_rec, size_t scale
         }
         // fixed issue order: sends (A -> +mu, B -> -mu) then receives (A <- -mu, B <- +mu);
         // with P_mu = 2 both peers coincide and NCCL matches per-peer operations in order.
-        g_nccl.Send(send + g.blk_off[mu][0], blk, ncclUint8, up, ctx->comm->comm, s);
-        g_nccl.Send(send + g.blk_off[mu][1], blk, ncclUint8, dn, ctx->comm->comm, s);
-        g_nccl.Recv(recv + g.blk_off[mu][0], blk, ncclUint8, dn, ctx->comm->comm, s);
-        g_nccl.Recv(recv + g.blk_off[mu][1], blk, ncclUint8, up, ctx->comm->comm, s);
+        g_nccl.Send(send + offA, blk, ncclUint8, up, ctx->comm->comm, s);
+        g_nccl.Send(send + offB, blk, ncclUint8, dn, ctx->comm->comm, s);
+        g_nccl.Recv(recv + offA, blk, ncclUint8, dn, ctx->comm->comm, s);
+        g_nccl.Recv(recv + offB, blk, ncclUint8, up, ctx->comm->comm, s);
     }
     if (group) {
         ncclResult_t r = g_nccl.GroupEnd();

@@ -9,6 +9,5 @@ int nccl_unique_id(uint8_t out[128], std::string &err);
 int comm_create(const uint8_t id[128], int nranks, int rank, Comm **out, std::string &err);
 void comm_destroy(Comm *c);
 int comm_check(Comm *c, std::string &err);
-int halo_exchange(cd_context *ctx, const KGeom &g, size_t prec_rec, size_t scale_rec, cudaStream_t s,
-                  std::string &err);
+int halo_exchange(cd_context *ctx, const cd_halo_plan &plan, cudaStream_t s, std::string &err);
 }  // namespace cd

@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(RingCfg<P, NV>::THREADS, 1) dslash_ring(ApplyA
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
     uint64_t *empty = full + RC::MAXS;
     float *red = reinterpret_cast<float *>(smem + 16 * RC::MAXS);   // 2 x 32 floats
+    int *siteq = reinterpret_cast<int *>(smem + 16 * RC::MAXS + 256);   // site id per stage
     unsigned char *stages = smem + RC::HDR;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -109,12 +110,20 @@ __global__ void __launch_bounds__(RingCfg<P, NV>::THREADS, 1) dslash_ring(ApplyA
     pdl_trigger();
 
     if (warp == RC::NCW) {
-        // ===== producer: one elected lane streams (matrix, vector) records into the ring
+        // ===== producer: one elected lane takes sites from a global ticket counter (dynamic
+        // load balance across SMs) and streams their (matrix, vector) records into the ring.
         if (lane == 0) {
-            pdl_wait();   // `in` is written by the previous kernel in the stream
+            pdl_wait();   // `in` (and the ticket counter reset) come from the previous kernel
             int stage = 0;
             uint32_t phase = 0;
-            for (int site = blockIdx.x; site < V; site += gridDim.x) {
+            for (;;) {
+                const int site = atomicAdd(a.work, 1);
+                if (site >= V) {   // sentinel stage: tells the consumers to stop
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    *reinterpret_cast<volatile int *>(&siteq[stage]) = -1;
+                    mbar_arrive(&full[stage]);
+                    break;
+                }
                 int x[4];
                 decode(a.g, site, x);
                 const unsigned char *lsite = links + (size_t)site * 9 * Q::MREC;
@@ -123,12 +132,20 @@ __global__ void __launch_bounds__(RingCfg<P, NV>::THREADS, 1) dslash_ring(ApplyA
                     if (a.halo && remote_hop(a.g, x, k)) continue;
                     const int nb = neighbour(a.g, x, site, k);
                     mbar_wait(&empty[stage], phase ^ 1);
+                    if (i == 0) *reinterpret_cast<volatile int *>(&siteq[stage]) = site;
                     unsigned char *st = stages + (size_t)stage * RC::STAGE;
                     mbar_arrive_expect_tx(&full[stage], Q::MREC + Q::VREC);
                     bulk_g2s(st, lsite + (size_t)k * Q::MREC, Q::MREC, &full[stage]);
                     bulk_g2s(st + Q::MREC, in + (size_t)nb * Q::VREC, Q::VREC, &full[stage]);
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
+            }
+            // the last CTA to finish resets the tickets for the next launch (which reads them
+            // only after griddepcontrol.wait / stream order, i.e. after this grid completed)
+            if (atomicAdd(a.work + 1, 1) == (int)gridDim.x - 1) {
+                a.work[0] = 0;
+                a.work[1] = 0;
+                __threadfence();
             }
         }
         return;
@@ -141,15 +158,17 @@ __global__ void __launch_bounds__(RingCfg<P, NV>::THREADS, 1) dslash_ring(ApplyA
     constexpr bool ROT = (Q::ROWB % 128 == 0) && (Q::D * 16 < 128);   // fp16 N=64: avoid 2-way bank conflict
     int stage = 0;
     uint32_t phase = 0;
-    int it = 0;
-    for (int site = blockIdx.x; site < V; site += gridDim.x, ++it) {
+    for (int it = 0;; ++it) {
+        mbar_wait(&full[stage], phase);   // first stage of the next site (X, never skipped)
+        const int site = *reinterpret_cast<volatile int *>(&siteq[stage]);
+        if (site < 0) break;
         int x[4];
         decode(a.g, site, x);
         float re = 0.0f, im = 0.0f;
         for (int i = 0; i < 9; i++) {
             const int k = kseq(i);
             if (a.halo && remote_hop(a.g, x, k)) continue;
-            mbar_wait(&full[stage], phase);
+            if (i > 0) mbar_wait(&full[stage], phase);
             const unsigned char *st = stages + (size_t)stage * RC::STAGE;
             const unsigned char *mrow = st + row * Q::ROWB;
             const unsigned char *vrec = st + Q::MREC;
