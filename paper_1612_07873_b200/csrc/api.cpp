@@ -340,8 +340,11 @@ int cd_context_create(const cd_geometry *geom, int device, int nranks, int rank,
         return cuda_fail(e, "cudaGetDeviceProperties");
     }
     c->num_sms = prop.multiProcessorCount;
-    e = cudaMalloc(&c->work, 2 * sizeof(int));
-    if (e == cudaSuccess) e = cudaMemset(c->work, 0, 2 * sizeof(int));
+    e = cudaMalloc(&c->work, 8 * sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(c->work, 0, 8 * sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&c->ysplit, sizeof(float2) * c->V * c->N);
+    if (e == cudaSuccess) e = cudaMalloc(&c->site_cnt, sizeof(int) * c->V);
+    if (e == cudaSuccess) e = cudaMemset(c->site_cnt, 0, sizeof(int) * c->V);
     if (e != cudaSuccess) {
         delete c;
         return cuda_fail(e, "cudaMalloc(work)");
@@ -378,6 +381,8 @@ int cd_context_destroy(cd_context *c)
     if (c->face_scratch) cudaFree(c->face_scratch);
     if (c->face_sites) cudaFree(c->face_sites);
     if (c->work) cudaFree(c->work);
+    if (c->ysplit) cudaFree(c->ysplit);
+    if (c->site_cnt) cudaFree(c->site_cnt);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->ev_in) cudaEventDestroy(c->ev_in);
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
@@ -745,6 +750,13 @@ static int check_objs(const cd_links *l, const cd_field *out, const cd_field *in
 // Pick the kernel variant for (prec, dagger): forced > cached > tuned > heuristic.
 // Tuning (first call of a key, "auto-tuned upon first call and cached") times
 // every variant with CUDA events on the caller's stream; trial launches write `out` only.
+// Every dslash launch gets the next sequence number (the ring kernel's ticket slot).
+static cudaError_t launch_next(cd_context *c, cd_precision p, int id, ApplyArgs a, cudaStream_t s, bool pdl)
+{
+    a.seq = c->seq++;
+    return launch_dslash(p, id, a, s, pdl, c->num_sms);
+}
+
 static int resolve_variant(cd_context *c, cd_precision p, int dag, const ApplyArgs &a, cudaStream_t s, int *id)
 {
     const int nvar = variant_count(p, c->nvec);
@@ -776,13 +788,13 @@ static int resolve_variant(cd_context *c, cd_precision p, int dag, const ApplyAr
             const int reps = c->V >= 2048 ? 3 : 20;
             for (int id2 = 0; id2 < nvar; id2++) {
                 cudaError_t e = cudaSuccess;
-                for (int w = 0; w < 2 && e == cudaSuccess; w++) e = launch_dslash(p, id2, a, s, false, c->num_sms);
+                for (int w = 0; w < 2 && e == cudaSuccess; w++) e = launch_next(c, p, id2, a, s, false);
                 if (e != cudaSuccess) {
                     cudaGetLastError();
                     continue;
                 }
                 cudaEventRecord(e0, s);
-                for (int rr = 0; rr < reps && e == cudaSuccess; rr++) e = launch_dslash(p, id2, a, s, false, c->num_sms);
+                for (int rr = 0; rr < reps && e == cudaSuccess; rr++) e = launch_next(c, p, id2, a, s, false);
                 cudaEventRecord(e1, s);
                 if (e != cudaSuccess || cudaEventSynchronize(e1) != cudaSuccess) {
                     cudaGetLastError();
@@ -832,11 +844,13 @@ static int do_apply(const cd_links *l, cd_field *out, const cd_field *in, void *
     a.face_sites = c->face_sites;
     a.n_face = c->n_face;
     a.work = c->work;
+    a.ysplit = c->ysplit;
+    a.site_cnt = c->site_cnt;
     int id = 0;
     r = resolve_variant(c, l->prec, dag, a, s, &id);
     if (r != CD_OK) return r;
     if (!halo) {
-        CUDA_TRY(launch_dslash(l->prec, id, a, s, c->pdl != 0, c->num_sms), "dslash launch");
+        CUDA_TRY(launch_next(c, l->prec, id, a, s, c->pdl != 0), "dslash launch");
         return CD_OK;
     }
     // multi-rank: pack + exchange on the comm stream, interior on the caller's stream,
@@ -850,7 +864,7 @@ static int do_apply(const cd_links *l, cd_field *out, const cd_field *in, void *
         if (r != CD_OK) return fail(r, err);
     }
     CUDA_TRY(cudaEventRecord(c->ev_halo, c->comm_stream), "cudaEventRecord");
-    CUDA_TRY(launch_dslash(l->prec, id, a, s, false, c->num_sms), "dslash interior launch");
+    CUDA_TRY(launch_next(c, l->prec, id, a, s, false), "dslash interior launch");
     CUDA_TRY(cudaStreamWaitEvent(s, c->ev_halo, 0), "cudaStreamWaitEvent");
     CUDA_TRY(launch_halo(l->prec, a, s), "halo kernel");
     return CD_OK;

@@ -83,8 +83,11 @@ struct cd_context {
     size_t halo_cap = 0;
     float2 *face_scratch = nullptr;   // fp32 partial y for face sites [V][N]
     int *face_sites = nullptr;        // device list of face site indices
-    int *work = nullptr;              // ring kernel ticket counters (2 ints, zero between launches);
-                                      // applies on one context must be stream-ordered
+    int *work = nullptr;              // ring kernel ticket counters (4 slots x 2 ints, zero between
+                                      // launches); applies on one context must be stream-ordered
+    uint32_t seq = 0;                 // dslash launch sequence number
+    float2 *ysplit = nullptr;         // fp16 row-split scratch [V][N]
+    int *site_cnt = nullptr;          // fp16 row-split per-site counters [V]
     int n_face = 0;
     bool halo_ready = false;
     cudaStream_t comm_stream = nullptr;
@@ -128,7 +131,10 @@ struct ApplyArgs {
     const void *recv;      // halo receive buffer (halo kernel)
     const int *face_sites; // halo kernel site list
     int n_face;
-    int *work;             // ring: [0] site tickets, [1] finished CTAs (reset by the last CTA)
+    int *work;             // ring: 4 slots x {site tickets, finished CTAs} (reset by the last CTA)
+    uint32_t seq;          // launch sequence number (ring ticket slot = seq % 4)
+    float2 *ysplit;        // fp16 row-split fg: fp32 rows of a site [V][N] (L2 resident)
+    int *site_cnt;         // fp16 row-split fg: per-site arrival counters (zero between launches)
     KGeom g;
     int nvec;
     int dagger;

@@ -174,16 +174,22 @@ __device__ __forceinline__ int encode(const KGeom &g, const int x[4])
 {
     return ((x[3] * g.L[2] + x[2]) * g.L[1] + x[1]) * g.L[0] + x[0];
 }
-// Neighbour of x through hop k (k = 2mu + dir; k = 8 -> x), periodic (R10).
+// x[mu] for a run-time mu without dynamic register indexing (keeps x in registers).
+__device__ __forceinline__ int sel4(const int v[4], int mu)
+{
+    return mu == 0 ? v[0] : (mu == 1 ? v[1] : (mu == 2 ? v[2] : v[3]));
+}
+// Neighbour of x through hop k (k = 2mu + dir; k = 8 -> x), periodic (R10):
+// s +- stride(mu), with the wrap folded in -- no re-encode, no dynamic indexing.
 __device__ __forceinline__ int neighbour(const KGeom &g, const int x[4], int s, int k)
 {
     if (k == 8) return s;
     const int mu = k >> 1;
-    int y[4] = {x[0], x[1], x[2], x[3]};
-    int c = y[mu] + ((k & 1) ? -1 : 1);
-    c = c < 0 ? g.L[mu] - 1 : (c >= g.L[mu] ? 0 : c);
-    y[mu] = c;
-    return encode(g, y);
+    const int L = sel4(g.L, mu);
+    const int xm = sel4(x, mu);
+    const int stride = mu == 0 ? 1 : (mu == 1 ? g.L[0] : (mu == 2 ? g.L[0] * g.L[1] : g.L[0] * g.L[1] * g.L[2]));
+    if (k & 1) return xm == 0 ? s + (L - 1) * stride : s - stride;
+    return xm == L - 1 ? s - (L - 1) * stride : s + stride;
 }
 // Is hop k of x remote (its neighbour lives on another rank / in the halo)?
 __device__ __forceinline__ bool remote_hop(const KGeom &g, const int x[4], int k)
@@ -191,7 +197,8 @@ __device__ __forceinline__ bool remote_hop(const KGeom &g, const int x[4], int k
     if (k == 8) return false;
     const int mu = k >> 1;
     if (!((g.split >> mu) & 1)) return false;
-    return (k & 1) ? (x[mu] == 0) : (x[mu] == g.L[mu] - 1);
+    const int xm = sel4(x, mu);
+    return (k & 1) ? (xm == 0) : (xm == sel4(g.L, mu) - 1);
 }
 
 // Hop order inside a site: X first, then k = 0..7 (fixed term order, R11).

@@ -71,26 +71,38 @@ __device__ __forceinline__ void store_site(unsigned char *out, int site, int row
 }
 
 // ------------------------------------------------------------------ RING variant
-template <cd_precision P, int NV>
+// MPS = link matrices per ring stage.  A site's nine matrices are contiguous in HBM
+// ([site][k], k = 0..8), so a stage holding MPS of them is ONE bulk copy (plus the MPS vector
+// records they multiply): fewer, larger cp.async.bulk operations per byte (the ring was
+// measured to be bound by the bulk-copy count, profiles/r01_summary.md).
+template <cd_precision P, int NV, int MPS>
 struct RingCfg {
     using Q = Cfg<P, NV>;
     static constexpr int NCW = Q::N / Q::R;                         // consumer warps
     static constexpr int THREADS = 32 * (NCW + 1);
-    static constexpr int STAGE = ((Q::MREC + Q::VREC) + 127) / 128 * 128;
+    static constexpr int VOFF = MPS * Q::MREC;                      // vector records after the matrices
+    static constexpr int STAGE = ((MPS * (Q::MREC + Q::VREC)) + 127) / 128 * 128;
     static constexpr int HDR = 1024;                                // barriers + reduction scratch
     static constexpr int MAXS = 32;
+    static constexpr int SMEM_BUDGET = 227 * 1024;                  // the ring is latency bound: all of it
+    static constexpr int S = ((SMEM_BUDGET - HDR) / STAGE) > MAXS ? MAXS : ((SMEM_BUDGET - HDR) / STAGE);
+    static constexpr int SMEM = HDR + S * STAGE;
+    static constexpr int SLOTS = 4;                                  // ticket-counter slots (launch % 4)
+    static_assert(9 % MPS == 0, "MPS must divide 9");
 };
 
-template <cd_precision P, int NV>
-__global__ void __launch_bounds__(RingCfg<P, NV>::THREADS, 1) dslash_ring(ApplyArgs a, int S)
+template <cd_precision P, int NV, int MPS>
+__global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(ApplyArgs a, int slot)
 {
     using Q = Cfg<P, NV>;
-    using RC = RingCfg<P, NV>;
+    using RC = RingCfg<P, NV, MPS>;
+    constexpr int S = RC::S;
+    constexpr int G = 9 / MPS;                                       // stages per site
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
     uint64_t *empty = full + RC::MAXS;
-    float *red = reinterpret_cast<float *>(smem + 16 * RC::MAXS);   // 2 x 32 floats
-    int *siteq = reinterpret_cast<int *>(smem + 16 * RC::MAXS + 256);   // site id per stage
+    float *red = reinterpret_cast<float *>(smem + 16 * RC::MAXS);        // 2 x 32 floats
+    int *siteq = reinterpret_cast<int *>(smem + 16 * RC::MAXS + 256);    // site id per stage
     unsigned char *stages = smem + RC::HDR;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -98,6 +110,7 @@ __global__ void __launch_bounds__(RingCfg<P, NV>::THREADS, 1) dslash_ring(ApplyA
     const unsigned char *in = static_cast<const unsigned char *>(a.in);
     unsigned char *out = static_cast<unsigned char *>(a.out);
     const int V = a.g.V;
+    int *tickets = a.work + 2 * slot;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; s++) {
@@ -111,13 +124,15 @@ __global__ void __launch_bounds__(RingCfg<P, NV>::THREADS, 1) dslash_ring(ApplyA
 
     if (warp == RC::NCW) {
         // ===== producer: one elected lane takes sites from a global ticket counter (dynamic
-        // load balance across SMs) and streams their (matrix, vector) records into the ring.
+        // load balance across SMs) and streams their records into the ring.  Ticket slot
+        // `slot` (launch % 4) was reset by the last CTA of the launch 4 before this one, which
+        // completed before this launch's predecessor did (stream order / griddepcontrol.wait).
         if (lane == 0) {
-            pdl_wait();   // `in` (and the ticket counter reset) come from the previous kernel
+            pdl_wait();   // `in` is written by the previous kernel in the stream
             int stage = 0;
             uint32_t phase = 0;
             for (;;) {
-                const int site = atomicAdd(a.work, 1);
+                const int site = atomicAdd(tickets, 1);
                 if (site >= V) {   // sentinel stage: tells the consumers to stop
                     mbar_wait(&empty[stage], phase ^ 1);
                     *reinterpret_cast<volatile int *>(&siteq[stage]) = -1;
@@ -127,24 +142,29 @@ __global__ void __launch_bounds__(RingCfg<P, NV>::THREADS, 1) dslash_ring(ApplyA
                 int x[4];
                 decode(a.g, site, x);
                 const unsigned char *lsite = links + (size_t)site * 9 * Q::MREC;
-                for (int i = 0; i < 9; i++) {
-                    const int k = kseq(i);
-                    if (a.halo && remote_hop(a.g, x, k)) continue;
-                    const int nb = neighbour(a.g, x, site, k);
+                for (int gi = 0; gi < G; gi++) {
+                    int nvc = 0;
+#pragma unroll
+                    for (int j = 0; j < MPS; j++) nvc += !(a.halo && remote_hop(a.g, x, gi * MPS + j));
                     mbar_wait(&empty[stage], phase ^ 1);
-                    if (i == 0) *reinterpret_cast<volatile int *>(&siteq[stage]) = site;
+                    if (gi == 0) *reinterpret_cast<volatile int *>(&siteq[stage]) = site;
                     unsigned char *st = stages + (size_t)stage * RC::STAGE;
-                    mbar_arrive_expect_tx(&full[stage], Q::MREC + Q::VREC);
-                    bulk_g2s(st, lsite + (size_t)k * Q::MREC, Q::MREC, &full[stage]);
-                    bulk_g2s(st + Q::MREC, in + (size_t)nb * Q::VREC, Q::VREC, &full[stage]);
+                    mbar_arrive_expect_tx(&full[stage], MPS * Q::MREC + nvc * Q::VREC);
+                    bulk_g2s(st, lsite + (size_t)gi * MPS * Q::MREC, MPS * Q::MREC, &full[stage]);
+#pragma unroll
+                    for (int j = 0; j < MPS; j++) {
+                        const int k = gi * MPS + j;
+                        if (a.halo && remote_hop(a.g, x, k)) continue;
+                        bulk_g2s(st + RC::VOFF + j * Q::VREC, in + (size_t)neighbour(a.g, x, site, k) * Q::VREC,
+                                 Q::VREC, &full[stage]);
+                    }
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
             }
-            // the last CTA to finish resets the tickets for the next launch (which reads them
-            // only after griddepcontrol.wait / stream order, i.e. after this grid completed)
-            if (atomicAdd(a.work + 1, 1) == (int)gridDim.x - 1) {
-                a.work[0] = 0;
-                a.work[1] = 0;
+            // the last CTA to finish resets this slot's tickets (for launch + 4)
+            if (atomicAdd(tickets + 1, 1) == (int)gridDim.x - 1) {
+                tickets[0] = 0;
+                tickets[1] = 0;
                 __threadfence();
             }
         }
@@ -159,46 +179,50 @@ __global__ void __launch_bounds__(RingCfg<P, NV>::THREADS, 1) dslash_ring(ApplyA
     int stage = 0;
     uint32_t phase = 0;
     for (int it = 0;; ++it) {
-        mbar_wait(&full[stage], phase);   // first stage of the next site (X, never skipped)
+        mbar_wait(&full[stage], phase);   // first stage of the next site
         const int site = *reinterpret_cast<volatile int *>(&siteq[stage]);
         if (site < 0) break;
         int x[4];
         decode(a.g, site, x);
         float re = 0.0f, im = 0.0f;
-        for (int i = 0; i < 9; i++) {
-            const int k = kseq(i);
-            if (a.halo && remote_hop(a.g, x, k)) continue;
-            if (i > 0) mbar_wait(&full[stage], phase);
+        for (int gi = 0; gi < G; gi++) {
+            if (gi > 0) mbar_wait(&full[stage], phase);
             const unsigned char *st = stages + (size_t)stage * RC::STAGE;
-            const unsigned char *mrow = st + row * Q::ROWB;
-            const unsigned char *vrec = st + Q::MREC;
-            if constexpr (P == CD_FP32) {
-                float pr[Q::C], pi[Q::C];
 #pragma unroll
-                for (int c = 0; c < Q::C; c++) {
-                    pr[c] = 0.0f;
-                    pi[c] = 0.0f;
-                    const int q = d + Q::D * c;
-                    uint4 vq = lds128(vrec + q * 16);
-                    if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<false>(vq);
-                    cmac2(lds128(mrow + q * 16), vq, pr[c], pi[c]);
+            for (int j = 0; j < MPS; j++) {
+                const int k = gi * MPS + j;
+                if (a.halo && remote_hop(a.g, x, k)) continue;
+                const unsigned char *mrec = st + j * Q::MREC;
+                const unsigned char *mrow = mrec + row * Q::ROWB;
+                const unsigned char *vrec = st + RC::VOFF + j * Q::VREC;
+                if constexpr (P == CD_FP32) {
+                    float pr[Q::C], pi[Q::C];
+#pragma unroll
+                    for (int c = 0; c < Q::C; c++) {
+                        pr[c] = 0.0f;
+                        pi[c] = 0.0f;
+                        const int q = d + Q::D * c;
+                        uint4 vq = lds128(vrec + q * 16);
+                        if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<false>(vq);
+                        cmac2(lds128(mrow + q * 16), vq, pr[c], pi[c]);
+                    }
+#pragma unroll
+                    for (int c = 0; c < Q::C; c++) { re += pr[c]; im += pi[c]; }
+                } else {
+                    float ra = 0.f, rb = 0.f, ia = 0.f, ib = 0.f;
+#pragma unroll
+                    for (int c = 0; c < Q::C; c++) {
+                        const int cc = ROT ? ((c + (r & 1)) % Q::C) : c;
+                        const int q = d + Q::D * cc;
+                        uint4 vq = lds128(vrec + q * 16);
+                        if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<true>(vq);
+                        hmac4(lds128(mrow + q * 16), vq, ra, rb, ia, ib);
+                    }
+                    const float sc = *reinterpret_cast<const float *>(mrec + Q::MSCALE) *
+                                     *reinterpret_cast<const float *>(vrec + Q::VSCALE);
+                    re = fmaf(ra - rb, sc, re);
+                    im = fmaf(ia + ib, sc, im);
                 }
-#pragma unroll
-                for (int c = 0; c < Q::C; c++) { re += pr[c]; im += pi[c]; }
-            } else {
-                float ra = 0.f, rb = 0.f, ia = 0.f, ib = 0.f;
-#pragma unroll
-                for (int c = 0; c < Q::C; c++) {
-                    const int cc = ROT ? ((c + (r & 1)) % Q::C) : c;
-                    const int q = d + Q::D * cc;
-                    uint4 vq = lds128(vrec + q * 16);
-                    if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<true>(vq);
-                    hmac4(lds128(mrow + q * 16), vq, ra, rb, ia, ib);
-                }
-                const float sc = *reinterpret_cast<const float *>(st + Q::MSCALE) *
-                                 *reinterpret_cast<const float *>(vrec + Q::VSCALE);
-                re = fmaf(ra - rb, sc, re);
-                im = fmaf(ia + ib, sc, im);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
@@ -230,8 +254,10 @@ struct FgCfg {
     static constexpr int NRB = Q::N / ROWS;
     static_assert(WK * KW == 9, "KW must divide 9");
     static_assert(NRB * ROWS == Q::N, "row blocks must tile N");
-    static_assert(P == CD_FP32 || NRB == 1, "fp16 output needs the whole site in one CTA");
     static_assert(NW <= 32, "too many warps");
+    // fp16 output with the site split over NRB CTAs: the last CTA to finish quantises it
+    static constexpr bool SPLIT16 = (P == CD_FP16) && NRB > 1;
+    static_assert(!SPLIT16 || THREADS >= Q::N, "the finishing CTA needs a thread per row");
 };
 
 template <cd_precision P, int NV, int KW, int WR>
@@ -340,7 +366,25 @@ __global__ void __launch_bounds__(FgCfg<P, NV, KW, WR>::THREADS) dslash_fg(Apply
         return;
     }
     const float sg = (a.dagger && orow >= NV) ? -1.0f : 1.0f;
-    store_site<P, NV>(out, site, orow, owner, sg * yr, sg * yi, red, F::THREADS, -1);
+    if constexpr (F::SPLIT16) {
+        // fp16 storage needs the whole site's max |y| (R12): every row block parks its
+        // fp32 rows in an L2-resident scratch; the last CTA of the site (per-site arrival
+        // counter, reset by that CTA) quantises all N rows.  No atomics on data, deterministic.
+        __shared__ int last;
+        if (owner) a.ysplit[(size_t)site * Q::N + orow] = make_float2(sg * yr, sg * yi);
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) last = (atomicAdd(&a.site_cnt[site], 1) == F::NRB - 1);
+        __syncthreads();
+        if (!last) return;
+        __threadfence();
+        const bool own = threadIdx.x < Q::N;
+        const float2 v = own ? __ldcg(&a.ysplit[(size_t)site * Q::N + threadIdx.x]) : make_float2(0.f, 0.f);
+        if (threadIdx.x == 0) a.site_cnt[site] = 0;
+        store_site<P, NV>(out, site, own ? threadIdx.x : 0, own, v.x, v.y, red, F::THREADS, -1);
+    } else {
+        store_site<P, NV>(out, site, orow, owner, sg * yr, sg * yi, red, F::THREADS, -1);
+    }
 }
 
 // ------------------------------------------------------------------ halo term (multi-rank)
@@ -449,7 +493,7 @@ __global__ void halo_pack(const unsigned char *field, unsigned char *send, KGeom
 
 // ------------------------------------------------------------------ variant table
 struct VDesc {
-    int kind;  // 0 = ring, 1 = fg
+    int kind;  // 0 = ring (kw = matrices per stage), 1 = fg (kw hops per warp, wr row-warps)
     int kw, wr;
 };
 
@@ -457,25 +501,27 @@ template <cd_precision P, int NV>
 struct Variants;
 template <>
 struct Variants<CD_FP32, 24> {
-    static constexpr int n = 10;
-    static constexpr VDesc v[n] = {{0, 0, 0}, {1, 1, 1}, {1, 1, 2}, {1, 1, 3}, {1, 3, 2},
-                                   {1, 3, 4}, {1, 3, 6}, {1, 9, 3}, {1, 9, 6}, {1, 9, 12}};
+    static constexpr int n = 11;
+    static constexpr VDesc v[n] = {{0, 1, 0}, {1, 1, 1}, {1, 1, 2}, {1, 1, 3}, {1, 3, 2}, {1, 3, 4},
+                                   {1, 3, 6}, {1, 9, 3}, {1, 9, 6}, {1, 9, 12}, {0, 3, 0}};
 };
 template <>
 struct Variants<CD_FP32, 32> {
     static constexpr int n = 9;
-    static constexpr VDesc v[n] = {{0, 0, 0}, {1, 1, 1}, {1, 1, 2}, {1, 3, 2}, {1, 3, 4},
-                                   {1, 3, 8}, {1, 9, 4}, {1, 9, 8}, {1, 9, 16}};
+    static constexpr VDesc v[n] = {{0, 1, 0}, {1, 1, 1}, {1, 1, 2}, {1, 3, 2}, {1, 3, 4},
+                                   {1, 3, 8}, {1, 9, 4}, {1, 9, 8}, {0, 3, 0}};
 };
 template <>
 struct Variants<CD_FP16, 24> {
-    static constexpr int n = 3;
-    static constexpr VDesc v[n] = {{0, 0, 0}, {1, 3, 6}, {1, 9, 6}};
+    static constexpr int n = 11;
+    static constexpr VDesc v[n] = {{0, 1, 0}, {1, 3, 6}, {1, 9, 6}, {1, 1, 1}, {1, 1, 2}, {1, 3, 2},
+                                   {1, 3, 3}, {1, 9, 2}, {1, 9, 3}, {0, 3, 0}, {0, 9, 0}};
 };
 template <>
 struct Variants<CD_FP16, 32> {
-    static constexpr int n = 3;
-    static constexpr VDesc v[n] = {{0, 0, 0}, {1, 3, 8}, {1, 9, 8}};
+    static constexpr int n = 9;
+    static constexpr VDesc v[n] = {{0, 1, 0}, {1, 3, 8}, {1, 9, 8}, {1, 1, 1}, {1, 1, 2},
+                                   {1, 3, 2}, {1, 3, 4}, {1, 9, 4}, {0, 3, 0}};
 };
 
 template <cd_precision P, int NV>
@@ -486,7 +532,7 @@ inline const char *variant_name_t(int id)
     if (!init) {
         for (int i = 0; i < Variants<P, NV>::n; i++) {
             const VDesc &v = Variants<P, NV>::v[i];
-            if (v.kind == 0) snprintf(names[i], 48, "ring_tma_%s_nv%d", P == CD_FP32 ? "f32" : "f16", NV);
+            if (v.kind == 0) snprintf(names[i], 48, "ring_tma_m%d_%s_nv%d", v.kw, P == CD_FP32 ? "f32" : "f16", NV);
             else snprintf(names[i], 48, "fg_kw%d_wr%d_%s_nv%d", v.kw, v.wr, P == CD_FP32 ? "f32" : "f16", NV);
         }
         init = true;
@@ -510,31 +556,23 @@ inline cudaError_t launch_ex(const void *fn, dim3 grid, dim3 block, size_t smem,
     return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
-template <cd_precision P, int NV>
-inline int ring_stages()
-{
-    using RC = RingCfg<P, NV>;
-    int s = (227 * 1024 - RC::HDR) / RC::STAGE;
-    return s > RC::MAXS ? RC::MAXS : s;
-}
-
-template <cd_precision P, int NV>
+template <cd_precision P, int NV, int MPS>
 cudaError_t launch_ring(const ApplyArgs &a, cudaStream_t s, bool pdl, int num_sms)
 {
-    using RC = RingCfg<P, NV>;
+    using RC = RingCfg<P, NV, MPS>;
+    static_assert(RC::S >= 2, "ring needs at least two stages");
     static bool attr = false;
-    const int S = ring_stages<P, NV>();
-    const size_t smem = RC::HDR + (size_t)S * RC::STAGE;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(dslash_ring<P, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e =
+            cudaFuncSetAttribute(dslash_ring<P, NV, MPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, RC::SMEM);
         if (e != cudaSuccess) return e;
         attr = true;
     }
     int grid = a.g.V < num_sms ? a.g.V : num_sms;
     ApplyArgs aa = a;
-    int SS = S;
-    void *args[] = {&aa, &SS};
-    return launch_ex((const void *)dslash_ring<P, NV>, dim3(grid), dim3(RC::THREADS), smem, s, pdl, args);
+    int slot = a.seq & (RC::SLOTS - 1);
+    void *args[] = {&aa, &slot};
+    return launch_ex((const void *)dslash_ring<P, NV, MPS>, dim3(grid), dim3(RC::THREADS), RC::SMEM, s, pdl, args);
 }
 
 template <cd_precision P, int NV, int KW, int WR>
@@ -555,7 +593,7 @@ cudaError_t dispatch_variant(int id, const ApplyArgs &a, cudaStream_t s, bool pd
     } else {
         if (id == I) {
             constexpr VDesc v = Variants<P, NV>::v[I];
-            if constexpr (v.kind == 0) return launch_ring<P, NV>(a, s, pdl, num_sms);
+            if constexpr (v.kind == 0) return launch_ring<P, NV, v.kw>(a, s, pdl, num_sms);
             else return launch_fg<P, NV, v.kw, v.wr>(a, s, pdl);
         }
         return dispatch_variant<P, NV, I + 1>(id, a, s, pdl, num_sms);
