@@ -120,7 +120,7 @@ def oracle_time_per_site(nvec, dims=(4, 4, 4, 4)):
     return (time.perf_counter() - t0) / (dims[0] * dims[1] * dims[2] * dims[3])
 
 
-def cpu_baseline(nvec, budget_s=15.0, dims=(8, 8, 8, 2)):
+def cpu_baseline(nvec, budget_s=15.0, dims=(8, 8, 8, 8)):
     """float64 oracle apply on a periodic sub-lattice, repeated for ~budget_s seconds."""
     from paper_1612_07873_b200 import perfmodel  # model only; no library call
     oracle, synth, cores = _oracle_setup(nvec)
@@ -133,13 +133,13 @@ def cpu_baseline(nvec, budget_s=15.0, dims=(8, 8, 8, 2)):
         v = oracle.apply(dims, L, v)
         reps += 1
         el = time.perf_counter() - t0
-        if (el >= budget_s and reps >= 3) or reps >= 1000:
+        if (el >= budget_s and reps >= 3) or reps >= 100000:
             break
     V = dims[0] * dims[1] * dims[2] * dims[3]
     gflops = perfmodel.flops_per_site(nvec) * V * reps / el / 1e9
     return {"value": round(gflops, 3), "unit": "GFLOPS", "cores": cores, "kind": "oracle",
-            "sample": f"{reps} float64 oracle applies on a periodic {'x'.join(map(str, dims))} sub-lattice "
-                      f"({V} sites, Nvec={nvec}; same per-site work as the 8^4 workload), {el:.1f} s",
+            "sample": f"{reps} chained float64 oracle applies of a periodic {'x'.join(map(str, dims))} lattice "
+                      f"({V} sites, Nvec={nvec}), {el:.1f} s on {cores} threads",
             "gbs_fp64": round(perfmodel.metric_bytes_per_site(nvec, 'fp64') * V * reps / el / 1e9, 3)}
 
 
@@ -179,12 +179,13 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(prec):
+def ncu_traffic(prec, variant):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel from the
-    committed ncu --set full capture (profiles/ncu_traffic.json), or None."""
+    committed ncu --set full capture (profiles/ncu_traffic.json) -- only if that capture is of
+    the variant this run chose -- else None."""
     try:
-        t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        return t.get(f"8^4_nvec24_{prec}")
+        t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[f"8^4_nvec24_{prec}"]
+        return t["bytes"] if variant in t["kernel"] else None
     except Exception:
         return None
 
@@ -285,7 +286,7 @@ def run_ours(args):
 
     if rank == 0:
         variant = ctx.variants(prec)[ctx.chosen_variant(prec)]
-        traffic = ncu_traffic(prec)
+        traffic = ncu_traffic(prec, variant)
         out = {
             "metric": "coarse-Dslash GFLOPS and HBM GB/s (% of B200 roofline)",
             "value": round(gflops, 2),
