@@ -199,6 +199,16 @@ int coarse_dslash_apply(const cd_links *links, cd_field *out, const cd_field *in
 /* out = tau3 D tau3 in  (= D^H in for tau3-hermitian links; R5). */
 int coarse_dslash_apply_dagger(const cd_links *links, cd_field *out, const cd_field *in, void *stream);
 
+/* n chained applies in ONE persistent kernel (latency regime: the coarsest grid, where the
+ * operator is applied over and over): for t = 0..n-1, t even: y = D x, t odd: x = D y (with
+ * dagger != 0: the tau3 dagger).  The result of the last apply is in y for odd n, in x for
+ * even n.  CTAs keep their link rows on chip for all n applies and synchronise point to point
+ * (per-site counters) instead of through kernel boundaries (the 2^4 lattice is
+ * latency bound).  Single-rank contexts only; the first call per (precision, dagger) tunes
+ * (host sync).  CD_ERR_UNSUPPORTED if the decomposition does not fit co-resident on the GPU
+ * (use coarse_dslash_apply for large lattices). */
+int coarse_dslash_apply_chain(const cd_links *links, cd_field *x, cd_field *y, int n, int dagger, void *stream);
+
 /* Halo send buffer of `in` in the canonical wire order (R13): packs on `stream`
  * and copies to dst (host or device).  *bytes receives the size; dst may be NULL to query. */
 int coarse_halo_pack(cd_context *ctx, const cd_field *in, void *dst, int dst_on_device, size_t *bytes,

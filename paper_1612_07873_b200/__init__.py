@@ -40,6 +40,7 @@ EXPORTS = (
     "coarse_field_stored_bytes", "coarse_field_read_stored", "coarse_links_upload", "coarse_links_generate",
     "coarse_links_stored_bytes", "coarse_links_read_stored", "coarse_links_free", "coarse_dslash_apply",
     "coarse_dslash_apply_dagger", "coarse_halo_pack", "cd_flush_l2", "cd_halo_plan_create",
+    "coarse_dslash_apply_chain",
 )
 
 
@@ -100,6 +101,7 @@ def _load():
         "coarse_halo_pack": ([P, P, P, I, ctypes.POINTER(SZ), P], I),
         "cd_flush_l2": ([P, SZ, P], I),
         "cd_halo_plan_create": ([ctypes.POINTER(_Geometry), I, I, I, ctypes.c_int32, ctypes.POINTER(HaloPlan)], I),
+        "coarse_dslash_apply_chain": ([P, P, P, I, I, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -231,6 +233,11 @@ def coarse_dslash_apply_dagger(links, out, in_, stream=None):
     _check(lib.coarse_dslash_apply_dagger(links, out, in_, _stream(stream)))
 
 
+def coarse_dslash_apply_chain(links, x, y, n, dagger=False, stream=None):
+    """n chained applies in one persistent kernel: t even y = D x, t odd x = D y."""
+    _check(lib.coarse_dslash_apply_chain(links, x, y, int(n), int(bool(dagger)), _stream(stream)))
+
+
 # ------------------------------------------------------------------ classes
 class Context:
     """A lattice geometry on one GPU (one rank of a process grid)."""
@@ -358,6 +365,9 @@ class Links:
 
     def apply_dagger(self, out: Field, in_: Field, stream=None):
         coarse_dslash_apply_dagger(self.handle, out.handle, in_.handle, stream)
+
+    def apply_chain(self, x: Field, y: Field, n: int, dagger=False, stream=None):
+        coarse_dslash_apply_chain(self.handle, x.handle, y.handle, n, dagger, stream)
 
     def read_stored(self, stream=None) -> bytes:
         n = int(lib.coarse_links_stored_bytes(self.handle))

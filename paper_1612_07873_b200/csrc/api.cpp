@@ -96,6 +96,17 @@ cudaError_t launch_halo(cd_precision p, const ApplyArgs &a, cudaStream_t s)
     return PICK(p, a.nvec, launch_halo_f32_24(a, s), launch_halo_f32_32(a, s), launch_halo_f16_24(a, s),
                 launch_halo_f16_32(a, s));
 }
+cudaError_t launch_chain_f32_24(int, const ApplyArgs &, int, unsigned, cudaStream_t, int, int *);
+cudaError_t launch_chain_f32_32(int, const ApplyArgs &, int, unsigned, cudaStream_t, int, int *);
+cudaError_t launch_chain_f16_24(int, const ApplyArgs &, int, unsigned, cudaStream_t, int, int *);
+cudaError_t launch_chain_f16_32(int, const ApplyArgs &, int, unsigned, cudaStream_t, int, int *);
+cudaError_t launch_chain(cd_precision p, int id, const ApplyArgs &a, int n, unsigned base, cudaStream_t s, int sms,
+                         int *nrb)
+{
+    return PICK(p, a.nvec, launch_chain_f32_24(id, a, n, base, s, sms, nrb),
+                launch_chain_f32_32(id, a, n, base, s, sms, nrb), launch_chain_f16_24(id, a, n, base, s, sms, nrb),
+                launch_chain_f16_32(id, a, n, base, s, sms, nrb));
+}
 cudaError_t launch_pack(cd_precision p, int nv, const void *f, void *d, const KGeom &g, cudaStream_t s)
 {
     return PICK(p, nv, launch_pack_f32_24(f, d, g, s), launch_pack_f32_32(f, d, g, s), launch_pack_f16_24(f, d, g, s),
@@ -345,6 +356,8 @@ int cd_context_create(const cd_geometry *geom, int device, int nranks, int rank,
     if (e == cudaSuccess) e = cudaMalloc(&c->ysplit, sizeof(float2) * c->V * c->N);
     if (e == cudaSuccess) e = cudaMalloc(&c->site_cnt, sizeof(int) * c->V);
     if (e == cudaSuccess) e = cudaMemset(c->site_cnt, 0, sizeof(int) * c->V);
+    if (e == cudaSuccess) e = cudaMalloc(&c->chain_cnt, sizeof(unsigned) * c->V);
+    if (e == cudaSuccess) e = cudaMemset(c->chain_cnt, 0, sizeof(unsigned) * c->V);
     if (e != cudaSuccess) {
         delete c;
         return cuda_fail(e, "cudaMalloc(work)");
@@ -383,6 +396,7 @@ int cd_context_destroy(cd_context *c)
     if (c->work) cudaFree(c->work);
     if (c->ysplit) cudaFree(c->ysplit);
     if (c->site_cnt) cudaFree(c->site_cnt);
+    if (c->chain_cnt) cudaFree(c->chain_cnt);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->ev_in) cudaEventDestroy(c->ev_in);
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
@@ -846,6 +860,7 @@ static int do_apply(const cd_links *l, cd_field *out, const cd_field *in, void *
     a.work = c->work;
     a.ysplit = c->ysplit;
     a.site_cnt = c->site_cnt;
+    a.chain_cnt = c->chain_cnt;
     int id = 0;
     r = resolve_variant(c, l->prec, dag, a, s, &id);
     if (r != CD_OK) return r;
@@ -881,6 +896,94 @@ int coarse_dslash_apply_dagger(const cd_links *l, cd_field *out, const cd_field 
 {
     API_BEGIN
     return do_apply(l, out, in, stream, 1);
+    API_END
+}
+
+// One chain launch of variant `id`; advances the context's counter base on success.
+static cudaError_t chain_launch(cd_context *c, cd_precision p, int id, const ApplyArgs &a, int n, cudaStream_t s)
+{
+    int nrb = 0;
+    cudaError_t e = launch_chain(p, id, a, n, c->chain_base, s, c->num_sms, &nrb);
+    if (e == cudaSuccess) c->chain_base += (unsigned)(n * nrb);
+    return e;
+}
+
+int coarse_dslash_apply_chain(const cd_links *l, cd_field *x, cd_field *y, int n, int dagger, void *stream)
+{
+    API_BEGIN
+    int r = check_objs(l, y, x);
+    if (r != CD_OK) return r;
+    if (n < 0) return fail(CD_ERR_INVALID, "n must be >= 0");
+    cd_context *c = l->ctx;
+    if (c->kg.split != 0) return fail(CD_ERR_UNSUPPORTED, "apply_chain is single-rank (no halo split)");
+    if (n == 0) return CD_OK;
+    cudaStream_t s = S(stream);
+    c->applied = true;
+    ApplyArgs a{};
+    a.links = l->base;
+    a.in = x->base;
+    a.out = y->base;
+    a.nvec = c->nvec;
+    a.dagger = dagger ? 1 : 0;
+    a.g = c->kg;
+    a.chain_cnt = c->chain_cnt;
+    const cd_precision p = l->prec;
+    const TuneKey key{(int)p, 2 + a.dagger};
+    int id = -1;
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        auto it = c->chosen.find(key);
+        if (it != c->chosen.end()) id = it->second;
+    }
+    if (c->force_variant >= 0) id = c->force_variant;
+    if (id < 0) {
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(s, &cap);
+        if (cap != cudaStreamCaptureStatusNone) return fail(CD_ERR_INVALID, "tune apply_chain before capturing it");
+        // tune: time a short chain of every fine-grained variant that fits co-resident, on
+        // scratch fields (a chain writes both of its buffers; the caller's x must survive)
+        const size_t fb = coarse_field_bytes(c, p);
+        void *scratch = nullptr;
+        CUDA_TRY(cudaMallocAsync(&scratch, 2 * fb, s), "cudaMallocAsync(tune scratch)");
+        CUDA_TRY(cudaMemsetAsync(scratch, 0, 2 * fb, s), "cudaMemsetAsync");
+        ApplyArgs ta = a;
+        ta.in = scratch;
+        ta.out = static_cast<unsigned char *>(scratch) + fb;
+        cudaEvent_t e0, e1;
+        CUDA_TRY(cudaEventCreate(&e0), "event");
+        CUDA_TRY(cudaEventCreate(&e1), "event");
+        float best = 1e30f;
+        const int trial = 64;
+        for (int v = 0; v < variant_count(p, c->nvec); v++) {
+            if (chain_launch(c, p, v, ta, 2, s) != cudaSuccess) {
+                cudaGetLastError();
+                continue;
+            }
+            cudaEventRecord(e0, s);
+            cudaError_t e = chain_launch(c, p, v, ta, trial, s);
+            cudaEventRecord(e1, s);
+            if (e != cudaSuccess || cudaEventSynchronize(e1) != cudaSuccess) {
+                cudaGetLastError();
+                continue;
+            }
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (ms < best) best = ms, id = v;
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaFreeAsync(scratch, s);
+        if (id < 0) return fail(CD_ERR_UNSUPPORTED, "no chain variant fits this lattice co-resident");
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->chosen[key] = id;
+    }
+    cudaError_t e = chain_launch(c, p, id, a, n, s);
+    if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        return fail(CD_ERR_UNSUPPORTED, "chain variant does not fit co-resident / not a chain variant");
+    }
+    CUDA_TRY(e, "chain launch");
+    return CD_OK;
     API_END
 }
 

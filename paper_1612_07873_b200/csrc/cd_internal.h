@@ -88,6 +88,8 @@ struct cd_context {
     uint32_t seq = 0;                 // dslash launch sequence number
     float2 *ysplit = nullptr;         // fp16 row-split scratch [V][N]
     int *site_cnt = nullptr;          // fp16 row-split per-site counters [V]
+    unsigned *chain_cnt = nullptr;    // chain kernel per-site counters [V] (monotonic)
+    unsigned chain_base = 0;          // value every chain counter holds between chain calls
     int n_face = 0;
     bool halo_ready = false;
     cudaStream_t comm_stream = nullptr;
@@ -135,6 +137,7 @@ struct ApplyArgs {
     uint32_t seq;          // launch sequence number (ring ticket slot = seq % 4)
     float2 *ysplit;        // fp16 row-split fg: fp32 rows of a site [V][N] (L2 resident)
     int *site_cnt;         // fp16 row-split fg: per-site arrival counters (zero between launches)
+    unsigned *chain_cnt;   // chain kernel: monotonic per-site completion counters
     KGeom g;
     int nvec;
     int dagger;

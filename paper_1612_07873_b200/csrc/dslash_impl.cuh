@@ -387,6 +387,134 @@ __global__ void __launch_bounds__(FgCfg<P, NV, KW, WR>::THREADS) dslash_fg(Apply
     }
 }
 
+// ------------------------------------------------------------------ CHAIN variant (latency regime)
+// n chained applies (t even: y = D x, t odd: x = D y) in ONE cooperative launch.  The CTA grid
+// is the FG decomposition; every CTA keeps its link rows in registers for all n applies (the
+// whole 2^4 operator is 2.7 MB spread over the SMs) and waits point-to-point for the nine
+// neighbour sites of the previous apply through per-site counters (release / acquire at gpu
+// scope) -- no kernel boundary and no grid-wide barrier between applies.  Waiting for the
+// neighbours' counters covers both hazards: their outputs (RAW) and their reads of the buffer
+// this CTA is about to overwrite (WAR; the stencil is symmetric).  Counters are monotonic; the
+// host passes the base value.
+__device__ __forceinline__ uint4 ld_cg(const void *p)
+{
+    uint4 r;
+    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p)
+{
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <cd_precision P, int NV, int KW, int WR>
+__global__ void __launch_bounds__(FgCfg<P, NV, KW, WR>::THREADS) dslash_chain(ApplyArgs a, int n, unsigned base)
+{
+    using Q = Cfg<P, NV>;
+    using F = FgCfg<P, NV, KW, WR>;
+    static_assert(!F::SPLIT16, "fp16 chain needs whole-site CTAs");
+    __shared__ __align__(16) unsigned char vs[9 * Q::VREC];
+    __shared__ float2 part[F::WK][F::ROWS];
+    __shared__ float red[32];
+
+    const int site = blockIdx.x / F::NRB, rb = blockIdx.x - site * F::NRB;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wk = warp / WR, wr = warp - wk * WR;
+    const int r = lane / Q::D, d = lane % Q::D;
+    const int rowl = wr * Q::R + r, row = rb * F::ROWS + rowl;
+    const unsigned char *links = static_cast<const unsigned char *>(a.links);
+    unsigned char *const buf0 = const_cast<unsigned char *>(static_cast<const unsigned char *>(a.in));
+    unsigned char *const buf1 = static_cast<unsigned char *>(a.out);
+    unsigned *cnt = a.chain_cnt;
+
+    int x[4];
+    decode(a.g, site, x);
+    uint4 Lc[KW][Q::C];
+    float sl[KW];
+#pragma unroll
+    for (int kk = 0; kk < KW; kk++) {
+        const int k = kseq(wk * KW + kk);
+        const unsigned char *m = links + ((size_t)site * 9 + k) * Q::MREC;
+#pragma unroll
+        for (int c = 0; c < Q::C; c++) Lc[kk][c] = ld_stream(m + row * Q::ROWB + (d + Q::D * c) * 16);
+        sl[kk] = Q::F16 ? ld_nc_f32(m + Q::MSCALE) : 0.0f;
+    }
+    const int t9 = threadIdx.x < 9 ? neighbour(a.g, x, site, threadIdx.x) : 0;
+
+    for (int t = 0; t < n; t++) {
+        const unsigned char *in = (t & 1) ? buf1 : buf0;
+        unsigned char *out = (t & 1) ? buf0 : buf1;
+        if (t > 0 && threadIdx.x < 9) {   // neighbours (and self) finished apply t-1
+            const unsigned target = base + (unsigned)(t * F::NRB);
+            while ((int)(ld_acquire(&cnt[t9]) - target) < 0) {
+            }
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < 9 * Q::VCH; e += F::THREADS) {
+            const int k = e / Q::VCH, c16 = e - k * Q::VCH;
+            const int nb = neighbour(a.g, x, site, k);
+            *reinterpret_cast<uint4 *>(vs + k * Q::VREC + c16 * 16) = ld_cg(in + (size_t)nb * Q::VREC + c16 * 16);
+        }
+        __syncthreads();
+        float re = 0.0f, im = 0.0f;
+#pragma unroll
+        for (int kk = 0; kk < KW; kk++) {
+            const int k = kseq(wk * KW + kk);
+            const unsigned char *vrec = vs + k * Q::VREC;
+            if constexpr (P == CD_FP32) {
+                float pr[Q::C], pi[Q::C];
+#pragma unroll
+                for (int c = 0; c < Q::C; c++) {
+                    pr[c] = 0.0f;
+                    pi[c] = 0.0f;
+                    const int q = d + Q::D * c;
+                    uint4 vq = lds128(vrec + q * 16);
+                    if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<false>(vq);
+                    cmac2(Lc[kk][c], vq, pr[c], pi[c]);
+                }
+#pragma unroll
+                for (int c = 0; c < Q::C; c++) { re += pr[c]; im += pi[c]; }
+            } else {
+                float ra = 0.f, rb2 = 0.f, ia = 0.f, ib = 0.f;
+#pragma unroll
+                for (int c = 0; c < Q::C; c++) {
+                    const int q = d + Q::D * c;
+                    uint4 vq = lds128(vrec + q * 16);
+                    if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<true>(vq);
+                    hmac4(Lc[kk][c], vq, ra, rb2, ia, ib);
+                }
+                const float sc = sl[kk] * *reinterpret_cast<const float *>(vrec + Q::VSCALE);
+                re = fmaf(ra - rb2, sc, re);
+                im = fmaf(ia + ib, sc, im);
+            }
+        }
+#pragma unroll
+        for (int m = Q::D / 2; m >= 1; m >>= 1) {
+            re += shfl_xor(re, m);
+            im += shfl_xor(im, m);
+        }
+        if (d == 0) part[wk][rowl] = make_float2(re, im);
+        __syncthreads();
+        const bool owner = threadIdx.x < F::ROWS;
+        float yr = 0.0f, yi = 0.0f;
+        if (owner) {
+#pragma unroll
+            for (int w = 0; w < F::WK; w++) {
+                yr += part[w][threadIdx.x].x;
+                yi += part[w][threadIdx.x].y;
+            }
+        }
+        const int orow = rb * F::ROWS + (owner ? threadIdx.x : 0);
+        const float sg = (a.dagger && orow >= NV) ? -1.0f : 1.0f;
+        store_site<P, NV>(out, site, orow, owner, sg * yr, sg * yi, red, F::THREADS, -1);
+        __syncthreads();
+        if (threadIdx.x == 0)   // publish: this row block finished apply t (release, gpu scope)
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&cnt[site]) : "memory");
+    }
+}
+
 // ------------------------------------------------------------------ halo term (multi-rank)
 // One CTA per face site: y(x) = partial(x) + sum over remote hops L_k(x) v_halo, then the
 // final store (fp16: whole-site re-quantisation).  Neighbour records come from the receive
@@ -540,18 +668,21 @@ inline const char *variant_name_t(int id)
     return (id >= 0 && id < Variants<P, NV>::n) ? names[id] : nullptr;
 }
 
-inline cudaError_t launch_ex(const void *fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl, void **args)
+inline cudaError_t launch_ex(const void *fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl, void **args,
+                             bool cooperative = false)
 {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    at[1].id = cudaLaunchAttributeCooperative;   // all CTAs co-resident (or the launch fails)
+    at[1].val.cooperative = cooperative ? 1 : 0;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     count_launch();
     return cudaLaunchKernelExC(&cfg, fn, args);
 }
@@ -583,6 +714,45 @@ cudaError_t launch_fg(const ApplyArgs &a, cudaStream_t s, bool pdl)
     void *args[] = {&aa};
     return launch_ex((const void *)dslash_fg<P, NV, KW, WR>, dim3((unsigned)(a.g.V * F::NRB)), dim3(F::THREADS), 0, s,
                      pdl, args);
+}
+
+template <cd_precision P, int NV, int KW, int WR>
+cudaError_t launch_chain_t(const ApplyArgs &a, int n, unsigned base, cudaStream_t s, int num_sms)
+{
+    using F = FgCfg<P, NV, KW, WR>;
+    if constexpr (F::SPLIT16) {
+        return cudaErrorNotSupported;
+    } else {
+        int per_sm = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dslash_chain<P, NV, KW, WR>, F::THREADS, 0);
+        if (e != cudaSuccess) return e;
+        if ((int64_t)a.g.V * F::NRB > (int64_t)per_sm * num_sms) return cudaErrorCooperativeLaunchTooLarge;
+        ApplyArgs aa = a;
+        int nn = n;
+        unsigned bb = base;
+        void *args[] = {&aa, &nn, &bb};
+        return launch_ex((const void *)dslash_chain<P, NV, KW, WR>, dim3((unsigned)(a.g.V * F::NRB)), dim3(F::THREADS),
+                         0, s, false, args, true);
+    }
+}
+
+template <cd_precision P, int NV, int I>
+cudaError_t dispatch_chain(int id, const ApplyArgs &a, int n, unsigned base, cudaStream_t s, int num_sms, int *nrb)
+{
+    if constexpr (I >= Variants<P, NV>::n) {
+        return cudaErrorInvalidValue;
+    } else {
+        if (id == I) {
+            constexpr VDesc v = Variants<P, NV>::v[I];
+            if constexpr (v.kind == 0) {
+                return cudaErrorNotSupported;
+            } else {
+                *nrb = FgCfg<P, NV, v.kw, v.wr>::NRB;
+                return launch_chain_t<P, NV, v.kw, v.wr>(a, n, base, s, num_sms);
+            }
+        }
+        return dispatch_chain<P, NV, I + 1>(id, a, n, base, s, num_sms, nrb);
+    }
 }
 
 template <cd_precision P, int NV, int I>
@@ -636,6 +806,11 @@ cudaError_t launch_pack_t(const void *field, void *send, const KGeom &g, cudaStr
         return dispatch_variant<P, NV, 0>(id, a, s, pdl, sms);                                                    \
     }                                                                                                             \
     cudaError_t launch_halo_##TAG(const ApplyArgs &a, cudaStream_t s) { return launch_halo_t<P, NV>(a, s); }      \
+    cudaError_t launch_chain_##TAG(int id, const ApplyArgs &a, int n, unsigned base, cudaStream_t s, int sms,     \
+                                   int *nrb)                                                                      \
+    {                                                                                                             \
+        return dispatch_chain<P, NV, 0>(id, a, n, base, s, sms, nrb);                                             \
+    }                                                                                                             \
     cudaError_t launch_pack_##TAG(const void *f, void *d, const KGeom &g, cudaStream_t s)                         \
     {                                                                                                             \
         return launch_pack_t<P, NV>(f, d, g, s);                                                                  \

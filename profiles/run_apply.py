@@ -29,9 +29,25 @@ def setup(dims, nvec, prec):
     return ctx, L, a, b
 
 
-def time_variant(ctx, L, a, b, var, reps, dagger=False, flush=False, graph=False):
+def time_variant(ctx, L, a, b, var, reps, dagger=False, flush=False, graph=False, chain=False):
     ctx.set_option(cd.CD_OPT_VARIANT, var)
     f = L.apply_dagger if dagger else L.apply
+    if chain:   # one persistent kernel for all reps applies
+        try:
+            L.apply_chain(a, b, 4, dagger)
+        except cd.CDError:
+            return float("nan")
+        torch.cuda.synchronize()
+        s = torch.cuda.current_stream()
+        best = 1e30
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            L.apply_chain(a, b, reps, dagger)
+            e1.record(s)
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1) / reps * 1e3)
+        return best
     for _ in range(3):
         f(b, a)
     torch.cuda.synchronize()
@@ -89,6 +105,7 @@ def main():
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--cold", action="store_true", help="L2 flush before every timed apply")
     ap.add_argument("--graph", action="store_true", help="time K chained applies replayed as one CUDA graph")
+    ap.add_argument("--chain", action="store_true", help="time coarse_dslash_apply_chain (one persistent kernel)")
     ap.add_argument("--json", default=None)
     a = ap.parse_args()
     dims = tuple(a.dims)
@@ -109,14 +126,14 @@ def main():
     rows = []
     for var, name in enumerate(ctx.variants(a.prec)):
         reps = max(20, min(2000, int(2e5 / max(1, V))))
-        us = time_variant(ctx, L, x, y, var, reps, a.dagger, a.cold, a.graph)
+        us = time_variant(ctx, L, x, y, var, reps, a.dagger, a.cold, a.graph, a.chain)
         rows.append({"variant": name, "us": round(us, 3), "GBs": round(mb / us / 1e3, 1),
                      "GFLOPS": round(fl / us / 1e3, 1), "pct_8TBs": round(100 * mb / us / 1e3 / 8000, 1)})
-        print(f"{'x'.join(map(str, dims))} nvec={a.nvec} {a.prec} {'cold' if a.cold else ('graph' if a.graph else 'hot')} "
+        print(f"{'x'.join(map(str, dims))} nvec={a.nvec} {a.prec} {'cold' if a.cold else ('graph' if a.graph else ('chain' if a.chain else 'hot'))} "
               f"{name:28s} {us:9.3f} us  {mb / us / 1e3:8.1f} GB/s  {fl / us / 1e3:8.1f} GFLOPS", flush=True)
     if a.json:
         with open(a.json, "a") as fh:
-            fh.write(json.dumps({"dims": dims, "nvec": a.nvec, "prec": a.prec, "cold": a.cold, "graph": a.graph,
+            fh.write(json.dumps({"dims": dims, "nvec": a.nvec, "prec": a.prec, "cold": a.cold, "graph": a.graph, "chain": a.chain,
                                  "dagger": a.dagger, "rows": rows}) + "\n")
 
 

@@ -333,3 +333,55 @@ def test_cuda_graph_chain_matches_eager():
     g.replay()
     torch.cuda.synchronize()
     np.testing.assert_array_equal(a.export(), eager)
+
+
+# ---------------------------------------------------------------- chained applies (one persistent kernel)
+@pytest.mark.parametrize("dims,nvec,prec,n", [((2, 2, 2, 2), 24, "fp32", 7), ((2, 2, 2, 2), 24, "fp16", 3),
+                                              ((2, 2, 2, 2), 32, "fp32", 4), ((3, 2, 2, 2), 24, "fp32", 5),
+                                              ((4, 4, 4, 4), 24, "fp16", 3)])
+def test_apply_chain_matches_oracle(dims, nvec, prec, n):
+    N = 2 * nvec
+    Lh = synth.links(dims, N, kind="general", scale_log2=-4)
+    v = synth.vector(dims, N)
+    ref = v
+    for _ in range(n):
+        ref = oracle.apply(dims, Lh, ref)
+    ctx = cd.Context(dims, nvec)
+    L = ctx.links_upload(Lh, prec)
+    x, y = ctx.field(prec), ctx.field(prec)
+    x.import_(v)
+    L.apply_chain(x, y, n)
+    got = (y if n % 2 else x).export()
+    assert rel_l2(got, ref) <= (2e-6 * n if prec == "fp32" else 2e-3 * n)
+
+
+def test_apply_chain_dagger_and_bitwise_vs_single_applies():
+    dims, nvec = (2, 2, 2, 2), 24
+    N = 2 * nvec
+    Lh = synth.links(dims, N, kind="hermitian", scale_log2=-4)
+    w = synth.vector(dims, N, tag=synth.TAG_W)
+    ctx = cd.Context(dims, nvec)
+    L = ctx.links_upload(Lh, "fp32")
+    x, y = ctx.field("fp32"), ctx.field("fp32")
+    x.import_(w)
+    L.apply_chain(x, y, 3, dagger=True)
+    got = y.export()
+    ref = w
+    for _ in range(3):
+        ref = oracle.adjoint(dims, Lh, ref)
+    assert rel_l2(got, ref) <= 1e-5
+    # same variant through single applies: identical arithmetic -> bitwise equal
+    var = ctx.chosen_variant("fp32", dagger=True) if False else None
+    for v in range(1, len(ctx.variants("fp32"))):
+        ctx.set_option(cd.CD_OPT_VARIANT, v)
+        x.import_(w)
+        try:
+            L.apply_chain(x, y, 3, dagger=True)
+        except cd.CDError:
+            continue
+        chain = y.export()
+        x.import_(w)
+        L.apply_dagger(y, x)
+        L.apply_dagger(x, y)
+        L.apply_dagger(y, x)
+        np.testing.assert_array_equal(chain, y.export())
