@@ -397,6 +397,7 @@ int cd_context_destroy(cd_context *c)
     if (c->ysplit) cudaFree(c->ysplit);
     if (c->site_cnt) cudaFree(c->site_cnt);
     if (c->chain_cnt) cudaFree(c->chain_cnt);
+    if (c->llbuf) cudaFree(c->llbuf);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->ev_in) cudaEventDestroy(c->ev_in);
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
@@ -903,8 +904,12 @@ int coarse_dslash_apply_dagger(const cd_links *l, cd_field *out, const cd_field 
 static cudaError_t chain_launch(cd_context *c, cd_precision p, int id, const ApplyArgs &a, int n, cudaStream_t s)
 {
     int nrb = 0;
-    cudaError_t e = launch_chain(p, id, a, n, c->chain_base, s, c->num_sms, &nrb);
-    if (e == cudaSuccess) c->chain_base += (unsigned)(n * nrb);
+    const bool ll = id >= LL_CHAIN_ID0;
+    cudaError_t e = launch_chain(p, id, a, n, ll ? c->ll_base : c->chain_base, s, c->num_sms, &nrb);
+    if (e == cudaSuccess) {
+        if (ll) c->ll_base += (unsigned)n;   // epochs ll_base+1 .. ll_base+n used
+        else c->chain_base += (unsigned)(n * nrb);
+    }
     return e;
 }
 
@@ -927,6 +932,12 @@ int coarse_dslash_apply_chain(const cd_links *l, cd_field *x, cd_field *y, int n
     a.dagger = dagger ? 1 : 0;
     a.g = c->kg;
     a.chain_cnt = c->chain_cnt;
+    if (!c->llbuf) {   // 2 x V LL records of at most 16N bytes, zeroed (epoch 0 is never awaited)
+        const size_t llb = 2 * (size_t)c->V * 16 * c->N;
+        CUDA_TRY(cudaMalloc(&c->llbuf, llb), "cudaMalloc(llbuf)");
+        CUDA_TRY(cudaMemset(c->llbuf, 0, llb), "cudaMemset(llbuf)");
+    }
+    a.llbuf = c->llbuf;
     const cd_precision p = l->prec;
     const TuneKey key{(int)p, 2 + a.dagger};
     int id = -1;
@@ -954,7 +965,12 @@ int coarse_dslash_apply_chain(const cd_links *l, cd_field *x, cd_field *y, int n
         CUDA_TRY(cudaEventCreate(&e1), "event");
         float best = 1e30f;
         const int trial = 64;
+        std::vector<int> cands{CLUSTER_CHAIN_ID};
         for (int v = 0; v < variant_count(p, c->nvec); v++) {
+            cands.push_back(LL_CHAIN_ID0 + v);
+            cands.push_back(v);
+        }
+        for (int v : cands) {
             if (chain_launch(c, p, v, ta, 2, s) != cudaSuccess) {
                 cudaGetLastError();
                 continue;

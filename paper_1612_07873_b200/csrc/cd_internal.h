@@ -90,6 +90,8 @@ struct cd_context {
     int *site_cnt = nullptr;          // fp16 row-split per-site counters [V]
     unsigned *chain_cnt = nullptr;    // chain kernel per-site counters [V] (monotonic)
     unsigned chain_base = 0;          // value every chain counter holds between chain calls
+    void *llbuf = nullptr;            // LL chain buffers (allocated on first use, zeroed)
+    unsigned ll_base = 0;             // LL chain epochs used so far
     int n_face = 0;
     bool halo_ready = false;
     cudaStream_t comm_stream = nullptr;
@@ -138,11 +140,15 @@ struct ApplyArgs {
     float2 *ysplit;        // fp16 row-split fg: fp32 rows of a site [V][N] (L2 resident)
     int *site_cnt;         // fp16 row-split fg: per-site arrival counters (zero between launches)
     unsigned *chain_cnt;   // chain kernel: monotonic per-site completion counters
+    void *llbuf;           // LL chain: 2 x V LL records (epoch-tagged payload words)
     KGeom g;
     int nvec;
     int dagger;
     int halo;              // 1: skip remote hops, face sites -> scratch
 };
+
+constexpr int CLUSTER_CHAIN_ID = 1000;   // apply_chain variant: whole lattice in one cluster
+constexpr int LL_CHAIN_ID0 = 2000;       // apply_chain variants 2000 + fg id: LL-protocol chain
 
 int variant_count(cd_precision p, int nvec);
 const char *variant_name(cd_precision p, int nvec, int id);

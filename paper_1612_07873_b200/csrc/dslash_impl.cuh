@@ -515,6 +515,412 @@ __global__ void __launch_bounds__(FgCfg<P, NV, KW, WR>::THREADS) dslash_chain(Ap
     }
 }
 
+inline cudaError_t launch_ex(const void *fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl, void **args,
+                             bool cooperative);
+
+// ------------------------------------------------------------------ LL chain (latency regime)
+// As dslash_chain, but the intermediate vectors travel in an "LL" format (as NCCL's LL
+// protocol): every 4-byte payload word is stored together with its epoch in ONE 8-byte store,
+// so a reader polls the data itself -- no separate completion flag, no release fence, one L2
+// round trip per apply on the critical path.  Double-buffered: apply t reads LL[t&1] (epoch
+// base+t), writes LL[(t+1)&1] (epoch base+t+1); having read all nine neighbour records of
+// epoch base+t proves those CTAs finished apply t-1, including their reads of the buffer this
+// CTA now overwrites (symmetric stencil).  Every iterate is also stored in the ordinary
+// format (x / y ping-pong), off the critical path.
+template <cd_precision P, int NV>
+struct LLCfg {
+    using Q = Cfg<P, NV>;
+    static constexpr int W = Q::F16 ? Q::N + 1 : 2 * Q::N;   // payload words per record (+scale for fp16)
+    static constexpr int WP = (W + 1) / 2;                     // 16-byte units (2 LL words) per record
+    static constexpr int REC = WP * 16;                        // LL record bytes
+};
+
+template <cd_precision P, int NV, int KW, int WR>
+__global__ void __launch_bounds__(FgCfg<P, NV, KW, WR>::THREADS) dslash_llchain(ApplyArgs a, int n, unsigned base)
+{
+    using Q = Cfg<P, NV>;
+    using F = FgCfg<P, NV, KW, WR>;
+    using LL = LLCfg<P, NV>;
+    static_assert(!F::SPLIT16, "fp16 chain needs whole-site CTAs");
+    constexpr int UNITS = 9 * LL::WP;                               // 16-B LL units to gather
+    constexpr int U = (UNITS + F::THREADS - 1) / F::THREADS;       // per thread
+    __shared__ __align__(16) unsigned char vs[9 * Q::VREC];
+    __shared__ float2 part[F::WK][F::ROWS];
+    __shared__ float red[32];
+
+    const int site = blockIdx.x / F::NRB, rb = blockIdx.x - site * F::NRB;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wk = warp / WR, wr = warp - wk * WR;
+    const int r = lane / Q::D, d = lane % Q::D;
+    const int rowl = wr * Q::R + r, row = rb * F::ROWS + rowl;
+    const unsigned char *links = static_cast<const unsigned char *>(a.links);
+    unsigned char *const buf0 = const_cast<unsigned char *>(static_cast<const unsigned char *>(a.in));
+    unsigned char *const buf1 = static_cast<unsigned char *>(a.out);
+    unsigned char *const ll = reinterpret_cast<unsigned char *>(a.llbuf);
+    const size_t llhalf = (size_t)a.g.V * LL::REC;
+
+    int x[4];
+    decode(a.g, site, x);
+    uint4 Lc[KW][Q::C];
+    float sl[KW];
+#pragma unroll
+    for (int kk = 0; kk < KW; kk++) {
+        const int k = kseq(wk * KW + kk);
+        const unsigned char *m = links + ((size_t)site * 9 + k) * Q::MREC;
+#pragma unroll
+        for (int c = 0; c < Q::C; c++) Lc[kk][c] = ld_stream(m + row * Q::ROWB + (d + Q::D * c) * 16);
+        sl[kk] = Q::F16 ? ld_nc_f32(m + Q::MSCALE) : 0.0f;
+    }
+    // the LL units this thread gathers: (hop k, unit w) -> source site
+    int uk[U], uw[U], unb[U];
+#pragma unroll
+    for (int i = 0; i < U; i++) {
+        const int e = threadIdx.x + i * F::THREADS;
+        uk[i] = e < UNITS ? e / LL::WP : -1;
+        uw[i] = e < UNITS ? e - uk[i] * LL::WP : 0;
+        unb[i] = e < UNITS ? neighbour(a.g, x, site, uk[i]) : 0;
+    }
+
+    for (int t = 0; t < n; t++) {
+        unsigned char *gout = (t & 1) ? buf0 : buf1;
+        if (t == 0) {   // the input is ready at launch: ordinary format
+            for (int e = threadIdx.x; e < 9 * Q::VCH; e += F::THREADS) {
+                const int k = e / Q::VCH, c16 = e - k * Q::VCH;
+                *reinterpret_cast<uint4 *>(vs + k * Q::VREC + c16 * 16) =
+                    ld_nc(buf0 + (size_t)neighbour(a.g, x, site, k) * Q::VREC + c16 * 16);
+            }
+        } else {        // poll the LL words of epoch base + t
+            const unsigned want = base + (unsigned)t;
+            const unsigned char *src = ll + (size_t)(t & 1) * llhalf;
+            uint4 v[U];
+            bool done[U];
+#pragma unroll
+            for (int i = 0; i < U; i++) done[i] = uk[i] < 0;
+            bool all = false;
+            while (!all) {
+#pragma unroll
+                for (int i = 0; i < U; i++)
+                    if (!done[i]) v[i] = ld_cg(src + (size_t)unb[i] * LL::REC + uw[i] * 16);
+                all = true;
+#pragma unroll
+                for (int i = 0; i < U; i++) {
+                    if (done[i]) continue;
+                    const bool last_odd = (LL::W & 1) && uw[i] == LL::WP - 1;   // second word is padding
+                    done[i] = v[i].y == want && (last_odd || v[i].w == want);
+                    if (done[i]) {   // unpack the (1 or 2) payload words into the ordinary record
+                        unsigned *dst = reinterpret_cast<unsigned *>(vs + uk[i] * Q::VREC);
+                        const int w0 = 2 * uw[i];
+                        if constexpr (Q::F16) {
+                            dst[w0 == Q::N ? Q::VSCALE / 4 : w0] = v[i].x;
+                            if (!last_odd) dst[w0 + 1 == Q::N ? Q::VSCALE / 4 : w0 + 1] = v[i].z;
+                        } else {
+                            dst[w0] = v[i].x;
+                            dst[w0 + 1] = v[i].z;
+                        }
+                    }
+                    all = all && done[i];
+                }
+            }
+        }
+        __syncthreads();
+        float re = 0.0f, im = 0.0f;
+#pragma unroll
+        for (int kk = 0; kk < KW; kk++) {
+            const int k = kseq(wk * KW + kk);
+            const unsigned char *vrec = vs + k * Q::VREC;
+            if constexpr (P == CD_FP32) {
+                float pr[Q::C], pi[Q::C];
+#pragma unroll
+                for (int c = 0; c < Q::C; c++) {
+                    pr[c] = 0.0f;
+                    pi[c] = 0.0f;
+                    const int q = d + Q::D * c;
+                    uint4 vq = lds128(vrec + q * 16);
+                    if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<false>(vq);
+                    cmac2(Lc[kk][c], vq, pr[c], pi[c]);
+                }
+#pragma unroll
+                for (int c = 0; c < Q::C; c++) { re += pr[c]; im += pi[c]; }
+            } else {
+                float ra = 0.f, rb2 = 0.f, ia = 0.f, ib = 0.f;
+#pragma unroll
+                for (int c = 0; c < Q::C; c++) {
+                    const int q = d + Q::D * c;
+                    uint4 vq = lds128(vrec + q * 16);
+                    if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<true>(vq);
+                    hmac4(Lc[kk][c], vq, ra, rb2, ia, ib);
+                }
+                const float sc = sl[kk] * *reinterpret_cast<const float *>(vrec + Q::VSCALE);
+                re = fmaf(ra - rb2, sc, re);
+                im = fmaf(ia + ib, sc, im);
+            }
+        }
+#pragma unroll
+        for (int m = Q::D / 2; m >= 1; m >>= 1) {
+            re += shfl_xor(re, m);
+            im += shfl_xor(im, m);
+        }
+        if (d == 0) part[wk][rowl] = make_float2(re, im);
+        __syncthreads();
+        const bool owner = threadIdx.x < F::ROWS;
+        float yr = 0.0f, yi = 0.0f;
+        if (owner) {
+#pragma unroll
+            for (int w = 0; w < F::WK; w++) {
+                yr += part[w][threadIdx.x].x;
+                yi += part[w][threadIdx.x].y;
+            }
+        }
+        const int orow = rb * F::ROWS + (owner ? threadIdx.x : 0);
+        const float sg = (a.dagger && orow >= NV) ? -1.0f : 1.0f;
+        yr *= sg;
+        yi *= sg;
+        const unsigned ep = base + (unsigned)t + 1;
+        unsigned char *dst = ll + (size_t)((t + 1) & 1) * llhalf + (size_t)site * LL::REC;
+        if constexpr (P == CD_FP32) {
+            if (owner) {   // one 16-byte store = two LL words {re, ep}, {im, ep}
+                reinterpret_cast<uint4 *>(dst)[orow] = make_uint4(__float_as_uint(yr), ep, __float_as_uint(yi), ep);
+                reinterpret_cast<float2 *>(gout + (size_t)site * Q::VREC)[orow] = make_float2(yr, yi);
+            }
+        } else {
+            float mx = owner ? fmaxf(fabsf(yr), fabsf(yi)) : 0.0f;
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, shfl_xor(mx, o));
+            if (lane == 0) red[warp] = mx;
+            __syncthreads();
+            float s = 0.0f;
+            for (int w = 0; w < F::NW; w++) s = fmaxf(s, red[w]);
+            if (owner) {
+                __half2 q;
+                if (s > 0.0f) q = __halves2half2(__float2half_rn(__fdiv_rn(yr, s)), __float2half_rn(__fdiv_rn(yi, s)));
+                else q = __halves2half2(__float2half_rn(0.0f), __float2half_rn(0.0f));
+                const unsigned qb = *reinterpret_cast<unsigned *>(&q);
+                reinterpret_cast<uint2 *>(dst)[orow] = make_uint2(qb, ep);
+                reinterpret_cast<unsigned *>(gout + (size_t)site * Q::VREC)[orow] = qb;
+                if (orow == 0) {
+                    reinterpret_cast<uint2 *>(dst)[Q::N] = make_uint2(__float_as_uint(s), ep);
+                    *reinterpret_cast<float *>(gout + (size_t)site * Q::VREC + Q::VSCALE) = s;
+                }
+            }
+        }
+        __syncthreads();   // vs / part / red reuse in the next apply
+    }
+}
+
+template <cd_precision P, int NV, int KW, int WR>
+cudaError_t launch_llchain_t(const ApplyArgs &a, int n, unsigned base, cudaStream_t s, int num_sms)
+{
+    using F = FgCfg<P, NV, KW, WR>;
+    if constexpr (F::SPLIT16) {
+        return cudaErrorNotSupported;
+    } else {
+        int per_sm = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dslash_llchain<P, NV, KW, WR>, F::THREADS, 0);
+        if (e != cudaSuccess) return e;
+        if ((int64_t)a.g.V * F::NRB > (int64_t)per_sm * num_sms) return cudaErrorCooperativeLaunchTooLarge;
+        ApplyArgs aa = a;
+        int nn = n;
+        unsigned bb = base;
+        void *args[] = {&aa, &nn, &bb};
+        return launch_ex((const void *)dslash_llchain<P, NV, KW, WR>, dim3((unsigned)(a.g.V * F::NRB)),
+                         dim3(F::THREADS), 0, s, false, args, true);
+    }
+}
+
+// ------------------------------------------------------------------ CLUSTER chain (V <= 16 sites)
+// The whole lattice in ONE thread-block cluster (non-portable size up to 16, one CTA per site):
+// every CTA keeps its site's nine matrices in registers for all n applies and its current
+// vector in shared memory; the neighbour records are read through distributed shared memory
+// (mapa + ld.shared::cluster) and one cluster barrier per apply orders everything (double-
+// buffered vectors: the barrier at the end of apply t lets apply t+1 overwrite the buffer
+// apply t read).  Per apply: cluster barrier + one DSMEM round trip + the math -- no HBM/L2
+// round trips, no kernel boundary.  Work per CTA: TASKS = 9 hops x (N/R) row groups, spread
+// over NW warps (TPW tasks per warp); lanes split each row D ways as everywhere else.
+template <cd_precision P, int NV, int NW>
+struct ClusterCfg {
+    using Q = Cfg<P, NV>;
+    static constexpr int RG = Q::N / Q::R;          // row groups
+    static constexpr int TASKS = 9 * RG;
+    static constexpr int TPW = TASKS / NW;
+    static constexpr int THREADS = 32 * NW;
+    static_assert(TPW * NW == TASKS, "tasks must tile the warps");
+    static_assert(THREADS >= 9 * (Q::VREC / 16), "one 16-B neighbour chunk per thread");
+};
+
+__device__ __forceinline__ unsigned cluster_rank()
+{
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint4 ld_dsmem(const void *local_ptr, unsigned cta)
+{
+    uint32_t la = (uint32_t)__cvta_generic_to_shared(local_ptr), ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(cta));
+    uint4 v;
+    asm volatile("ld.shared::cluster.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(ra)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void cluster_sync_all()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <cd_precision P, int NV, int NW>
+__global__ void __launch_bounds__(ClusterCfg<P, NV, NW>::THREADS, 1) dslash_cluster_chain(ApplyArgs a, int n)
+{
+    using Q = Cfg<P, NV>;
+    using K = ClusterCfg<P, NV, NW>;
+    __shared__ __align__(16) unsigned char vbuf[2][Q::VREC];   // this site's vector, by apply parity
+    __shared__ __align__(16) unsigned char vs[9 * Q::VREC];     // the nine neighbour records
+    __shared__ float2 part[9][Q::N];
+    __shared__ float red[32];
+
+    const int site = (int)cluster_rank();   // grid == one cluster of V CTAs
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r = lane / Q::D, d = lane % Q::D;
+    const unsigned char *links = static_cast<const unsigned char *>(a.links);
+    unsigned char *const g0 = const_cast<unsigned char *>(static_cast<const unsigned char *>(a.in));
+    unsigned char *const g1 = static_cast<unsigned char *>(a.out);
+    int x[4];
+    decode(a.g, site, x);
+
+    // links -> registers, once for all n applies
+    uint4 Lc[K::TPW][Q::C];
+    float sl[K::TPW];
+#pragma unroll
+    for (int j = 0; j < K::TPW; j++) {
+        const int task = warp + NW * j;
+        const int k = task / K::RG, rg = task - k * K::RG;
+        const int row = rg * Q::R + r;
+        const unsigned char *m = links + ((size_t)site * 9 + k) * Q::MREC;
+#pragma unroll
+        for (int c = 0; c < Q::C; c++) Lc[j][c] = ld_stream(m + row * Q::ROWB + (d + Q::D * c) * 16);
+        sl[j] = Q::F16 ? ld_nc_f32(m + Q::MSCALE) : 0.0f;
+    }
+    // this thread's neighbour chunk (for the staging step)
+    const int sk = threadIdx.x / Q::VCH, se = threadIdx.x - sk * Q::VCH;
+    const bool stager = sk < 9;
+    const unsigned src_cta = stager ? (unsigned)neighbour(a.g, x, site, sk) : 0u;
+    for (int e = threadIdx.x; e < Q::VCH; e += K::THREADS)
+        *reinterpret_cast<uint4 *>(vbuf[0] + e * 16) = ld_nc(g0 + (size_t)site * Q::VREC + e * 16);
+    cluster_sync_all();
+
+    for (int t = 0; t < n; t++) {
+        const int pin = t & 1;
+        if (stager)
+            *reinterpret_cast<uint4 *>(vs + sk * Q::VREC + se * 16) = ld_dsmem(vbuf[pin] + se * 16, src_cta);
+        __syncthreads();
+        float rr[K::TPW], ii[K::TPW];
+#pragma unroll
+        for (int j = 0; j < K::TPW; j++) {
+            const int task = warp + NW * j;
+            const int k = task / K::RG;
+            const unsigned char *vrec = vs + k * Q::VREC;
+            float re = 0.0f, im = 0.0f;
+            if constexpr (P == CD_FP32) {
+#pragma unroll
+                for (int c = 0; c < Q::C; c++) {
+                    const int q = d + Q::D * c;
+                    uint4 vq = lds128(vrec + q * 16);
+                    if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<false>(vq);
+                    cmac2(Lc[j][c], vq, re, im);
+                }
+            } else {
+                float ra = 0.f, rb2 = 0.f, ia = 0.f, ib = 0.f;
+#pragma unroll
+                for (int c = 0; c < Q::C; c++) {
+                    const int q = d + Q::D * c;
+                    uint4 vq = lds128(vrec + q * 16);
+                    if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<true>(vq);
+                    hmac4(Lc[j][c], vq, ra, rb2, ia, ib);
+                }
+                const float sc = sl[j] * *reinterpret_cast<const float *>(vrec + Q::VSCALE);
+                re = (ra - rb2) * sc;
+                im = (ia + ib) * sc;
+            }
+            rr[j] = re;
+            ii[j] = im;
+        }
+#pragma unroll
+        for (int j = 0; j < K::TPW; j++) {
+#pragma unroll
+            for (int m = Q::D / 2; m >= 1; m >>= 1) {
+                rr[j] += shfl_xor(rr[j], m);
+                ii[j] += shfl_xor(ii[j], m);
+            }
+            const int task = warp + NW * j;
+            const int k = task / K::RG, rg = task - k * K::RG;
+            if (d == 0) part[k][rg * Q::R + r] = make_float2(rr[j], ii[j]);
+        }
+        __syncthreads();
+        const bool owner = threadIdx.x < Q::N;
+        float yr = 0.0f, yi = 0.0f;
+        if (owner) {
+            const float2 p8 = part[8][threadIdx.x];   // X first, then k = 0..7 (R11 order)
+            yr = p8.x;
+            yi = p8.y;
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                yr += part[k][threadIdx.x].x;
+                yi += part[k][threadIdx.x].y;
+            }
+        }
+        const int orow = owner ? threadIdx.x : 0;
+        const float sg = (a.dagger && orow >= NV) ? -1.0f : 1.0f;
+        // new vector -> this CTA's shared buffer (read by the peers next apply) and to HBM
+        unsigned char *gout = (t & 1) ? g0 : g1;
+        store_site<P, NV>(vbuf[pin ^ 1] - (size_t)0, 0, orow, owner, sg * yr, sg * yi, red, K::THREADS, -1);
+        __syncthreads();
+        for (int e = threadIdx.x; e < Q::VCH; e += K::THREADS)
+            *reinterpret_cast<uint4 *>(gout + (size_t)site * Q::VREC + e * 16) =
+                *reinterpret_cast<const uint4 *>(vbuf[pin ^ 1] + e * 16);
+        cluster_sync_all();   // everybody's new vector is visible; everybody finished reading the old one
+    }
+}
+
+template <cd_precision P, int NV>
+struct ClusterNW {   // warps per site-CTA (0: the site's links do not fit in one SM's registers)
+    static constexpr int nw = (P == CD_FP32 && NV == 24) ? 27 : (P == CD_FP16 && NV == 24) ? 27
+                            : (P == CD_FP16 && NV == 32) ? 24 : 0;
+};
+
+template <cd_precision P, int NV, int NW>
+cudaError_t launch_cluster_chain_t(const ApplyArgs &a, int n, cudaStream_t s)
+{
+    using K = ClusterCfg<P, NV, NW>;
+    if (a.g.V > 16 || a.halo) return cudaErrorNotSupported;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(dslash_cluster_chain<P, NV, NW>,
+                                             cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)a.g.V);
+    cfg.blockDim = dim3(K::THREADS);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)a.g.V;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, dslash_cluster_chain<P, NV, NW>, &cfg);
+    if (e != cudaSuccess) return e;
+    if (nclusters < 1) return cudaErrorCooperativeLaunchTooLarge;
+    ApplyArgs aa = a;
+    int nn = n;
+    void *args[] = {&aa, &nn};
+    count_launch();
+    return cudaLaunchKernelExC(&cfg, (const void *)dslash_cluster_chain<P, NV, NW>, args);
+}
+
 // ------------------------------------------------------------------ halo term (multi-rank)
 // One CTA per face site: y(x) = partial(x) + sum over remote hops L_k(x) v_halo, then the
 // final store (fp16: whole-site re-quantisation).  Neighbour records come from the receive
@@ -756,6 +1162,21 @@ cudaError_t dispatch_chain(int id, const ApplyArgs &a, int n, unsigned base, cud
 }
 
 template <cd_precision P, int NV, int I>
+cudaError_t dispatch_llchain(int id, const ApplyArgs &a, int n, unsigned base, cudaStream_t s, int num_sms)
+{
+    if constexpr (I >= Variants<P, NV>::n) {
+        return cudaErrorInvalidValue;
+    } else {
+        if (id == I) {
+            constexpr VDesc v = Variants<P, NV>::v[I];
+            if constexpr (v.kind == 0) return cudaErrorNotSupported;
+            else return launch_llchain_t<P, NV, v.kw, v.wr>(a, n, base, s, num_sms);
+        }
+        return dispatch_llchain<P, NV, I + 1>(id, a, n, base, s, num_sms);
+    }
+}
+
+template <cd_precision P, int NV, int I>
 cudaError_t dispatch_variant(int id, const ApplyArgs &a, cudaStream_t s, bool pdl, int num_sms)
 {
     if constexpr (I >= Variants<P, NV>::n) {
@@ -809,6 +1230,17 @@ cudaError_t launch_pack_t(const void *field, void *send, const KGeom &g, cudaStr
     cudaError_t launch_chain_##TAG(int id, const ApplyArgs &a, int n, unsigned base, cudaStream_t s, int sms,     \
                                    int *nrb)                                                                      \
     {                                                                                                             \
+        if (id >= LL_CHAIN_ID0 && id < LL_CHAIN_ID0 + Variants<P, NV>::n) {                                       \
+            *nrb = 0;                                                                                             \
+            return dispatch_llchain<P, NV, 0>(id - LL_CHAIN_ID0, a, n, base, s, sms);                             \
+        }                                                                                                         \
+        if (id == CLUSTER_CHAIN_ID) {                                                                             \
+            *nrb = 0;                                                                                             \
+            if constexpr (ClusterNW<P, NV>::nw > 0)                                                               \
+                return launch_cluster_chain_t<P, NV, ClusterNW<P, NV>::nw>(a, n, s);                              \
+            else                                                                                                  \
+                return cudaErrorNotSupported;                                                                     \
+        }                                                                                                         \
         return dispatch_chain<P, NV, 0>(id, a, n, base, s, sms, nrb);                                             \
     }                                                                                                             \
     cudaError_t launch_pack_##TAG(const void *f, void *d, const KGeom &g, cudaStream_t s)                         \

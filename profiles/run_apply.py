@@ -124,7 +124,11 @@ def main():
               else ctx.variants(a.prec)[a.variant])
         return
     rows = []
-    for var, name in enumerate(ctx.variants(a.prec)):
+    cands = list(enumerate(ctx.variants(a.prec)))
+    if a.chain:
+        cands = [(1000, f"cluster_chain_{a.prec}_nv{a.nvec}")] + \
+            [(2000 + i, "ll_" + nm) for i, nm in cands] + cands
+    for var, name in cands:
         reps = max(20, min(2000, int(2e5 / max(1, V))))
         us = time_variant(ctx, L, x, y, var, reps, a.dagger, a.cold, a.graph, a.chain)
         rows.append({"variant": name, "us": round(us, 3), "GBs": round(mb / us / 1e3, 1),

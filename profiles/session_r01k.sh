@@ -1,0 +1,8 @@
+#!/bin/bash
+O=gpurun_out
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+S="python profiles/run_apply.py --sweep --json $O/sweep_k.jsonl"
+$S --dims 2 2 2 2 --nvec 24 --prec fp32 --chain
+$S --dims 2 2 2 2 --nvec 24 --prec fp16 --chain
+$S --dims 2 2 2 2 --nvec 32 --prec fp32 --chain
+$S --dims 4 4 4 4 --nvec 24 --prec fp16 --chain

@@ -385,3 +385,57 @@ def test_apply_chain_dagger_and_bitwise_vs_single_applies():
         L.apply_dagger(x, y)
         L.apply_dagger(y, x)
         np.testing.assert_array_equal(chain, y.export())
+
+
+@pytest.mark.parametrize("nvec,prec,n", [(24, "fp32", 5), (24, "fp16", 3), (32, "fp16", 3)])
+def test_cluster_chain_forced(nvec, prec, n):
+    """The whole-lattice thread-block-cluster chain (variant 1000) on the 2^4 coarsest grid."""
+    dims = (2, 2, 2, 2)
+    N = 2 * nvec
+    Lh = synth.links(dims, N, kind="hermitian", scale_log2=-4)
+    v = synth.vector(dims, N)
+    ctx = cd.Context(dims, nvec)
+    ctx.set_option(cd.CD_OPT_VARIANT, 1000)
+    L = ctx.links_upload(Lh, prec)
+    x, y = ctx.field(prec), ctx.field(prec)
+    for dag in (False, True):
+        x.import_(v)
+        L.apply_chain(x, y, n, dagger=dag)
+        ref, prev = v, None
+        for _ in range(n):
+            prev, ref = ref, (oracle.adjoint if dag else oracle.apply)(dims, Lh, ref)
+        last, other = (y, x) if n % 2 else (x, y)
+        assert rel_l2(last.export(), ref) <= (2e-6 * n if prec == "fp32" else 2e-3 * n)
+        assert rel_l2(other.export(), prev) <= (2e-6 * n if prec == "fp32" else 2e-3 * n)
+
+
+@pytest.mark.parametrize("dims,nvec,prec,n", [((2, 2, 2, 2), 24, "fp32", 6), ((2, 2, 2, 2), 24, "fp16", 3),
+                                              ((3, 2, 2, 2), 32, "fp32", 5), ((2, 2, 2, 2), 32, "fp16", 4)])
+def test_ll_chain_all_variants(dims, nvec, prec, n):
+    """LL-protocol chain (variants 2000 + fg id): every variant that fits, apply and dagger,
+    both iterates (last and previous) against the oracle; repeated calls (epoch continuity)."""
+    N = 2 * nvec
+    Lh = synth.links(dims, N, kind="hermitian", scale_log2=-4)
+    v = synth.vector(dims, N)
+    ctx = cd.Context(dims, nvec)
+    L = ctx.links_upload(Lh, prec)
+    x, y = ctx.field(prec), ctx.field(prec)
+    tol = 2e-6 * n if prec == "fp32" else 2e-3 * n
+    ran = 0
+    for var in range(len(ctx.variants(prec))):
+        ctx.set_option(cd.CD_OPT_VARIANT, 2000 + var)
+        for dag in (False, True):
+            for _rep in range(2):
+                x.import_(v)
+                try:
+                    L.apply_chain(x, y, n, dagger=dag)
+                except cd.CDError:
+                    break
+                ran += 1
+                ref, prev = v, None
+                for _ in range(n):
+                    prev, ref = ref, (oracle.adjoint if dag else oracle.apply)(dims, Lh, ref)
+                last, other = (y, x) if n % 2 else (x, y)
+                assert rel_l2(last.export(), ref) <= tol, (ctx.variants(prec)[var], dag)
+                assert rel_l2(other.export(), prev) <= tol, (ctx.variants(prec)[var], dag)
+    assert ran > 0
