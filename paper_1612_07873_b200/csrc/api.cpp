@@ -938,6 +938,8 @@ int coarse_dslash_apply_chain(const cd_links *l, cd_field *x, cd_field *y, int n
         CUDA_TRY(cudaMemset(c->llbuf, 0, llb), "cudaMemset(llbuf)");
     }
     a.llbuf = c->llbuf;
+    a.poll_ns = 0;
+    if (const char *ev = getenv("CD_POLL_NS")) a.poll_ns = atoi(ev);
     const cd_precision p = l->prec;
     const TuneKey key{(int)p, 2 + a.dagger};
     int id = -1;

@@ -141,6 +141,7 @@ struct ApplyArgs {
     int *site_cnt;         // fp16 row-split fg: per-site arrival counters (zero between launches)
     unsigned *chain_cnt;   // chain kernel: monotonic per-site completion counters
     void *llbuf;           // LL chain: 2 x V LL records (epoch-tagged payload words)
+    int poll_ns;           // LL chain: __nanosleep between unsuccessful polls (0 = spin)
     KGeom g;
     int nvec;
     int dagger;

@@ -597,7 +597,10 @@ __global__ void __launch_bounds__(FgCfg<P, NV, KW, WR>::THREADS) dslash_llchain(
 #pragma unroll
             for (int i = 0; i < U; i++) done[i] = uk[i] < 0;
             bool all = false;
+            bool first = true;
             while (!all) {
+                if (!first && a.poll_ns > 0) __nanosleep(a.poll_ns);   // back off: spinning loads share L2 with the writers
+                first = false;
 #pragma unroll
                 for (int i = 0; i < U; i++)
                     if (!done[i]) v[i] = ld_cg(src + (size_t)unb[i] * LL::REC + uw[i] * 16);
