@@ -40,7 +40,7 @@ EXPORTS = (
     "coarse_field_stored_bytes", "coarse_field_read_stored", "coarse_links_upload", "coarse_links_generate",
     "coarse_links_stored_bytes", "coarse_links_read_stored", "coarse_links_free", "coarse_dslash_apply",
     "coarse_dslash_apply_dagger", "coarse_halo_pack", "cd_flush_l2", "cd_halo_plan_create",
-    "coarse_dslash_apply_chain",
+    "coarse_dslash_apply_chain", "coarse_field_bytes_mrhs", "coarse_field_alloc_mrhs", "coarse_dslash_apply_mrhs",
 )
 
 
@@ -102,6 +102,9 @@ def _load():
         "cd_flush_l2": ([P, SZ, P], I),
         "cd_halo_plan_create": ([ctypes.POINTER(_Geometry), I, I, I, ctypes.c_int32, ctypes.POINTER(HaloPlan)], I),
         "coarse_dslash_apply_chain": ([P, P, P, I, I, P], I),
+        "coarse_field_bytes_mrhs": ([P, I, I], SZ),
+        "coarse_field_alloc_mrhs": ([P, I, I, P, SZ, PP], I),
+        "coarse_dslash_apply_mrhs": ([P, P, P, I, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -267,8 +270,8 @@ class Context:
     def chosen_variant(self, prec, dagger=False):
         return lib.cd_context_chosen_variant(self.handle, PREC[prec], int(bool(dagger)))
 
-    def field(self, prec="fp32", torch_memory=True):
-        return Field(self, prec, torch_memory)
+    def field(self, prec="fp32", torch_memory=True, nrhs=1):
+        return Field(self, prec, torch_memory, nrhs)
 
     def links_upload(self, links, prec="fp32", stream=None):
         return Links(self, prec, coarse_links_upload(self.handle, prec, np.ascontiguousarray(links)
@@ -304,17 +307,24 @@ class Context:
 class Field:
     """A colour-spinor field in the library's stored layout (device memory from torch)."""
 
-    def __init__(self, ctx: Context, prec="fp32", torch_memory=True):
+    def __init__(self, ctx: Context, prec="fp32", torch_memory=True, nrhs=1):
         self.ctx = ctx
         self.prec = PREC[prec]
-        self.nbytes = int(lib.coarse_field_bytes(ctx.handle, self.prec))
+        self.nrhs = int(nrhs)
+        self.nbytes = int(lib.coarse_field_bytes_mrhs(ctx.handle, self.prec, self.nrhs))
         self._mem = None
+        ptr = None
         if torch_memory:
             import torch
             self._mem = torch.empty(self.nbytes, dtype=torch.uint8, device="cuda")
-            self.handle = coarse_field_alloc(ctx.handle, self.prec, self._mem.data_ptr(), self.nbytes)
+            ptr = self._mem.data_ptr()
+        if self.nrhs == 1:
+            self.handle = coarse_field_alloc(ctx.handle, self.prec, ptr, self.nbytes if ptr else 0)
         else:
-            self.handle = coarse_field_alloc(ctx.handle, self.prec)
+            out = ctypes.c_void_p()
+            _check(lib.coarse_field_alloc_mrhs(ctx.handle, self.prec, self.nrhs, ptr, self.nbytes if ptr else 0,
+                                               ctypes.byref(out)))
+            self.handle = out
 
     def import_(self, v, stream=None):
         """v: canonical LOCAL [V, N] complex64/complex128 (numpy host or torch host/device)."""
@@ -324,7 +334,8 @@ class Field:
 
     def export(self, dst=None, dtype=np.complex128, stream=None, sync=True):
         if dst is None:
-            dst = np.empty((self.ctx.V, self.ctx.N), dtype)
+            shape = (self.ctx.V, self.ctx.N) if self.nrhs == 1 else (self.nrhs, self.ctx.V, self.ctx.N)
+            dst = np.empty(shape, dtype)
         p, dev, _ = _ptr(dst)
         _check(lib.coarse_field_export(self.handle, p, dev, CD_C128 if _is_c128(dst) else CD_C64, _stream(stream)))
         if sync:
@@ -368,6 +379,10 @@ class Links:
 
     def apply_chain(self, x: Field, y: Field, n: int, dagger=False, stream=None):
         coarse_dslash_apply_chain(self.handle, x.handle, y.handle, n, dagger, stream)
+
+    def apply_mrhs(self, out: Field, in_: Field, dagger=False, stream=None):
+        """out_r = D in_r for all right-hand sides (tcgen05 tensor cores, fp16 storage)."""
+        _check(lib.coarse_dslash_apply_mrhs(self.handle, out.handle, in_.handle, int(bool(dagger)), _stream(stream)))
 
     def read_stored(self, stream=None) -> bytes:
         n = int(lib.coarse_links_stored_bytes(self.handle))

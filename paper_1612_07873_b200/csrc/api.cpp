@@ -507,7 +507,36 @@ int coarse_field_alloc(cd_context *c, cd_precision p, void *mem, size_t bytes, c
         if (reinterpret_cast<uintptr_t>(mem) % 256) return fail(CD_ERR_INVALID, "device_mem must be 256-B aligned");
         if (bytes < need) return fail(CD_ERR_INVALID, "device_mem too small (need coarse_field_bytes)");
     }
-    *out = new cd_field{c, p, mem, bytes, owned};
+    *out = new cd_field{c, p, mem, bytes, owned, 1};
+    return CD_OK;
+    API_END
+}
+
+size_t coarse_field_bytes_mrhs(const cd_context *c, cd_precision p, int nrhs)
+{
+    if (!c || (p != CD_FP32 && p != CD_FP16) || nrhs < 1) return 0;
+    return align256(vec_rec_bytes(c->N, p) * (size_t)c->V * (size_t)nrhs);
+}
+
+int coarse_field_alloc_mrhs(cd_context *c, cd_precision p, int nrhs, void *mem, size_t bytes, cd_field **out)
+{
+    API_BEGIN
+    if (!c || !out) return fail(CD_ERR_INVALID, "ctx/out is NULL");
+    if (p != CD_FP32 && p != CD_FP16) return fail(CD_ERR_INVALID, "bad precision");
+    if (nrhs < 1) return fail(CD_ERR_INVALID, "nrhs must be >= 1");
+    const size_t need = coarse_field_bytes_mrhs(c, p, nrhs);
+    bool owned = false;
+    if (!mem) {
+        CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
+        cudaError_t e = cudaMalloc(&mem, need);
+        if (e != cudaSuccess) return fail(CD_ERR_OOM, std::string("cudaMalloc(field): ") + cudaGetErrorString(e));
+        bytes = need;
+        owned = true;
+    } else {
+        if (reinterpret_cast<uintptr_t>(mem) % 256) return fail(CD_ERR_INVALID, "device_mem must be 256-B aligned");
+        if (bytes < need) return fail(CD_ERR_INVALID, "device_mem too small (need coarse_field_bytes_mrhs)");
+    }
+    *out = new cd_field{c, p, mem, bytes, owned, nrhs};
     return CD_OK;
     API_END
 }
@@ -536,9 +565,9 @@ int coarse_field_import(cd_field *f, const void *src, int src_on_device, cd_host
     if (dt != CD_C64 && dt != CD_C128) return fail(CD_ERR_INVALID, "bad dtype");
     cd_context *c = f->ctx;
     const size_t elem = dt == CD_C128 ? 16 : 8;
-    const size_t bytes = elem * c->N * (size_t)c->V;
+    const size_t bytes = elem * c->N * (size_t)c->V * f->nrhs;
     cudaStream_t s = S(stream);
-    if (f->prec == CD_FP32 && dt == CD_C64) {   // stored layout == canonical layout
+    if (f->prec == CD_FP32 && dt == CD_C64 && f->nrhs == 1) {   // stored layout == canonical layout
         CUDA_TRY(cudaMemcpyAsync(f->base, src, bytes, src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                                  s), "cudaMemcpyAsync(import)");
         return CD_OK;
@@ -551,7 +580,7 @@ int coarse_field_import(cd_field *f, const void *src, int src_on_device, cd_host
         if (r != CD_OK) return r;
         dsrc = stage;
     }
-    CUDA_TRY(launch_import(f->prec, c->nvec, c->V, dsrc, dt == CD_C128, f->base, s), "import kernel");
+    CUDA_TRY(launch_import(f->prec, c->nvec, c->V, dsrc, dt == CD_C128, f->base, s, f->nrhs), "import kernel");
     if (stage) CUDA_TRY(cudaFreeAsync(stage, s), "cudaFreeAsync");
     return CD_OK;
     API_END
@@ -564,9 +593,9 @@ int coarse_field_export(const cd_field *f, void *dst, int dst_on_device, cd_host
     if (dt != CD_C64 && dt != CD_C128) return fail(CD_ERR_INVALID, "bad dtype");
     cd_context *c = f->ctx;
     const size_t elem = dt == CD_C128 ? 16 : 8;
-    const size_t bytes = elem * c->N * (size_t)c->V;
+    const size_t bytes = elem * c->N * (size_t)c->V * f->nrhs;
     cudaStream_t s = S(stream);
-    if (f->prec == CD_FP32 && dt == CD_C64) {
+    if (f->prec == CD_FP32 && dt == CD_C64 && f->nrhs == 1) {
         CUDA_TRY(cudaMemcpyAsync(dst, f->base, bytes, dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                                  s), "cudaMemcpyAsync(export)");
         return CD_OK;
@@ -577,7 +606,7 @@ int coarse_field_export(const cd_field *f, void *dst, int dst_on_device, cd_host
         CUDA_TRY(cudaMallocAsync(&stage, bytes, s), "cudaMallocAsync(stage)");
         ddst = stage;
     }
-    CUDA_TRY(launch_export(f->prec, c->nvec, c->V, f->base, ddst, dt == CD_C128, s), "export kernel");
+    CUDA_TRY(launch_export(f->prec, c->nvec, c->V, f->base, ddst, dt == CD_C128, s, f->nrhs), "export kernel");
     if (stage) {
         CUDA_TRY(cudaMemcpyAsync(dst, stage, bytes, cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(D2H)");
         CUDA_TRY(cudaFreeAsync(stage, s), "cudaFreeAsync");
@@ -591,7 +620,7 @@ int coarse_field_generate(cd_field *f, uint64_t seed, uint32_t tag, int32_t scal
     API_BEGIN
     if (!f) return fail(CD_ERR_INVALID, "field is NULL");
     if (scale_log2 < -60 || scale_log2 > 60) return fail(CD_ERR_INVALID, "scale_log2 out of range");
-    CUDA_TRY(launch_field_generate(f->prec, f->ctx->nvec, f->ctx, seed, tag, scale_log2, f->base, S(stream)),
+    CUDA_TRY(launch_field_generate(f->prec, f->ctx->nvec, f->ctx, seed, tag, scale_log2, f->base, S(stream), f->nrhs),
              "field generate");
     return CD_OK;
     API_END
@@ -756,6 +785,7 @@ static int check_objs(const cd_links *l, const cd_field *out, const cd_field *in
     if (l->ctx != out->ctx || l->ctx != in->ctx) return fail(CD_ERR_MISMATCH, "objects from different contexts");
     if (l->prec != out->prec || l->prec != in->prec) return fail(CD_ERR_MISMATCH, "precision mismatch");
     if (out->base == in->base) return fail(CD_ERR_INVALID, "out must not alias in");
+    if (out->nrhs != 1 || in->nrhs != 1) return fail(CD_ERR_INVALID, "multi-RHS fields need coarse_dslash_apply_mrhs");
     const char *ob = static_cast<const char *>(out->base), *ib = static_cast<const char *>(in->base);
     const size_t need = coarse_field_bytes(l->ctx, l->prec);
     if (ob < ib + need && ib < ob + need) return fail(CD_ERR_INVALID, "out overlaps in");
@@ -897,6 +927,25 @@ int coarse_dslash_apply_dagger(const cd_links *l, cd_field *out, const cd_field 
 {
     API_BEGIN
     return do_apply(l, out, in, stream, 1);
+    API_END
+}
+
+int coarse_dslash_apply_mrhs(const cd_links *l, cd_field *out, const cd_field *in, int dagger, void *stream)
+{
+    API_BEGIN
+    if (!l || !out || !in) return fail(CD_ERR_INVALID, "links/out/in is NULL");
+    if (l->ctx != out->ctx || l->ctx != in->ctx) return fail(CD_ERR_MISMATCH, "objects from different contexts");
+    if (l->prec != CD_FP16 || out->prec != CD_FP16 || in->prec != CD_FP16)
+        return fail(CD_ERR_UNSUPPORTED, "the tensor-core multi-RHS path needs fp16 storage (links and fields)");
+    if (in->nrhs != out->nrhs) return fail(CD_ERR_MISMATCH, "nrhs mismatch");
+    if (in->nrhs % 128) return fail(CD_ERR_UNSUPPORTED, "nrhs must be a multiple of 128");
+    if (out->base == in->base) return fail(CD_ERR_INVALID, "out must not alias in");
+    cd_context *c = l->ctx;
+    if (c->kg.split != 0) return fail(CD_ERR_UNSUPPORTED, "apply_mrhs is single-rank (no halo split) for now");
+    c->applied = true;
+    CUDA_TRY(launch_mrhs(c->nvec, l->base, in->base, out->base, c->kg, in->nrhs, dagger ? 1 : 0, S(stream)),
+             "mrhs launch");
+    return CD_OK;
     API_END
 }
 

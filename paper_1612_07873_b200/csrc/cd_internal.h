@@ -115,6 +115,7 @@ struct cd_field {
     void *base;
     size_t bytes;
     bool owned;
+    int nrhs;   // right-hand sides (records stored [site][rhs]); 1 for an ordinary field
 };
 
 struct cd_links {
@@ -160,15 +161,17 @@ cudaError_t launch_halo(cd_precision p, const ApplyArgs &a, cudaStream_t s);
 cudaError_t launch_pack(cd_precision p, int nvec, const void *field, void *send, const KGeom &g, cudaStream_t s);
 
 cudaError_t launch_import(cd_precision p, int nvec, int64_t nsites, const void *src, int src_c128, void *dst,
-                          cudaStream_t s);
+                          cudaStream_t s, int nrhs = 1);
 cudaError_t launch_export(cd_precision p, int nvec, int64_t nsites, const void *src, void *dst, int dst_c128,
-                          cudaStream_t s);
+                          cudaStream_t s, int nrhs = 1);
 cudaError_t launch_links_convert(cd_precision p, int nvec, int64_t nmats, const void *src, int src_c128, void *dst,
                                  cudaStream_t s, int64_t mat0);
 cudaError_t launch_links_generate(cd_precision p, int nvec, const cd_context *ctx, int kind, uint64_t seed,
                                   int scale_log2, void *dst, cudaStream_t s);
 cudaError_t launch_field_generate(cd_precision p, int nvec, const cd_context *ctx, uint64_t seed, uint32_t tag,
-                                  int scale_log2, void *dst, cudaStream_t s);
+                                  int scale_log2, void *dst, cudaStream_t s, int nrhs = 1);
+cudaError_t launch_mrhs(int nvec, const void *links, const void *in, void *out, const KGeom &g, int nrhs, int dagger,
+                        cudaStream_t s);
 cudaError_t launch_flush(void *buf, size_t bytes, cudaStream_t s);
 
 void count_launch(int n = 1);

@@ -42,13 +42,13 @@ __device__ __forceinline__ float2 load_canon(const void *src, int c128, size_t e
     return static_cast<const float2 *>(src)[e];
 }
 
-// canonical vector [V][N] -> stored records; one warp per site
-__global__ void import_kernel(int fp16, int N, int64_t nsites, const void *src, int c128, unsigned char *dst)
+// canonical vector(s) [rhs][V][N] -> stored records [site][rhs]; one warp per record
+__global__ void import_kernel(int fp16, int N, int64_t nsites, const void *src, int c128, unsigned char *dst, int nrhs)
 {
     const int lane = threadIdx.x & 31;
-    const int64_t site = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (site >= nsites) return;
-    const size_t base = (size_t)site * N;
+    const int64_t site = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);   // record index
+    if (site >= nsites * nrhs) return;
+    const size_t base = ((size_t)(site % nrhs) * nsites + (size_t)(site / nrhs)) * N;
     if (!fp16) {
         float2 *o = reinterpret_cast<float2 *>(dst + (size_t)site * 8 * N);
         for (int i = lane; i < N; i += 32) o[i] = load_canon(src, c128, base + i);
@@ -73,13 +73,13 @@ __global__ void import_kernel(int fp16, int N, int64_t nsites, const void *src, 
     if (lane == 0) *reinterpret_cast<float *>(rec + 4 * N) = m;
 }
 
-// stored records -> canonical vector (fp16: x = float(q) * s in fp32)
-__global__ void export_kernel(int fp16, int N, int64_t nsites, const unsigned char *src, void *dst, int c128)
+// stored records [site][rhs] -> canonical vector(s) [rhs][V][N] (fp16: x = float(q) * s in fp32)
+__global__ void export_kernel(int fp16, int N, int64_t nsites, const unsigned char *src, void *dst, int c128, int nrhs)
 {
     const int lane = threadIdx.x & 31;
-    const int64_t site = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (site >= nsites) return;
-    const size_t base = (size_t)site * N;
+    const int64_t site = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);   // record index
+    if (site >= nsites * nrhs) return;
+    const size_t base = ((size_t)(site % nrhs) * nsites + (size_t)(site / nrhs)) * N;
     for (int i = lane; i < N; i += 32) {
         float2 v;
         if (!fp16) {
@@ -223,13 +223,15 @@ __global__ void __launch_bounds__(BS) links_generate_kernel(int fp16, int N, Gen
     if (threadIdx.x == 0) *reinterpret_cast<float4 *>(rec + 4 * NN) = make_float4(sc, 0.f, 0.f, 0.f);
 }
 
-// one warp per local site
-__global__ void field_generate_kernel(int fp16, int N, int64_t nsites, GenGeom g, uint64_t base, float scale,
-                                      unsigned char *dst)
+// one warp per record [site][rhs]; right-hand side r uses tag + r
+__global__ void field_generate_kernel(int fp16, int N, int64_t nsites, GenGeom g, uint64_t seed, uint32_t tag,
+                                      float scale, unsigned char *dst, int nrhs)
 {
     const int lane = threadIdx.x & 31;
-    const int64_t s = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (s >= nsites) return;
+    const int64_t e = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (e >= nsites * nrhs) return;
+    const int64_t s = e / nrhs;
+    const uint64_t base = splitmix(seed ^ ((uint64_t)(tag + (uint32_t)(e % nrhs)) << 56));
     int xg[4];
     local_to_global(g, s, xg);
     const int64_t gs = gindex(g, xg);
@@ -247,7 +249,7 @@ __global__ void field_generate_kernel(int fp16, int N, int64_t nsites, GenGeom g
         m = fmaxf(m, fmaxf(fabsf(v[t].x), fabsf(v[t].y)));
     }
     if (!fp16) {
-        float2 *o = reinterpret_cast<float2 *>(dst + (size_t)s * 8 * N);
+        float2 *o = reinterpret_cast<float2 *>(dst + (size_t)e * 8 * N);
 #pragma unroll
         for (int t = 0; t < 2; t++)
             if (lane + 32 * t < N) o[lane + 32 * t] = v[t];
@@ -255,7 +257,7 @@ __global__ void field_generate_kernel(int fp16, int N, int64_t nsites, GenGeom g
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, shfl_xor(m, o));
-    unsigned char *rec = dst + (size_t)s * (4 * N + 16);
+    unsigned char *rec = dst + (size_t)e * (4 * N + 16);
 #pragma unroll
     for (int t = 0; t < 2; t++)
         if (lane + 32 * t < N) reinterpret_cast<__half2 *>(rec)[lane + 32 * t] = quant2(v[t].x, v[t].y, m);
@@ -289,22 +291,22 @@ static GenGeom gen_geom(const cd_context *ctx)
 }
 
 cudaError_t launch_import(cd_precision p, int nvec, int64_t nsites, const void *src, int src_c128, void *dst,
-                          cudaStream_t s)
+                          cudaStream_t s, int nrhs)
 {
     if (nsites == 0) return cudaSuccess;
     count_launch();
-    import_kernel<<<(unsigned)((nsites + 7) / 8), 256, 0, s>>>(p == CD_FP16, 2 * nvec, nsites, src, src_c128,
-                                                                  static_cast<unsigned char *>(dst));
+    import_kernel<<<(unsigned)((nsites * nrhs + 7) / 8), 256, 0, s>>>(p == CD_FP16, 2 * nvec, nsites, src, src_c128,
+                                                                         static_cast<unsigned char *>(dst), nrhs);
     return cudaGetLastError();
 }
 
 cudaError_t launch_export(cd_precision p, int nvec, int64_t nsites, const void *src, void *dst, int dst_c128,
-                          cudaStream_t s)
+                          cudaStream_t s, int nrhs)
 {
     if (nsites == 0) return cudaSuccess;
     count_launch();
-    export_kernel<<<(unsigned)((nsites + 7) / 8), 256, 0, s>>>(p == CD_FP16, 2 * nvec, nsites,
-                                                                  static_cast<const unsigned char *>(src), dst, dst_c128);
+    export_kernel<<<(unsigned)((nsites * nrhs + 7) / 8), 256, 0, s>>>(
+        p == CD_FP16, 2 * nvec, nsites, static_cast<const unsigned char *>(src), dst, dst_c128, nrhs);
     return cudaGetLastError();
 }
 
@@ -331,13 +333,12 @@ cudaError_t launch_links_generate(cd_precision p, int nvec, const cd_context *ct
 }
 
 cudaError_t launch_field_generate(cd_precision p, int nvec, const cd_context *ctx, uint64_t seed, uint32_t tag,
-                                  int scale_log2, void *dst, cudaStream_t s)
+                                  int scale_log2, void *dst, cudaStream_t s, int nrhs)
 {
-    const uint64_t base = host_splitmix(seed ^ ((uint64_t)tag << 56));
     count_launch();
-    field_generate_kernel<<<(unsigned)((ctx->V + 7) / 8), 256, 0, s>>>(p == CD_FP16, 2 * nvec, ctx->V, gen_geom(ctx),
-                                                                       base, ldexpf(1.0f, scale_log2),
-                                                                       static_cast<unsigned char *>(dst));
+    field_generate_kernel<<<(unsigned)((ctx->V * nrhs + 7) / 8), 256, 0, s>>>(
+        p == CD_FP16, 2 * nvec, ctx->V, gen_geom(ctx), seed, tag, ldexpf(1.0f, scale_log2),
+        static_cast<unsigned char *>(dst), nrhs);
     return cudaGetLastError();
 }
 
