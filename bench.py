@@ -185,9 +185,70 @@ def ncu_traffic(prec, variant):
     the variant this run chose -- else None."""
     try:
         t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[f"8^4_nvec24_{prec}"]
-        return t["bytes"] if variant in t["kernel"] else None
+        return t[variant]["bytes"] if variant in t else None
     except Exception:
         return None
+
+
+def _events_us(torch, fn, reps):
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    fn(reps)
+    e1.record(s)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e3 / reps
+
+
+def extras(cd, perfmodel, torch, other_prec="fp16"):
+    """Secondary measurements (each a few hundred ms), reported under "also"."""
+    out = {}
+    nvec = WORKLOAD["nvec"]
+    # the 8^4 workload with the other storage precision
+    ctx = cd.Context(WORKLOAD["dims"], nvec)
+    L = ctx.links_generate(other_prec, scale_log2=-4)
+    a, b = ctx.field(other_prec), ctx.field(other_prec)
+    a.generate()
+
+    def chained(n):
+        x, y = a, b
+        for _ in range(n):
+            L.apply(y, x)
+            x, y = y, x
+    chained(20)
+    torch.cuda.synchronize()
+    us = _events_us(torch, chained, 500)
+    V = 4096
+    gbs = perfmodel.metric_bytes_per_site(nvec, other_prec) * V / us / 1e3
+    out[f"8^4_{other_prec}"] = {"us_per_apply": round(us, 2), "GFLOPS": round(perfmodel.flops_per_site(nvec) * V / us / 1e3, 1),
+                                "GBs": round(gbs, 1), "pct_of_8tbs": round(100 * gbs / 8000, 1),
+                                "variant": ctx.variants(other_prec)[ctx.chosen_variant(other_prec)]}
+    del L, a, b, ctx
+    # 2^4 coarsest grid (BASELINE.json configs[0] shape): n chained applies in one kernel
+    ctx = cd.Context((2, 2, 2, 2), nvec)
+    L = ctx.links_generate("fp32", scale_log2=-4)
+    a, b = ctx.field("fp32"), ctx.field("fp32")
+    a.generate()
+    L.apply_chain(a, b, 8)
+    torch.cuda.synchronize()
+    us = _events_us(torch, lambda n: L.apply_chain(a, b, n), 2000)
+    gbs = perfmodel.metric_bytes_per_site(nvec, "fp32") * 16 / us / 1e3
+    out["2^4_fp32_chain"] = {"us_per_apply": round(us, 3), "GBs_effective": round(gbs, 1),
+                             "pct_of_8tbs": round(100 * gbs / 8000, 1),
+                             "note": "coarse_dslash_apply_chain (one persistent kernel, L2/on-chip resident)"}
+    del L, a, b, ctx
+    # 128 right-hand sides on the tcgen05 tensor cores (fp16 storage), 8^4
+    ctx = cd.Context(WORKLOAD["dims"], nvec)
+    L = ctx.links_generate("fp16", scale_log2=-4)
+    a, b = ctx.field("fp16", nrhs=128), ctx.field("fp16", nrhs=128)
+    a.generate()
+    L.apply_mrhs(b, a)
+    torch.cuda.synchronize()
+    us = _events_us(torch, lambda n: [L.apply_mrhs(b, a) for _ in range(n)], 10)
+    out["8^4_fp16_mrhs128"] = {"us_per_apply": round(us, 1), "us_per_rhs": round(us / 128, 3),
+                               "TFLOPS": round(perfmodel.flops_per_site(nvec) * V * 128 / us / 1e6, 1),
+                               "note": "coarse_dslash_apply_mrhs, tcgen05.mma kind::f16, fp32 accumulators in TMEM"}
+    return out
 
 
 # ------------------------------------------------------------------ our arm
@@ -279,6 +340,12 @@ def run_ours(args):
     ms_e2e = dist_max(f0.elapsed_time(f1) / k_e2e, world, device=f"cuda:{local}")
     e2e_val = flops / (ms_e2e * 1e-3) / 1e9
 
+    # ---- informational extras on one GPU (not the headline): fp16 storage, the 2^4 coarsest
+    # grid as chained applies in one kernel, 128 right-hand sides on the tcgen05 tensor cores
+    also = None
+    if world == 1 and not args.no_extras:
+        also = extras(cd, perfmodel, torch, other_prec="fp16" if prec == "fp32" else "fp32")
+
     # ---- cpu baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -319,6 +386,7 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "clocks": clocks,
             "cpu_baseline": cpu,
+            "also": also,
         }
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -378,6 +446,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--prec", choices=["fp32", "fp16"], default="fp32")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-extras", action="store_true", help="skip the informational 'also' measurements")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-budget", type=float, default=90.0)
     args = ap.parse_args()
