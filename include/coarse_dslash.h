@@ -196,6 +196,16 @@ int coarse_links_read_stored(const cd_links *l, void *dst, int dst_on_device, vo
 
 int coarse_links_free(cd_links *l);
 
+/* Hermiticity-compressed links: for tau3-hermitian operators -- every Galerkin
+ * coarse operator with chirality-preserving aggregation, PAPER.md:121 fn. 1 -- the backward links
+ * are L_{2mu+1}(x) = tau3 L_{2mu}(x-mu)^H tau3, so only X and the four forward links are stored
+ * (5 of 9 matrices per site; the apply reads the neighbour's forward link transposed).  Creates a
+ * new links object from `full`; if max_dev != NULL it first measures (host sync) the largest
+ * deviation |L_{2mu+1}(x) - tau3 L_{2mu}(x-mu)^H tau3| (fp32 links only) so the caller can
+ * decide whether the compression is exact.  Applies with compressed links: fp32, single rank
+ * (CD_ERR_UNSUPPORTED otherwise). */
+int coarse_links_compress_hermitian(const cd_links *full, double *max_dev, void *stream, cd_links **out);
+
 /* ------------------------------------------------------------------ operator */
 
 /* out = D in  (Eq. 3).  in, out, links: same context and precision (else CD_ERR_MISMATCH);

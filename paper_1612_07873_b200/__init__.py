@@ -41,6 +41,7 @@ EXPORTS = (
     "coarse_links_stored_bytes", "coarse_links_read_stored", "coarse_links_free", "coarse_dslash_apply",
     "coarse_dslash_apply_dagger", "coarse_halo_pack", "cd_flush_l2", "cd_halo_plan_create",
     "coarse_dslash_apply_chain", "coarse_field_bytes_mrhs", "coarse_field_alloc_mrhs", "coarse_dslash_apply_mrhs",
+    "coarse_links_compress_hermitian",
 )
 
 
@@ -105,6 +106,7 @@ def _load():
         "coarse_field_bytes_mrhs": ([P, I, I], SZ),
         "coarse_field_alloc_mrhs": ([P, I, I, P, SZ, PP], I),
         "coarse_dslash_apply_mrhs": ([P, P, P, I, P], I),
+        "coarse_links_compress_hermitian": ([P, ctypes.POINTER(ctypes.c_double), P, PP], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -379,6 +381,14 @@ class Links:
 
     def apply_chain(self, x: Field, y: Field, n: int, dagger=False, stream=None):
         coarse_dslash_apply_chain(self.handle, x.handle, y.handle, n, dagger, stream)
+
+    def compress_hermitian(self, check=True, stream=None):
+        """tau3-hermitian compressed copy (X + 4 forward links per site); returns (Links, max_dev)."""
+        dev = ctypes.c_double(-1.0)
+        out = ctypes.c_void_p()
+        _check(lib.coarse_links_compress_hermitian(self.handle, ctypes.byref(dev) if check else None,
+                                                   _stream(stream), ctypes.byref(out)))
+        return Links(self.ctx, self.prec, out), (dev.value if check else None)
 
     def apply_mrhs(self, out: Field, in_: Field, dagger=False, stream=None):
         """out_r = D in_r for all right-hand sides (tcgen05 tensor cores, fp16 storage)."""

@@ -107,6 +107,33 @@ cudaError_t launch_chain(cd_precision p, int id, const ApplyArgs &a, int n, unsi
                 launch_chain_f32_32(id, a, n, base, s, sms, nrb), launch_chain_f16_24(id, a, n, base, s, sms, nrb),
                 launch_chain_f16_32(id, a, n, base, s, sms, nrb));
 }
+cudaError_t launch_fgh_f32_24(const ApplyArgs &, cudaStream_t, bool);
+cudaError_t launch_fgh_f32_32(const ApplyArgs &, cudaStream_t, bool);
+cudaError_t launch_fgh_f16_24(const ApplyArgs &, cudaStream_t, bool);
+cudaError_t launch_fgh_f16_32(const ApplyArgs &, cudaStream_t, bool);
+cudaError_t launch_compress_f32_24(const void *, void *, int64_t, cudaStream_t);
+cudaError_t launch_compress_f32_32(const void *, void *, int64_t, cudaStream_t);
+cudaError_t launch_compress_f16_24(const void *, void *, int64_t, cudaStream_t);
+cudaError_t launch_compress_f16_32(const void *, void *, int64_t, cudaStream_t);
+cudaError_t launch_hermdev_f32_24(const void *, const KGeom &, float *, cudaStream_t);
+cudaError_t launch_hermdev_f32_32(const void *, const KGeom &, float *, cudaStream_t);
+cudaError_t launch_hermdev_f16_24(const void *, const KGeom &, float *, cudaStream_t);
+cudaError_t launch_hermdev_f16_32(const void *, const KGeom &, float *, cudaStream_t);
+cudaError_t launch_fgh(cd_precision p, const ApplyArgs &a, cudaStream_t s, bool pdl)
+{
+    return PICK(p, a.nvec, launch_fgh_f32_24(a, s, pdl), launch_fgh_f32_32(a, s, pdl), launch_fgh_f16_24(a, s, pdl),
+                launch_fgh_f16_32(a, s, pdl));
+}
+cudaError_t launch_compress(cd_precision p, int nv, const void *f, void *c, int64_t n, cudaStream_t s)
+{
+    return PICK(p, nv, launch_compress_f32_24(f, c, n, s), launch_compress_f32_32(f, c, n, s),
+                launch_compress_f16_24(f, c, n, s), launch_compress_f16_32(f, c, n, s));
+}
+cudaError_t launch_hermdev(cd_precision p, int nv, const void *f, const KGeom &g, float *d, cudaStream_t s)
+{
+    return PICK(p, nv, launch_hermdev_f32_24(f, g, d, s), launch_hermdev_f32_32(f, g, d, s),
+                launch_hermdev_f16_24(f, g, d, s), launch_hermdev_f16_32(f, g, d, s));
+}
 cudaError_t launch_pack(cd_precision p, int nv, const void *f, void *d, const KGeom &g, cudaStream_t s)
 {
     return PICK(p, nv, launch_pack_f32_24(f, d, g, s), launch_pack_f32_32(f, d, g, s), launch_pack_f16_24(f, d, g, s),
@@ -665,15 +692,49 @@ int coarse_field_read_stored(const cd_field *f, void *dst, int dst_on_device, vo
 }
 
 // ------------------------------------------------------------------ links
-static int links_new(cd_context *c, cd_precision p, cd_links **out)
+static int links_new(cd_context *c, cd_precision p, cd_links **out, int compressed = 0)
 {
-    const size_t bytes = align256(mat_rec_bytes(c->N, p) * 9 * (size_t)c->V);
+    const size_t bytes = align256(mat_rec_bytes(c->N, p) * (compressed ? 5 : 9) * (size_t)c->V);
     void *mem = nullptr;
     CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
     cudaError_t e = cudaMalloc(&mem, bytes);
     if (e != cudaSuccess) return fail(CD_ERR_OOM, std::string("cudaMalloc(links): ") + cudaGetErrorString(e));
-    *out = new cd_links{c, p, mem, bytes};
+    *out = new cd_links{c, p, mem, bytes, compressed};
     return CD_OK;
+}
+
+int coarse_links_compress_hermitian(const cd_links *full, double *max_dev, void *stream, cd_links **out)
+{
+    API_BEGIN
+    if (!full || !out) return fail(CD_ERR_INVALID, "links/out is NULL");
+    if (full->compressed) return fail(CD_ERR_INVALID, "links are already compressed");
+    cd_context *c = full->ctx;
+    if (c->kg.split != 0) return fail(CD_ERR_UNSUPPORTED, "compressed links are single-rank (no link halo yet)");
+    cudaStream_t s = S(stream);
+    if (max_dev) {
+        if (full->prec != CD_FP32) return fail(CD_ERR_UNSUPPORTED, "the hermiticity check needs fp32 links");
+        float *d = nullptr;
+        CUDA_TRY(cudaMallocAsync(&d, sizeof(float), s), "cudaMallocAsync");
+        CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(float), s), "cudaMemsetAsync");
+        CUDA_TRY(launch_hermdev(full->prec, c->nvec, full->base, c->kg, d, s), "hermiticity check");
+        float h = 0.0f;
+        CUDA_TRY(cudaMemcpyAsync(&h, d, sizeof(float), cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
+        CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        cudaFree(d);
+        *max_dev = h;
+    }
+    cd_links *l = nullptr;
+    int r = links_new(c, full->prec, &l, 1);
+    if (r != CD_OK) return r;
+    cudaError_t e = launch_compress(full->prec, c->nvec, full->base, l->base, c->V, s);
+    if (e != cudaSuccess) {
+        cudaFree(l->base);
+        delete l;
+        return cuda_fail(e, "links compress");
+    }
+    *out = l;
+    return CD_OK;
+    API_END
 }
 
 int coarse_links_upload(cd_context *c, cd_precision p, const void *src, int src_on_device, cd_host_dtype dt,
@@ -752,7 +813,7 @@ int coarse_links_generate(cd_context *c, cd_precision p, int kind, uint64_t seed
 size_t coarse_links_stored_bytes(const cd_links *l)
 {
     if (!l) return 0;
-    const size_t nm = 9 * (size_t)l->ctx->V;
+    const size_t nm = (l->compressed ? 5 : 9) * (size_t)l->ctx->V;
     const size_t NN = (size_t)l->ctx->N * l->ctx->N;
     return l->prec == CD_FP32 ? 8 * NN * nm : 4 * NN * nm + 4 * nm;
 }
@@ -763,8 +824,8 @@ int coarse_links_read_stored(const cd_links *l, void *dst, int dst_on_device, vo
     if (!l || !dst) return fail(CD_ERR_INVALID, "links/dst is NULL");
     const size_t NN = (size_t)l->ctx->N * l->ctx->N;
     const bool f16 = l->prec == CD_FP16;
-    return read_stored(l->base, 9 * l->ctx->V, f16 ? 4 * NN : 8 * NN, mat_rec_bytes(l->ctx->N, l->prec), f16, dst,
-                       dst_on_device, S(stream));
+    return read_stored(l->base, (l->compressed ? 5 : 9) * l->ctx->V, f16 ? 4 * NN : 8 * NN,
+                       mat_rec_bytes(l->ctx->N, l->prec), f16, dst, dst_on_device, S(stream));
     API_END
 }
 
@@ -882,6 +943,13 @@ static int do_apply(const cd_links *l, cd_field *out, const cd_field *in, void *
     a.nvec = c->nvec;
     a.dagger = dag;
     const bool halo = c->kg.split != 0;
+    if (l->compressed) {   // tau3-hermitian compressed links (NEXT-2): one kernel, fp32, single rank
+        if (halo) return fail(CD_ERR_UNSUPPORTED, "compressed links are single-rank");
+        if (l->prec != CD_FP32) return fail(CD_ERR_UNSUPPORTED, "compressed links: fp32 storage only");
+        a.g = c->kg;
+        CUDA_TRY(launch_fgh(l->prec, a, s, c->pdl != 0), "compressed dslash launch");
+        return CD_OK;
+    }
     a.g = halo ? halo_geom(c, l->prec) : c->kg;
     a.halo = halo ? 1 : 0;
     a.scratch = c->face_scratch;

@@ -123,6 +123,7 @@ struct cd_links {
     cd_precision prec;
     void *base;
     size_t bytes;
+    int compressed;   // 1: tau3-hermitian compressed storage (X + 4 forward links per site)
 };
 
 namespace cd {
@@ -170,6 +171,9 @@ cudaError_t launch_links_generate(cd_precision p, int nvec, const cd_context *ct
                                   int scale_log2, void *dst, cudaStream_t s);
 cudaError_t launch_field_generate(cd_precision p, int nvec, const cd_context *ctx, uint64_t seed, uint32_t tag,
                                   int scale_log2, void *dst, cudaStream_t s, int nrhs = 1);
+cudaError_t launch_fgh(cd_precision p, const ApplyArgs &a, cudaStream_t s, bool pdl);
+cudaError_t launch_compress(cd_precision p, int nv, const void *full, void *comp, int64_t nsites, cudaStream_t s);
+cudaError_t launch_hermdev(cd_precision p, int nv, const void *full, const KGeom &g, float *dev, cudaStream_t s);
 cudaError_t launch_mrhs(int nvec, const void *links, const void *in, void *out, const KGeom &g, int nrhs, int dagger,
                         cudaStream_t s);
 cudaError_t launch_flush(void *buf, size_t bytes, cudaStream_t s);

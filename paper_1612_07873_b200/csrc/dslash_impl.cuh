@@ -387,6 +387,153 @@ __global__ void __launch_bounds__(FgCfg<P, NV, KW, WR>::THREADS) dslash_fg(Apply
     }
 }
 
+// ------------------------------------------------------------------ compressed (tau3-hermitian) links
+// for tau3-hermitian operators L_{2mu+1}(x) = tau3 L_{2mu}(x-mu)^H tau3 (PAPER.md:121
+// fn. 1), so only X and the four forward links are stored: record c of a site is
+// c = 0: X, c = 1 + mu: L_{2mu}.  The backward hop of x reads the forward link of x - mu
+// TRANSPOSED:  w_i = s_i sum_j conj(M_ji) s_j u_j  (s = tau3 signs, M = L_{2mu}(x-mu), u = v(x-mu)),
+// with lanes = (4 output rows i) x (8 groups of input rows j): each warp load is 8 rows x a
+// 32-byte strip of M (sector-exact), reduced over j with xor-shuffles.  CTA = (site, 4 rows),
+// one warp per hop (the fg kw1/wr1 decomposition).  fp32 storage.
+template <int NV>
+__global__ void __launch_bounds__(288, NV == 24 ? 3 : 2) dslash_fgh(ApplyArgs a)
+{
+    using Q = Cfg<CD_FP32, NV>;
+    constexpr int ROWS = 16;                 // output rows per CTA
+    constexpr int NRB = Q::N / ROWS;
+    constexpr int RG = ROWS / Q::R;          // forward: row groups of R = 4 rows per warp
+    constexpr int TJ = Q::N / 2;             // backward: input rows j per lane (2 j-groups)
+    __shared__ __align__(16) unsigned char vs[9 * Q::VREC];
+    __shared__ float2 part[9][ROWS];
+    const int site = blockIdx.x / NRB, rb = blockIdx.x - site * NRB;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int k = kseq(warp);   // X, then 0..7
+    const unsigned char *links = static_cast<const unsigned char *>(a.links);
+    const unsigned char *in = static_cast<const unsigned char *>(a.in);
+    int x[4];
+    decode(a.g, site, x);
+    const bool fwd = (k == 8) || !(k & 1);
+    // forward / X hop: own record; backward hop: forward record of the -mu neighbour
+    const int msite = fwd ? site : neighbour(a.g, x, site, k);
+    const int crec = (k == 8) ? 0 : 1 + (k >> 1);
+    const unsigned char *m = links + ((size_t)msite * 5 + crec) * Q::MREC;
+    const int r = lane / Q::D, d = lane % Q::D;           // forward mapping: (row, dot chunk)
+    const int il = lane & 15, gj = lane >> 4;             // backward mapping: (row i, j group)
+    uint4 Lc[RG][Q::C];
+    uint2 Mc[TJ];
+    if (fwd) {
+#pragma unroll
+        for (int g = 0; g < RG; g++)
+#pragma unroll
+            for (int c = 0; c < Q::C; c++)
+                Lc[g][c] = ld_stream(m + (rb * ROWS + g * Q::R + r) * Q::ROWB + (d + Q::D * c) * 16);
+    } else {
+#pragma unroll
+        for (int t = 0; t < TJ; t++) {   // rows j = gj + 2t: 2 x 128-byte column strips per instruction
+            const uint2 *p = reinterpret_cast<const uint2 *>(m + (size_t)(gj + 2 * t) * Q::ROWB + (rb * ROWS + il) * 8);
+            asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(Mc[t].x), "=r"(Mc[t].y) : "l"(p));
+        }
+    }
+    pdl_trigger();
+    pdl_wait();
+    for (int t = threadIdx.x; t < 9 * Q::VCH; t += 288) {
+        const int kk = t / Q::VCH, e = t - kk * Q::VCH;
+        const int nb = neighbour(a.g, x, site, kk);
+        *reinterpret_cast<uint4 *>(vs + kk * Q::VREC + e * 16) = ld_nc(in + (size_t)nb * Q::VREC + e * 16);
+    }
+    __syncthreads();
+    const float2 *vk = reinterpret_cast<const float2 *>(vs + k * Q::VREC);
+    if (fwd) {
+#pragma unroll
+        for (int g = 0; g < RG; g++) {
+            float re = 0.0f, im = 0.0f;
+#pragma unroll
+            for (int c = 0; c < Q::C; c++) {
+                const int q = d + Q::D * c;
+                uint4 vq = lds128(reinterpret_cast<const unsigned char *>(vk) + q * 16);
+                if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<false>(vq);
+                cmac2(Lc[g][c], vq, re, im);
+            }
+#pragma unroll
+            for (int o = Q::D / 2; o >= 1; o >>= 1) {
+                re += shfl_xor(re, o);
+                im += shfl_xor(im, o);
+            }
+            if (d == 0) part[warp][g * Q::R + r] = make_float2(re, im);
+        }
+    } else {
+        float re = 0.0f, im = 0.0f;
+#pragma unroll
+        for (int t = 0; t < TJ; t++) {
+            const int j = gj + 2 * t;
+            float2 u = vk[j];
+            // s_j of the tau3 structure, times the dagger's tau3 on the input
+            const bool neg = (j >= NV) != (a.dagger && j >= NV);
+            if (neg) u = make_float2(-u.x, -u.y);
+            const float ma = __uint_as_float(Mc[t].x), mb = __uint_as_float(Mc[t].y);
+            re = fmaf(ma, u.x, fmaf(mb, u.y, re));    // conj(M) u: (ma - i mb)(ux + i uy)
+            im = fmaf(ma, u.y, fmaf(-mb, u.x, im));
+        }
+        re += shfl_xor(re, 16);
+        im += shfl_xor(im, 16);
+        const int i = rb * ROWS + il;
+        const float si = (i >= NV) ? -1.0f : 1.0f;   // s_i of the tau3 structure
+        if (gj == 0) part[warp][il] = make_float2(si * re, si * im);
+    }
+    __syncthreads();
+    if (threadIdx.x < ROWS) {
+        float yr = 0.0f, yi = 0.0f;
+#pragma unroll
+        for (int w = 0; w < 9; w++) {
+            yr += part[w][threadIdx.x].x;
+            yi += part[w][threadIdx.x].y;
+        }
+        const int row = rb * ROWS + threadIdx.x;
+        const float sg = (a.dagger && row >= NV) ? -1.0f : 1.0f;
+        reinterpret_cast<float2 *>(static_cast<unsigned char *>(a.out) + (size_t)site * Q::VREC)[row] =
+            make_float2(sg * yr, sg * yi);
+    }
+}
+
+// full links -> compressed records (X, L_0, L_2, L_4, L_6 per site), one CTA per output record
+template <cd_precision P, int NV>
+__global__ void links_compress_kernel(const unsigned char *full, unsigned char *comp, int64_t nrec)
+{
+    using Q = Cfg<P, NV>;
+    const int64_t rec = blockIdx.x;
+    const int64_t site = rec / 5;
+    const int c = (int)(rec - site * 5);
+    const int k = c == 0 ? 8 : 2 * (c - 1);
+    const uint4 *src = reinterpret_cast<const uint4 *>(full + ((size_t)site * 9 + k) * Q::MREC);
+    uint4 *dst = reinterpret_cast<uint4 *>(comp + (size_t)rec * Q::MREC);
+    for (int e = threadIdx.x; e < Q::MREC / 16; e += blockDim.x) dst[e] = src[e];
+}
+
+// max |L_{2mu+1}(x) - tau3 L_{2mu}(x-mu)^H tau3| over the lattice (fp32 links): the validity check
+// of the compression.  One CTA per (site, mu); result via an atomic max on the float bits (>= 0).
+template <int NV>
+__global__ void links_herm_dev_kernel(const unsigned char *full, KGeom g, float *dev)
+{
+    using Q = Cfg<CD_FP32, NV>;
+    const int site = blockIdx.x >> 2, mu = blockIdx.x & 3;
+    int x[4];
+    decode(g, site, x);
+    const int nb = neighbour(g, x, site, 2 * mu + 1);
+    const float2 *B = reinterpret_cast<const float2 *>(full + ((size_t)site * 9 + 2 * mu + 1) * Q::MREC);
+    const float2 *F = reinterpret_cast<const float2 *>(full + ((size_t)nb * 9 + 2 * mu) * Q::MREC);
+    float m = 0.0f;
+    for (int e = threadIdx.x; e < Q::N * Q::N; e += blockDim.x) {
+        const int i = e / Q::N, j = e - i * Q::N;
+        const float s = ((i < NV) == (j < NV)) ? 1.0f : -1.0f;
+        const float2 f = F[j * Q::N + i];
+        const float2 b = B[e];
+        m = fmaxf(m, fmaxf(fabsf(b.x - s * f.x), fabsf(b.y + s * f.y)));
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, shfl_xor(m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int *>(dev), __float_as_int(m));
+}
+
 // ------------------------------------------------------------------ CHAIN variant (latency regime)
 // n chained applies (t even: y = D x, t odd: x = D y) in ONE cooperative launch.  The CTA grid
 // is the FG decomposition; every CTA keeps its link rows in registers for all n applies (the
@@ -1230,6 +1377,35 @@ cudaError_t launch_pack_t(const void *field, void *send, const KGeom &g, cudaStr
         return dispatch_variant<P, NV, 0>(id, a, s, pdl, sms);                                                    \
     }                                                                                                             \
     cudaError_t launch_halo_##TAG(const ApplyArgs &a, cudaStream_t s) { return launch_halo_t<P, NV>(a, s); }      \
+    cudaError_t launch_fgh_##TAG(const ApplyArgs &a, cudaStream_t s, bool pdl)                                    \
+    {                                                                                                             \
+        if constexpr (P != CD_FP32) {                                                                             \
+            return cudaErrorNotSupported;                                                                         \
+        } else {                                                                                                  \
+            ApplyArgs aa = a;                                                                                     \
+            void *args[] = {&aa};                                                                                 \
+            return launch_ex((const void *)dslash_fgh<NV>, dim3((unsigned)(a.g.V * (2 * NV / 16))), dim3(288), 0, \
+                             s, pdl, args);                                                                       \
+        }                                                                                                         \
+    }                                                                                                             \
+    cudaError_t launch_compress_##TAG(const void *full, void *comp, int64_t nsites, cudaStream_t s)               \
+    {                                                                                                             \
+        count_launch();                                                                                           \
+        links_compress_kernel<P, NV><<<(unsigned)(nsites * 5), 256, 0, s>>>(                                      \
+            static_cast<const unsigned char *>(full), static_cast<unsigned char *>(comp), nsites * 5);             \
+        return cudaGetLastError();                                                                                \
+    }                                                                                                             \
+    cudaError_t launch_hermdev_##TAG(const void *full, const KGeom &g, float *dev, cudaStream_t s)                \
+    {                                                                                                             \
+        if constexpr (P != CD_FP32) {                                                                             \
+            return cudaErrorNotSupported;                                                                         \
+        } else {                                                                                                  \
+            count_launch();                                                                                       \
+            links_herm_dev_kernel<NV><<<(unsigned)(g.V * 4), 256, 0, s>>>(static_cast<const unsigned char *>(full), \
+                                                                         g, dev);                                 \
+            return cudaGetLastError();                                                                            \
+        }                                                                                                         \
+    }                                                                                                             \
     cudaError_t launch_chain_##TAG(int id, const ApplyArgs &a, int n, unsigned base, cudaStream_t s, int sms,     \
                                    int *nrb)                                                                      \
     {                                                                                                             \
