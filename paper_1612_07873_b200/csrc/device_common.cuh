@@ -101,6 +101,18 @@ __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src, uint32
         ::"r"((uint32_t)__cvta_generic_to_shared(dst_smem)), "l"(src), "r"(bytes),
           "r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
 }
+// 4-byte asynchronous shared-memory store whose completion is counted (4 tx bytes) on an
+// mbarrier: a value delivered exactly like TMA data, ordered by the barrier's phase.
+__device__ __forceinline__ void st_async_u32(void *dst_smem, uint32_t v, uint64_t *bar)
+{
+    // st.async addresses live in the shared::cluster window: map this CTA's own addresses there
+    uint32_t rank, d, b;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(d) : "r"((uint32_t)__cvta_generic_to_shared(dst_smem)), "r"(rank));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(b) : "r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(rank));
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(d), "r"(v), "r"(b)
+                 : "memory");
+}
 __device__ __forceinline__ void bar_named(int id, int nthreads)
 {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

@@ -135,8 +135,8 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
                 const int site = atomicAdd(tickets, 1);
                 if (site >= V) {   // sentinel stage: tells the consumers to stop
                     mbar_wait(&empty[stage], phase ^ 1);
-                    *reinterpret_cast<volatile int *>(&siteq[stage]) = -1;
-                    mbar_arrive(&full[stage]);
+                    mbar_arrive_expect_tx(&full[stage], 4);
+                    st_async_u32(&siteq[stage], 0xFFFFFFFFu, &full[stage]);
                     break;
                 }
                 int x[4];
@@ -147,9 +147,10 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
 #pragma unroll
                     for (int j = 0; j < MPS; j++) nvc += !(a.halo && remote_hop(a.g, x, gi * MPS + j));
                     mbar_wait(&empty[stage], phase ^ 1);
-                    if (gi == 0) *reinterpret_cast<volatile int *>(&siteq[stage]) = site;
                     unsigned char *st = stages + (size_t)stage * RC::STAGE;
-                    mbar_arrive_expect_tx(&full[stage], MPS * Q::MREC + nvc * Q::VREC);
+                    // the site id travels like the data: an async store counted on the same barrier
+                    mbar_arrive_expect_tx(&full[stage], MPS * Q::MREC + nvc * Q::VREC + (gi == 0 ? 4 : 0));
+                    if (gi == 0) st_async_u32(&siteq[stage], (uint32_t)site, &full[stage]);
                     bulk_g2s(st, lsite + (size_t)gi * MPS * Q::MREC, MPS * Q::MREC, &full[stage]);
 #pragma unroll
                     for (int j = 0; j < MPS; j++) {
@@ -1255,11 +1256,28 @@ cudaError_t launch_ring(const ApplyArgs &a, cudaStream_t s, bool pdl, int num_sm
         if (e != cudaSuccess) return e;
         attr = true;
     }
+    // 2-CTA clusters (148 SMs = 74 TPC pairs): st.async (the site-id handoff) needs a cluster of >= 2
     int grid = a.g.V < num_sms ? a.g.V : num_sms;
+    grid = (grid + 1) & ~1;
     ApplyArgs aa = a;
     int slot = a.seq & (RC::SLOTS - 1);
     void *args[] = {&aa, &slot};
-    return launch_ex((const void *)dslash_ring<P, NV, MPS>, dim3(grid), dim3(RC::THREADS), RC::SMEM, s, pdl, args);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(RC::THREADS);
+    cfg.dynamicSmemBytes = RC::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = 2;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    count_launch();
+    return cudaLaunchKernelExC(&cfg, (const void *)dslash_ring<P, NV, MPS>, args);
 }
 
 template <cd_precision P, int NV, int KW, int WR>

@@ -1,0 +1,47 @@
+"""Small invocation of every kernel family (run under compute-sanitizer by tests/test_sanitizers.py)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+import torch  # noqa: E402
+
+import paper_1612_07873_b200 as cd  # noqa: E402
+
+which = sys.argv[1] if len(sys.argv) > 1 else "all"
+os.environ.setdefault("CD_TUNE", "0")
+for prec in ("fp32", "fp16"):
+    ctx = cd.Context((2, 2, 2, 2), 24)
+    L = ctx.links_generate(prec, kind="hermitian", scale_log2=-4)
+    a, b = ctx.field(prec), ctx.field(prec)
+    a.generate()
+    if which in ("all", "apply"):
+        for v in range(len(ctx.variants(prec))):
+            ctx.set_option(cd.CD_OPT_VARIANT, v)
+            L.apply(b, a)
+            L.apply_dagger(a, b)
+    if which in ("all", "chain"):
+        for v in [1000, 2001, 2002, 1]:
+            ctx.set_option(cd.CD_OPT_VARIANT, v)
+            try:
+                L.apply_chain(a, b, 3)
+            except cd.CDError:
+                pass
+    if which in ("all", "halo"):
+        h = cd.Context((2, 2, 2, 4), 24)
+        h.set_option(cd.CD_OPT_HALO_SELF_MASK, 0b1100)
+        Lh = h.links_generate(prec, scale_log2=-4)
+        x, y = h.field(prec), h.field(prec)
+        x.generate()
+        for v in range(len(h.variants(prec))):
+            h.set_option(cd.CD_OPT_VARIANT, v)
+            Lh.apply(y, x)
+    if which in ("all", "mrhs") and prec == "fp16":
+        x, y = ctx.field("fp16", nrhs=128), ctx.field("fp16", nrhs=128)
+        x.generate()
+        L.apply_mrhs(y, x)
+    if which in ("all", "compressed") and prec == "fp32":
+        C, _ = L.compress_hermitian()
+        ctx.set_option(cd.CD_OPT_VARIANT, -1)
+        C.apply(b, a)
+torch.cuda.synchronize()
+print("sanitize run ok")
