@@ -54,6 +54,8 @@ def _load():
             lib.oracle_site_apply.argtypes = [ctypes.c_int, P, P, P]
             lib.oracle_quantise_fp16.argtypes = [ctypes.c_int64, ctypes.c_int64, P, P, P]
             lib.oracle_dequantise_fp16.argtypes = [ctypes.c_int64, ctypes.c_int64, P, P, P]
+            lib.oracle_invert.argtypes = [ctypes.c_int, P, P]
+            lib.oracle_schur_apply.argtypes = [I4, ctypes.c_int, P, P, P]
             _lib = lib
     return _lib
 
@@ -186,3 +188,37 @@ def dequantise_fp16(q, s, reals_per_rec: int):
     x = np.empty(q.size, np.float64)
     _load().oracle_dequantise_fp16(s.size, reals_per_rec, q.ctypes.data, s.ctypes.data, x.ctypes.data)
     return x.view(np.complex128)
+
+
+def invert(A):
+    """N x N complex inverse by Gauss-Jordan with partial pivoting (fp64)."""
+    A = np.ascontiguousarray(A, dtype=np.complex128)
+    N = A.shape[0]
+    out = np.empty_like(A)
+    if _load().oracle_invert(N, A.ctypes.data, out.ctypes.data) != 0:
+        raise ValueError("singular matrix")
+    return out
+
+
+def parity(dims):
+    """Site parity (x0+x1+x2+x3) mod 2 of every site, canonical order."""
+    V = int(np.prod(dims))
+    s = np.arange(V)
+    x0 = s % dims[0]; s1 = s // dims[0]
+    x1 = s1 % dims[1]; s2 = s1 // dims[1]
+    x2 = s2 % dims[2]; x3 = s2 // dims[2]
+    return (x0 + x1 + x2 + x3) & 1
+
+
+def schur_apply(dims, links, v):
+    """Even-odd Schur complement y_e = X_e v_e - D_eo X_o^-1 D_oe v_e on FULL fields (only even
+    sites read / written; odd sites of y are 0).  PAPER.md:95 §3.3."""
+    if any(int(d) % 2 for d in dims):
+        raise ValueError("even-odd needs every L_mu even")
+    V, N = _geom(dims, links)
+    L = _c128(links, (V, 9, N, N))
+    x = _c128(v, (V, N))
+    y = np.empty((V, N), np.complex128)
+    if _load().oracle_schur_apply(_dims(dims), N, L.ctypes.data, x.ctypes.data, y.ctypes.data) != 0:
+        raise ValueError("singular X on an odd site")
+    return y

@@ -395,3 +395,100 @@ void oracle_dequantise_fp16(int64_t nrec, int64_t reals_per_rec, const uint16_t 
             x[r * reals_per_rec + e] = (double)((float)h * scale[r]);
         }
 }
+
+/* ---------------------------------------------------------------- even-odd */
+
+/* Inverse of an N x N complex matrix by Gauss-Jordan elimination with partial pivoting
+ * (textbook; fp64).  Returns 0 on success, -1 if singular. */
+int oracle_invert(int N, const double *A_, double *Ainv_)
+{
+    const cplx *A = (const cplx *)A_;
+    cplx *Ainv = (cplx *)Ainv_;
+    cplx *M = (cplx *)malloc(sizeof(cplx) * N * 2 * N);
+    for (int i = 0; i < N; i++)
+        for (int j = 0; j < 2 * N; j++)
+            M[i * 2 * N + j] = j < N ? A[i * N + j] : (j - N == i ? 1.0 : 0.0);
+    for (int c = 0; c < N; c++) {
+        int p = c;
+        for (int i = c + 1; i < N; i++)
+            if (cabs(M[i * 2 * N + c]) > cabs(M[p * 2 * N + c])) p = i;
+        if (cabs(M[p * 2 * N + c]) == 0.0) {
+            free(M);
+            return -1;
+        }
+        if (p != c)
+            for (int j = 0; j < 2 * N; j++) {
+                cplx t = M[c * 2 * N + j];
+                M[c * 2 * N + j] = M[p * 2 * N + j];
+                M[p * 2 * N + j] = t;
+            }
+        cplx piv = M[c * 2 * N + c];
+        for (int j = 0; j < 2 * N; j++) M[c * 2 * N + j] /= piv;
+        for (int i = 0; i < N; i++) {
+            if (i == c) continue;
+            cplx f = M[i * 2 * N + c];
+            if (f == 0) continue;
+            for (int j = 0; j < 2 * N; j++) M[i * 2 * N + j] -= f * M[c * 2 * N + j];
+        }
+    }
+    for (int i = 0; i < N; i++)
+        for (int j = 0; j < N; j++) Ainv[i * N + j] = M[i * 2 * N + N + j];
+    free(M);
+    return 0;
+}
+
+/* Even-odd Schur complement (red-black preconditioning, §3.3, used on all MG
+ * levels), written from its definition on the full lattice:
+ *     y_e = X_e v_e - D_eo X_o^{-1} D_oe v_e
+ * where site parity = (x0+x1+x2+x3) mod 2 (every L_mu even), D_oe = the hopping terms from
+ * even to odd sites, D_eo from odd to even.  v and y are FULL fields [V][N]; only their even
+ * sites are read / written (odd sites of y are set to 0).  Returns -1 if an X_o is singular. */
+int oracle_schur_apply(const int L[4], int N, const double *links_, const double *v_, double *y_)
+{
+    const cplx *links = (const cplx *)links_;
+    const cplx *v = (const cplx *)v_;
+    cplx *y = (cplx *)y_;
+    const int64_t V = volume_of(L);
+    const int64_t NN = (int64_t)N * N;
+    cplx *t = (cplx *)calloc((size_t)V * N, sizeof(cplx));
+    cplx *Xi = (cplx *)malloc(sizeof(cplx) * NN);
+    int status = 0;
+    for (int64_t s = 0; s < V && status == 0; s++) {   /* t_o = X_o^{-1} D_oe v_e */
+        int x[4];
+        coords_of(L, s, x);
+        if (((x[0] + x[1] + x[2] + x[3]) & 1) == 0) continue;
+        cplx u[MAXN];
+        for (int i = 0; i < N; i++) u[i] = 0;
+        int64_t nb[9];
+        oracle_neighbours(L, s, nb);
+        for (int k = 0; k < 8; k++) matvec_acc(N, links + (s * 9 + k) * NN, v + nb[k] * N, u);
+        if (oracle_invert(N, (const double *)(links + (s * 9 + 8) * NN), (double *)Xi) != 0) {
+            status = -1;
+            break;
+        }
+        for (int i = 0; i < N; i++) {
+            cplx a = 0;
+            for (int j = 0; j < N; j++) a += Xi[i * N + j] * u[j];
+            t[s * N + i] = a;
+        }
+    }
+    for (int64_t s = 0; s < V; s++) {                  /* y_e = X_e v_e - D_eo t_o */
+        int x[4];
+        coords_of(L, s, x);
+        cplx acc[MAXN];
+        for (int i = 0; i < N; i++) acc[i] = 0;
+        if (((x[0] + x[1] + x[2] + x[3]) & 1) == 0) {
+            cplx hopsum[MAXN];
+            for (int i = 0; i < N; i++) hopsum[i] = 0;
+            int64_t nb[9];
+            oracle_neighbours(L, s, nb);
+            matvec_acc(N, links + (s * 9 + 8) * NN, v + s * N, acc);
+            for (int k = 0; k < 8; k++) matvec_acc(N, links + (s * 9 + k) * NN, t + nb[k] * N, hopsum);
+            for (int i = 0; i < N; i++) acc[i] -= hopsum[i];
+        }
+        for (int i = 0; i < N; i++) y[s * N + i] = acc[i];
+    }
+    free(t);
+    free(Xi);
+    return status;
+}
