@@ -234,6 +234,26 @@ int coarse_dslash_apply_chain(const cd_links *links, cd_field *x, cd_field *y, i
  * contexts only in this version. */
 int coarse_dslash_apply_mrhs(const cd_links *links, cd_field *out, const cd_field *in, int dagger, void *stream);
 
+/* ------------------------------------------------------------------ even-odd
+ * Red-black preconditioning (§3.3; used on all MG levels): the Schur
+ * complement on the even sites,  M_ee v_e = X_e v_e - D_eo X_o^{-1} D_oe v_e,  site parity
+ * (x0+x1+x2+x3) mod 2.  Needs every local L_mu even and a single rank; fp32 storage.
+ * Parity fields hold the V/2 sites of one parity in half-index order h = s >> 1 (canonical
+ * import/export layout [V/2][N]). */
+size_t coarse_field_bytes_parity(const cd_context *ctx, cd_precision prec);
+int coarse_field_alloc_parity(cd_context *ctx, cd_precision prec, int parity, void *device_mem, size_t bytes,
+                              cd_field **out);
+
+/* Setup: X_o^{-1} on every odd site (fp64 Gauss-Jordan with partial pivoting) and
+ * X_o^{-1} L_k(o) for its 8 hops, plus the even sites' 9 matrices; host-synchronous (returns
+ * CD_ERR_INVALID if some X_o is singular).  The result is a new links object for
+ * coarse_dslash_apply_eo only. */
+int coarse_links_prepare_eo(const cd_links *full, void *stream, cd_links **out);
+
+/* out_e = M_ee in_e (dagger != 0: tau3 M_ee tau3 = M_ee^H for tau3-hermitian links); two
+ * kernels: t_o = X_o^{-1} D_oe in_e, then out_e = X_e in_e - D_eo t_o. */
+int coarse_dslash_apply_eo(const cd_links *eo_links, cd_field *out, const cd_field *in, int dagger, void *stream);
+
 /* Halo send buffer of `in` in the canonical wire order (R13): packs on `stream`
  * and copies to dst (host or device).  *bytes receives the size; dst may be NULL to query. */
 int coarse_halo_pack(cd_context *ctx, const cd_field *in, void *dst, int dst_on_device, size_t *bytes,

@@ -41,7 +41,8 @@ EXPORTS = (
     "coarse_links_stored_bytes", "coarse_links_read_stored", "coarse_links_free", "coarse_dslash_apply",
     "coarse_dslash_apply_dagger", "coarse_halo_pack", "cd_flush_l2", "cd_halo_plan_create",
     "coarse_dslash_apply_chain", "coarse_field_bytes_mrhs", "coarse_field_alloc_mrhs", "coarse_dslash_apply_mrhs",
-    "coarse_links_compress_hermitian",
+    "coarse_links_compress_hermitian", "coarse_field_bytes_parity", "coarse_field_alloc_parity",
+    "coarse_links_prepare_eo", "coarse_dslash_apply_eo",
 )
 
 
@@ -107,6 +108,10 @@ def _load():
         "coarse_field_alloc_mrhs": ([P, I, I, P, SZ, PP], I),
         "coarse_dslash_apply_mrhs": ([P, P, P, I, P], I),
         "coarse_links_compress_hermitian": ([P, ctypes.POINTER(ctypes.c_double), P, PP], I),
+        "coarse_field_bytes_parity": ([P, I], SZ),
+        "coarse_field_alloc_parity": ([P, I, I, P, SZ, PP], I),
+        "coarse_links_prepare_eo": ([P, P, PP], I),
+        "coarse_dslash_apply_eo": ([P, P, P, I, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -272,8 +277,8 @@ class Context:
     def chosen_variant(self, prec, dagger=False):
         return lib.cd_context_chosen_variant(self.handle, PREC[prec], int(bool(dagger)))
 
-    def field(self, prec="fp32", torch_memory=True, nrhs=1):
-        return Field(self, prec, torch_memory, nrhs)
+    def field(self, prec="fp32", torch_memory=True, nrhs=1, parity=None):
+        return Field(self, prec, torch_memory, nrhs, parity)
 
     def links_upload(self, links, prec="fp32", stream=None):
         return Links(self, prec, coarse_links_upload(self.handle, prec, np.ascontiguousarray(links)
@@ -309,18 +314,26 @@ class Context:
 class Field:
     """A colour-spinor field in the library's stored layout (device memory from torch)."""
 
-    def __init__(self, ctx: Context, prec="fp32", torch_memory=True, nrhs=1):
+    def __init__(self, ctx: Context, prec="fp32", torch_memory=True, nrhs=1, parity=None):
         self.ctx = ctx
         self.prec = PREC[prec]
         self.nrhs = int(nrhs)
-        self.nbytes = int(lib.coarse_field_bytes_mrhs(ctx.handle, self.prec, self.nrhs))
+        self.parity = parity
+        self.sites = ctx.V if parity is None else ctx.V // 2
+        self.nbytes = int(lib.coarse_field_bytes_mrhs(ctx.handle, self.prec, self.nrhs) if parity is None
+                          else lib.coarse_field_bytes_parity(ctx.handle, self.prec))
         self._mem = None
         ptr = None
         if torch_memory:
             import torch
             self._mem = torch.empty(self.nbytes, dtype=torch.uint8, device="cuda")
             ptr = self._mem.data_ptr()
-        if self.nrhs == 1:
+        if parity is not None:
+            out = ctypes.c_void_p()
+            _check(lib.coarse_field_alloc_parity(ctx.handle, self.prec, int(parity), ptr, self.nbytes if ptr else 0,
+                                                 ctypes.byref(out)))
+            self.handle = out
+        elif self.nrhs == 1:
             self.handle = coarse_field_alloc(ctx.handle, self.prec, ptr, self.nbytes if ptr else 0)
         else:
             out = ctypes.c_void_p()
@@ -336,7 +349,7 @@ class Field:
 
     def export(self, dst=None, dtype=np.complex128, stream=None, sync=True):
         if dst is None:
-            shape = (self.ctx.V, self.ctx.N) if self.nrhs == 1 else (self.nrhs, self.ctx.V, self.ctx.N)
+            shape = (self.sites, self.ctx.N) if self.nrhs == 1 else (self.nrhs, self.sites, self.ctx.N)
             dst = np.empty(shape, dtype)
         p, dev, _ = _ptr(dst)
         _check(lib.coarse_field_export(self.handle, p, dev, CD_C128 if _is_c128(dst) else CD_C64, _stream(stream)))
@@ -381,6 +394,16 @@ class Links:
 
     def apply_chain(self, x: Field, y: Field, n: int, dagger=False, stream=None):
         coarse_dslash_apply_chain(self.handle, x.handle, y.handle, n, dagger, stream)
+
+    def prepare_eo(self, stream=None):
+        """Even-odd preconditioned operator (X_o^-1 L_k(o) precomputed); returns new Links."""
+        out = ctypes.c_void_p()
+        _check(lib.coarse_links_prepare_eo(self.handle, _stream(stream), ctypes.byref(out)))
+        return Links(self.ctx, self.prec, out)
+
+    def apply_eo(self, out: Field, in_: Field, dagger=False, stream=None):
+        """out_e = M_ee in_e (Schur complement on even sites; parity-0 fields)."""
+        _check(lib.coarse_dslash_apply_eo(self.handle, out.handle, in_.handle, int(bool(dagger)), _stream(stream)))
 
     def compress_hermitian(self, check=True, stream=None):
         """tau3-hermitian compressed copy (X + 4 forward links per site); returns (Links, max_dev)."""

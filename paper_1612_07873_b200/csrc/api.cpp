@@ -169,6 +169,7 @@ static int cuda_fail(cudaError_t e, const char *what)
     catch (...) { return fail(CD_ERR_INVALID, "unknown C++ exception"); }
 
 static cudaStream_t S(void *s) { return static_cast<cudaStream_t>(s); }
+static int64_t field_sites(const cd_field *f) { return f->parity < 0 ? f->ctx->V : f->ctx->V / 2; }
 
 // ------------------------------------------------------------------ decomposition + halo plan
 // Geometry checks shared by cd_context_create and cd_halo_plan_create.
@@ -534,7 +535,7 @@ int coarse_field_alloc(cd_context *c, cd_precision p, void *mem, size_t bytes, c
         if (reinterpret_cast<uintptr_t>(mem) % 256) return fail(CD_ERR_INVALID, "device_mem must be 256-B aligned");
         if (bytes < need) return fail(CD_ERR_INVALID, "device_mem too small (need coarse_field_bytes)");
     }
-    *out = new cd_field{c, p, mem, bytes, owned, 1};
+    *out = new cd_field{c, p, mem, bytes, owned, 1, -1};
     return CD_OK;
     API_END
 }
@@ -563,7 +564,7 @@ int coarse_field_alloc_mrhs(cd_context *c, cd_precision p, int nrhs, void *mem, 
         if (reinterpret_cast<uintptr_t>(mem) % 256) return fail(CD_ERR_INVALID, "device_mem must be 256-B aligned");
         if (bytes < need) return fail(CD_ERR_INVALID, "device_mem too small (need coarse_field_bytes_mrhs)");
     }
-    *out = new cd_field{c, p, mem, bytes, owned, nrhs};
+    *out = new cd_field{c, p, mem, bytes, owned, nrhs, -1};
     return CD_OK;
     API_END
 }
@@ -592,7 +593,7 @@ int coarse_field_import(cd_field *f, const void *src, int src_on_device, cd_host
     if (dt != CD_C64 && dt != CD_C128) return fail(CD_ERR_INVALID, "bad dtype");
     cd_context *c = f->ctx;
     const size_t elem = dt == CD_C128 ? 16 : 8;
-    const size_t bytes = elem * c->N * (size_t)c->V * f->nrhs;
+    const size_t bytes = elem * c->N * (size_t)field_sites(f) * f->nrhs;
     cudaStream_t s = S(stream);
     if (f->prec == CD_FP32 && dt == CD_C64 && f->nrhs == 1) {   // stored layout == canonical layout
         CUDA_TRY(cudaMemcpyAsync(f->base, src, bytes, src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
@@ -607,7 +608,7 @@ int coarse_field_import(cd_field *f, const void *src, int src_on_device, cd_host
         if (r != CD_OK) return r;
         dsrc = stage;
     }
-    CUDA_TRY(launch_import(f->prec, c->nvec, c->V, dsrc, dt == CD_C128, f->base, s, f->nrhs), "import kernel");
+    CUDA_TRY(launch_import(f->prec, c->nvec, field_sites(f), dsrc, dt == CD_C128, f->base, s, f->nrhs), "import kernel");
     if (stage) CUDA_TRY(cudaFreeAsync(stage, s), "cudaFreeAsync");
     return CD_OK;
     API_END
@@ -620,7 +621,7 @@ int coarse_field_export(const cd_field *f, void *dst, int dst_on_device, cd_host
     if (dt != CD_C64 && dt != CD_C128) return fail(CD_ERR_INVALID, "bad dtype");
     cd_context *c = f->ctx;
     const size_t elem = dt == CD_C128 ? 16 : 8;
-    const size_t bytes = elem * c->N * (size_t)c->V * f->nrhs;
+    const size_t bytes = elem * c->N * (size_t)field_sites(f) * f->nrhs;
     cudaStream_t s = S(stream);
     if (f->prec == CD_FP32 && dt == CD_C64 && f->nrhs == 1) {
         CUDA_TRY(cudaMemcpyAsync(dst, f->base, bytes, dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
@@ -633,7 +634,7 @@ int coarse_field_export(const cd_field *f, void *dst, int dst_on_device, cd_host
         CUDA_TRY(cudaMallocAsync(&stage, bytes, s), "cudaMallocAsync(stage)");
         ddst = stage;
     }
-    CUDA_TRY(launch_export(f->prec, c->nvec, c->V, f->base, ddst, dt == CD_C128, s, f->nrhs), "export kernel");
+    CUDA_TRY(launch_export(f->prec, c->nvec, field_sites(f), f->base, ddst, dt == CD_C128, s, f->nrhs), "export kernel");
     if (stage) {
         CUDA_TRY(cudaMemcpyAsync(dst, stage, bytes, cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(D2H)");
         CUDA_TRY(cudaFreeAsync(stage, s), "cudaFreeAsync");
@@ -647,6 +648,7 @@ int coarse_field_generate(cd_field *f, uint64_t seed, uint32_t tag, int32_t scal
     API_BEGIN
     if (!f) return fail(CD_ERR_INVALID, "field is NULL");
     if (scale_log2 < -60 || scale_log2 > 60) return fail(CD_ERR_INVALID, "scale_log2 out of range");
+    if (f->parity >= 0) return fail(CD_ERR_UNSUPPORTED, "generate: full-lattice fields only");
     CUDA_TRY(launch_field_generate(f->prec, f->ctx->nvec, f->ctx, seed, tag, scale_log2, f->base, S(stream), f->nrhs),
              "field generate");
     return CD_OK;
@@ -656,8 +658,9 @@ int coarse_field_generate(cd_field *f, uint64_t seed, uint32_t tag, int32_t scal
 size_t coarse_field_stored_bytes(const cd_field *f)
 {
     if (!f) return 0;
-    const size_t n = (size_t)f->ctx->V * f->ctx->N;
-    return f->prec == CD_FP32 ? 8 * n : 4 * n + 4 * (size_t)f->ctx->V;
+    const size_t recs = (size_t)field_sites(f) * f->nrhs;
+    const size_t n = recs * f->ctx->N;
+    return f->prec == CD_FP32 ? 8 * n : 4 * n + 4 * recs;
 }
 
 // internal records -> canonical raw (payloads contiguous, then scales), via the host
@@ -686,7 +689,7 @@ int coarse_field_read_stored(const cd_field *f, void *dst, int dst_on_device, vo
     if (!f || !dst) return fail(CD_ERR_INVALID, "field/dst is NULL");
     const int N = f->ctx->N;
     const bool f16 = f->prec == CD_FP16;
-    return read_stored(f->base, f->ctx->V, f16 ? 4 * N : 8 * N, vec_rec_bytes(N, f->prec), f16, dst, dst_on_device,
+    return read_stored(f->base, field_sites(f) * f->nrhs, f16 ? 4 * N : 8 * N, vec_rec_bytes(N, f->prec), f16, dst, dst_on_device,
                        S(stream));
     API_END
 }
@@ -699,7 +702,7 @@ static int links_new(cd_context *c, cd_precision p, cd_links **out, int compress
     CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
     cudaError_t e = cudaMalloc(&mem, bytes);
     if (e != cudaSuccess) return fail(CD_ERR_OOM, std::string("cudaMalloc(links): ") + cudaGetErrorString(e));
-    *out = new cd_links{c, p, mem, bytes, compressed};
+    *out = new cd_links{c, p, mem, bytes, compressed, 0, nullptr, nullptr};
     return CD_OK;
 }
 
@@ -833,6 +836,8 @@ int coarse_links_free(cd_links *l)
 {
     API_BEGIN
     if (!l) return fail(CD_ERR_INVALID, "links is NULL");
+    if (l->aux) cudaFree(l->aux);
+    if (l->tbuf) cudaFree(l->tbuf);
     cudaFree(l->base);
     delete l;
     return CD_OK;
@@ -847,6 +852,7 @@ static int check_objs(const cd_links *l, const cd_field *out, const cd_field *in
     if (l->prec != out->prec || l->prec != in->prec) return fail(CD_ERR_MISMATCH, "precision mismatch");
     if (out->base == in->base) return fail(CD_ERR_INVALID, "out must not alias in");
     if (out->nrhs != 1 || in->nrhs != 1) return fail(CD_ERR_INVALID, "multi-RHS fields need coarse_dslash_apply_mrhs");
+    if (out->parity >= 0 || in->parity >= 0) return fail(CD_ERR_INVALID, "parity fields need coarse_dslash_apply_eo");
     const char *ob = static_cast<const char *>(out->base), *ib = static_cast<const char *>(in->base);
     const size_t need = coarse_field_bytes(l->ctx, l->prec);
     if (ob < ib + need && ib < ob + need) return fail(CD_ERR_INVALID, "out overlaps in");
@@ -995,6 +1001,96 @@ int coarse_dslash_apply_dagger(const cd_links *l, cd_field *out, const cd_field 
 {
     API_BEGIN
     return do_apply(l, out, in, stream, 1);
+    API_END
+}
+
+// ------------------------------------------------------------------ even-odd (NEXT-3)
+static bool eo_geometry_ok(const cd_context *c)
+{
+    for (int mu = 0; mu < 4; mu++)
+        if (c->local[mu] % 2) return false;
+    return c->kg.split == 0;
+}
+
+size_t coarse_field_bytes_parity(const cd_context *c, cd_precision p)
+{
+    if (!c || (p != CD_FP32 && p != CD_FP16)) return 0;
+    return align256(vec_rec_bytes(c->N, p) * (size_t)(c->V / 2));
+}
+
+int coarse_field_alloc_parity(cd_context *c, cd_precision p, int parity, void *mem, size_t bytes, cd_field **out)
+{
+    API_BEGIN
+    if (!c || !out) return fail(CD_ERR_INVALID, "ctx/out is NULL");
+    if (p != CD_FP32 && p != CD_FP16) return fail(CD_ERR_INVALID, "bad precision");
+    if (parity != 0 && parity != 1) return fail(CD_ERR_INVALID, "parity must be 0 (even) or 1 (odd)");
+    if (!eo_geometry_ok(c)) return fail(CD_ERR_UNSUPPORTED, "even-odd needs every local L_mu even, single rank");
+    const size_t need = coarse_field_bytes_parity(c, p);
+    bool owned = false;
+    if (!mem) {
+        CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
+        cudaError_t e = cudaMalloc(&mem, need);
+        if (e != cudaSuccess) return fail(CD_ERR_OOM, std::string("cudaMalloc(field): ") + cudaGetErrorString(e));
+        bytes = need;
+        owned = true;
+    } else {
+        if (reinterpret_cast<uintptr_t>(mem) % 256) return fail(CD_ERR_INVALID, "device_mem must be 256-B aligned");
+        if (bytes < need) return fail(CD_ERR_INVALID, "device_mem too small (need coarse_field_bytes_parity)");
+    }
+    *out = new cd_field{c, p, mem, bytes, owned, 1, parity};
+    return CD_OK;
+    API_END
+}
+
+int coarse_links_prepare_eo(const cd_links *full, void *stream, cd_links **out)
+{
+    API_BEGIN
+    if (!full || !out) return fail(CD_ERR_INVALID, "links/out is NULL");
+    if (full->compressed || full->eo) return fail(CD_ERR_INVALID, "needs full (uncompressed) links");
+    if (full->prec != CD_FP32) return fail(CD_ERR_UNSUPPORTED, "even-odd: fp32 storage only");
+    cd_context *c = full->ctx;
+    if (!eo_geometry_ok(c)) return fail(CD_ERR_UNSUPPORTED, "even-odd needs every local L_mu even, single rank");
+    cudaStream_t s = S(stream);
+    const size_t mrec = mat_rec_bytes(c->N, CD_FP32);
+    const size_t half = (size_t)(c->V / 2);
+    void *even = nullptr, *odd = nullptr, *t = nullptr;
+    int *sing = nullptr;
+    CUDA_TRY(cudaMalloc(&even, align256(half * 9 * mrec)), "cudaMalloc(eo even)");
+    CUDA_TRY(cudaMalloc(&odd, align256(half * 8 * mrec)), "cudaMalloc(eo odd)");
+    CUDA_TRY(cudaMalloc(&t, align256(half * vec_rec_bytes(c->N, CD_FP32))), "cudaMalloc(eo t)");
+    CUDA_TRY(cudaMallocAsync(&sing, sizeof(int), s), "cudaMallocAsync");
+    CUDA_TRY(cudaMemsetAsync(sing, 0, sizeof(int), s), "cudaMemsetAsync");
+    CUDA_TRY(launch_eo_prepare(c->nvec, full->base, even, odd, c->kg, sing, s), "eo prepare");
+    int hs = 0;
+    CUDA_TRY(cudaMemcpyAsync(&hs, sing, sizeof(int), cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
+    CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    cudaFree(sing);
+    if (hs) {
+        cudaFree(even);
+        cudaFree(odd);
+        cudaFree(t);
+        return fail(CD_ERR_INVALID, "a diagonal block X on an odd site is singular");
+    }
+    *out = new cd_links{c, CD_FP32, even, align256(half * 9 * mrec), 0, 1, odd, t};
+    return CD_OK;
+    API_END
+}
+
+int coarse_dslash_apply_eo(const cd_links *l, cd_field *out, const cd_field *in, int dagger, void *stream)
+{
+    API_BEGIN
+    if (!l || !out || !in) return fail(CD_ERR_INVALID, "links/out/in is NULL");
+    if (!l->eo) return fail(CD_ERR_INVALID, "links not prepared with coarse_links_prepare_eo");
+    if (l->ctx != out->ctx || l->ctx != in->ctx) return fail(CD_ERR_MISMATCH, "objects from different contexts");
+    if (out->parity != 0 || in->parity != 0) return fail(CD_ERR_INVALID, "in/out must be even-parity fields");
+    if (out->prec != CD_FP32 || in->prec != CD_FP32) return fail(CD_ERR_MISMATCH, "even-odd: fp32 fields");
+    if (out->base == in->base) return fail(CD_ERR_INVALID, "out must not alias in");
+    cd_context *c = l->ctx;
+    c->applied = true;
+    CUDA_TRY(launch_eo_apply(c->nvec, l->base, l->aux, in->base, l->tbuf, out->base, c->kg, dagger ? 1 : 0, S(stream),
+                             c->pdl != 0),
+             "eo apply");
+    return CD_OK;
     API_END
 }
 

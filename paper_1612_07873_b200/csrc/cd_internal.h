@@ -116,6 +116,7 @@ struct cd_field {
     size_t bytes;
     bool owned;
     int nrhs;   // right-hand sides (records stored [site][rhs]); 1 for an ordinary field
+    int parity; // -1: full lattice; 0 / 1: the V/2 even / odd sites in half-index order (s >> 1)
 };
 
 struct cd_links {
@@ -124,6 +125,9 @@ struct cd_links {
     void *base;
     size_t bytes;
     int compressed;   // 1: tau3-hermitian compressed storage (X + 4 forward links per site)
+    int eo;           // 1: even-odd prepared: base = even sites [V/2][9], aux = odd [V/2][8] (X^-1 L_k)
+    void *aux;        // eo: odd-site records
+    void *tbuf;       // eo: odd half-field scratch t_o (fp32)
 };
 
 namespace cd {
@@ -171,6 +175,10 @@ cudaError_t launch_links_generate(cd_precision p, int nvec, const cd_context *ct
                                   int scale_log2, void *dst, cudaStream_t s);
 cudaError_t launch_field_generate(cd_precision p, int nvec, const cd_context *ctx, uint64_t seed, uint32_t tag,
                                   int scale_log2, void *dst, cudaStream_t s, int nrhs = 1);
+cudaError_t launch_eo_prepare(int nvec, const void *full, void *even, void *odd, const KGeom &g, int *singular,
+                              cudaStream_t s);
+cudaError_t launch_eo_apply(int nvec, const void *even, const void *odd, const void *in_e, void *t_o, void *out_e,
+                            const KGeom &g, int dagger, cudaStream_t s, bool pdl);
 cudaError_t launch_fgh(cd_precision p, const ApplyArgs &a, cudaStream_t s, bool pdl);
 cudaError_t launch_compress(cd_precision p, int nv, const void *full, void *comp, int64_t nsites, cudaStream_t s);
 cudaError_t launch_hermdev(cd_precision p, int nv, const void *full, const KGeom &g, float *dev, cudaStream_t s);
