@@ -56,6 +56,10 @@ def _load():
             lib.oracle_dequantise_fp16.argtypes = [ctypes.c_int64, ctypes.c_int64, P, P, P]
             lib.oracle_invert.argtypes = [ctypes.c_int, P, P]
             lib.oracle_schur_apply.argtypes = [I4, ctypes.c_int, P, P, P]
+            CI = ctypes.c_int
+            lib.oracle_prolong.argtypes = [I4, I4, CI, CI, CI, P, P, P]
+            lib.oracle_restrict.argtypes = [I4, I4, CI, CI, CI, P, P, P]
+            lib.oracle_block_orthonormalise.argtypes = [I4, I4, CI, CI, CI, P]
             _lib = lib
     return _lib
 
@@ -222,3 +226,39 @@ def schur_apply(dims, links, v):
     if _load().oracle_schur_apply(_dims(dims), N, L.ctypes.data, x.ctypes.data, y.ctypes.data) != 0:
         raise ValueError("singular X on an odd site")
     return y
+
+
+# ---------------------------------------------------------------- transfer operators
+# Fine lattice = coarse dims x block B; fine field [Vf, Ns, Nc]; basis W [Vf, Ns, Nc, Nvec];
+# coarse field [Vc, 2*Nvec] (§3.4; §6.6; R20).
+def fine_dims(cdims, block):
+    return tuple(int(c) * int(b) for c, b in zip(cdims, block))
+
+
+def prolong(cdims, block, Ns, Nc, Nvec, W, vc):
+    """vf = P vc (gather per fine dof)."""
+    Vf, Vc = int(np.prod(fine_dims(cdims, block))), int(np.prod(cdims))
+    Wc = _c128(W, (Vf, Ns, Nc, Nvec))
+    x = _c128(vc, (Vc, 2 * Nvec))
+    out = np.empty((Vf, Ns, Nc), np.complex128)
+    _load().oracle_prolong(_dims(cdims), _dims(block), Ns, Nc, Nvec, Wc.ctypes.data, x.ctypes.data, out.ctypes.data)
+    return out
+
+
+def restrict(cdims, block, Ns, Nc, Nvec, W, vf):
+    """vc = P^dagger vf (restrictor = hermitian conjugate of the prolongator)."""
+    Vf, Vc = int(np.prod(fine_dims(cdims, block))), int(np.prod(cdims))
+    Wc = _c128(W, (Vf, Ns, Nc, Nvec))
+    x = _c128(vf, (Vf, Ns, Nc))
+    out = np.empty((Vc, 2 * Nvec), np.complex128)
+    _load().oracle_restrict(_dims(cdims), _dims(block), Ns, Nc, Nvec, Wc.ctypes.data, x.ctypes.data, out.ctypes.data)
+    return out
+
+
+def block_orthonormalise(cdims, block, Ns, Nc, Nvec, W):
+    """Per (aggregate, chirality) block: Q of the QR decomposition by modified Gram-Schmidt."""
+    Vf = int(np.prod(fine_dims(cdims, block)))
+    Wc = _c128(W, (Vf, Ns, Nc, Nvec)).copy()
+    if _load().oracle_block_orthonormalise(_dims(cdims), _dims(block), Ns, Nc, Nvec, Wc.ctypes.data) != 0:
+        raise ValueError("rank-deficient aggregate block")
+    return Wc

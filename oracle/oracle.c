@@ -492,3 +492,131 @@ int oracle_schur_apply(const int L[4], int N, const double *links_, const double
     free(Xi);
     return status;
 }
+
+/* ---------------------------------------------------------------- transfer operators
+ *
+ * Adaptive geometric aggregation (§3.4, setup steps 3-4; kernels §6.6):
+ * the fine lattice Lf = Lc * B (regular non-overlapping hypercube aggregates of B0 x B1 x B2 x B3
+ * fine sites, "regular non-overlapping hypercubes"); fine site xf belongs to the aggregate
+ * (coarse site) xc = floor(xf / B).  A fine site carries Ns spins x Nc colours, dof r = s*Nc + a
+ * (spin slower, as on the coarse grid).  Chirality-preserving aggregation (P:121 fn. 1): spins
+ * s < Ns/2 form chirality 0, the rest chirality 1 (R20), so coarse dof i = sigma*Nvec + k.
+ * Basis (the prolongator's columns): W[((sf*Ns + s)*Nc + a)*Nvec + k], complex.
+ *
+ *   prolong : vf(xf, s, a)      = sum_k W(xf, s, a, k) vc(xc(xf), chi(s)*Nvec + k)
+ *   restrict: vc(xc, sigma*Nvec + k) = sum_{xf in xc} sum_{s: chi(s)=sigma} sum_a conj(W(xf,s,a,k)) vf(xf,s,a)
+ *             (restrictor = P^dagger)
+ */
+
+static int64_t aggregate_of(const int Lc[4], const int B[4], const int xf[4])
+{
+    int xc[4] = {xf[0] / B[0], xf[1] / B[1], xf[2] / B[2], xf[3] / B[3]};
+    return site_of(Lc, xc);
+}
+
+/* Prolongator: a gather per fine dof. */
+void oracle_prolong(const int Lc[4], const int B[4], int Ns, int Nc, int Nvec, const double *W_, const double *vc_,
+                    double *vf_)
+{
+    const cplx *W = (const cplx *)W_;
+    const cplx *vc = (const cplx *)vc_;
+    cplx *vf = (cplx *)vf_;
+    const int Lf[4] = {Lc[0] * B[0], Lc[1] * B[1], Lc[2] * B[2], Lc[3] * B[3]};
+    const int64_t Vf = volume_of(Lf);
+    const int N = 2 * Nvec;
+#pragma omp parallel for schedule(static)
+    for (int64_t sf = 0; sf < Vf; sf++) {
+        int xf[4];
+        coords_of(Lf, sf, xf);
+        const int64_t xc = aggregate_of(Lc, B, xf);
+        for (int s = 0; s < Ns; s++) {
+            const int chi = s < Ns / 2 ? 0 : 1;
+            for (int a = 0; a < Nc; a++) {
+                cplx acc = 0;
+                for (int k = 0; k < Nvec; k++)
+                    acc += W[((sf * Ns + s) * Nc + a) * Nvec + k] * vc[xc * N + chi * Nvec + k];
+                vf[(sf * Ns + s) * Nc + a] = acc;
+            }
+        }
+    }
+}
+
+/* Restrictor = P^dagger, written as its definition: for every coarse dof, the sum over
+ * the aggregate's fine sites (fine site order), spins of that chirality and colours. */
+void oracle_restrict(const int Lc[4], const int B[4], int Ns, int Nc, int Nvec, const double *W_, const double *vf_,
+                     double *vc_)
+{
+    const cplx *W = (const cplx *)W_;
+    const cplx *vf = (const cplx *)vf_;
+    cplx *vc = (cplx *)vc_;
+    const int Lf[4] = {Lc[0] * B[0], Lc[1] * B[1], Lc[2] * B[2], Lc[3] * B[3]};
+    const int64_t Vf = volume_of(Lf), Vc = volume_of(Lc);
+    const int N = 2 * Nvec;
+    for (int64_t i = 0; i < Vc * N; i++) vc[i] = 0;
+    for (int64_t sf = 0; sf < Vf; sf++) {
+        int xf[4];
+        coords_of(Lf, sf, xf);
+        const int64_t xc = aggregate_of(Lc, B, xf);
+        for (int s = 0; s < Ns; s++) {
+            const int chi = s < Ns / 2 ? 0 : 1;
+            for (int a = 0; a < Nc; a++)
+                for (int k = 0; k < Nvec; k++)
+                    vc[xc * N + chi * Nvec + k] +=
+                        conj(W[((sf * Ns + s) * Nc + a) * Nvec + k]) * vf[(sf * Ns + s) * Nc + a];
+        }
+    }
+}
+
+/* Setup step 3: per aggregate and chirality, the block of basis rows (fine sites of the
+ * aggregate in fine site order, spins of that chirality, colours) x Nvec columns is replaced by
+ * the Q of its QR decomposition, computed by modified Gram-Schmidt in column order (R has a
+ * positive real diagonal).  In place.  Returns -1 if a block is rank deficient: a column whose
+ * norm after projection is <= 1e-10 x its norm before (R21). */
+int oracle_block_orthonormalise(const int Lc[4], const int B[4], int Ns, int Nc, int Nvec, double *W_)
+{
+    cplx *W = (cplx *)W_;
+    const int Lf[4] = {Lc[0] * B[0], Lc[1] * B[1], Lc[2] * B[2], Lc[3] * B[3]};
+    const int64_t Vf = volume_of(Lf), Vc = volume_of(Lc);
+    const int64_t Bvol = (int64_t)B[0] * B[1] * B[2] * B[3];
+    const int64_t M = Bvol * (Ns / 2) * Nc;   /* rows of one (aggregate, chirality) block */
+    int64_t *rows = (int64_t *)malloc(sizeof(int64_t) * Vc * 2 * M);   /* row -> offset of W(.., k=0) */
+    int64_t *fill = (int64_t *)calloc((size_t)Vc * 2, sizeof(int64_t));
+    for (int64_t sf = 0; sf < Vf; sf++) {
+        int xf[4];
+        coords_of(Lf, sf, xf);
+        const int64_t xc = aggregate_of(Lc, B, xf);
+        for (int s = 0; s < Ns; s++) {
+            const int chi = s < Ns / 2 ? 0 : 1;
+            for (int a = 0; a < Nc; a++) {
+                const int64_t blk = xc * 2 + chi;
+                rows[blk * M + fill[blk]++] = ((sf * Ns + s) * Nc + a) * Nvec;
+            }
+        }
+    }
+    int status = 0;
+    for (int64_t blk = 0; blk < Vc * 2 && status == 0; blk++) {
+        const int64_t *r = rows + blk * M;
+        for (int k = 0; k < Nvec; k++) {
+            double nrm0 = 0;
+            for (int64_t m = 0; m < M; m++) nrm0 += creal(W[r[m] + k]) * creal(W[r[m] + k]) +
+                                                   cimag(W[r[m] + k]) * cimag(W[r[m] + k]);
+            for (int j = 0; j < k; j++) {                 /* v_k -= <q_j, v_k> q_j */
+                cplx d = 0;
+                for (int64_t m = 0; m < M; m++) d += conj(W[r[m] + j]) * W[r[m] + k];
+                for (int64_t m = 0; m < M; m++) W[r[m] + k] -= d * W[r[m] + j];
+            }
+            double nrm = 0;
+            for (int64_t m = 0; m < M; m++) nrm += creal(W[r[m] + k]) * creal(W[r[m] + k]) +
+                                                  cimag(W[r[m] + k]) * cimag(W[r[m] + k]);
+            nrm = sqrt(nrm);
+            if (!(nrm > 1e-10 * sqrt(nrm0))) {           /* DESIGN.md R21: numerically dependent */
+                status = -1;
+                break;
+            }
+            for (int64_t m = 0; m < M; m++) W[r[m] + k] /= nrm;
+        }
+    }
+    free(rows);
+    free(fill);
+    return status;
+}
