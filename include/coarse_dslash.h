@@ -254,6 +254,42 @@ int coarse_links_prepare_eo(const cd_links *full, void *stream, cd_links **out);
  * kernels: t_o = X_o^{-1} D_oe in_e, then out_e = X_e in_e - D_eo t_o. */
 int coarse_dslash_apply_eo(const cd_links *eo_links, cd_field *out, const cd_field *in, int dagger, void *stream);
 
+/* ------------------------------------------------------------------ transfer operators
+ * Prolongator P and restrictor R = P^dagger between a fine lattice and this context's coarse
+ * lattice (§3.4; kernels §6.6).  Aggregates are block[0..3]
+ * hypercubes of fine sites; the fine local lattice is local_dims x block, so the operators
+ * are rank-local (no communication) when the coarse lattice is partitioned.  A fine site carries
+ * nspin x ncolor dofs r = s*ncolor + a; chirality 0 = spins s < nspin/2 (R20, P:121
+ * fn. 1), so coarse dof i = chirality*Nvec + k.
+ *   basis (the columns of P): complex [Vf][nspin][ncolor][Nvec], stored fp32 on the device;
+ *   fine fields: DEVICE pointers to complex64 [Vf][nspin][ncolor] (caller-owned);
+ *   coarse fields: ordinary fp32 or fp16 cd_field of the context. */
+typedef struct cd_transfer cd_transfer;
+typedef struct {
+    int32_t block[4];   /* aggregate extent per dim (>= 1)                                  */
+    int32_t nspin;      /* fine spins: 4 (Wilson-clover fine grid) or 2 (a coarse level)     */
+    int32_t ncolor;     /* fine colours per spin: 3 (Wilson) or the finer level's Nvec       */
+} cd_transfer_desc;
+
+/* Upload the basis (host or device, c64 or c128) as given -- call coarse_transfer_orthonormalise
+ * for setup step 3.  CD_ERR_UNSUPPORTED for nspin not in {2, 4}. */
+int coarse_transfer_create(cd_context *ctx, const cd_transfer_desc *desc, const void *basis, int src_on_device,
+                           cd_host_dtype dtype, void *stream, cd_transfer **out);
+int coarse_transfer_free(cd_transfer *t);
+/* Bytes of one fine field (complex64 [Vf][nspin][ncolor]). */
+size_t coarse_transfer_fine_bytes(const cd_transfer *t);
+/* Copy the stored basis (complex64 [Vf][nspin][ncolor][Nvec]) to dst; host-synchronous for host dst. */
+int coarse_transfer_read_basis(const cd_transfer *t, void *dst, int dst_on_device, void *stream);
+/* Setup step 3: per (aggregate, chirality) block, replace the basis rows by the Q of its QR
+ * decomposition (modified Gram-Schmidt, fp64 sums), in place.  Host-synchronous; CD_ERR_INVALID if
+ * a block is rank deficient (R21) or has fewer rows than Nvec. */
+int coarse_transfer_orthonormalise(cd_transfer *t, void *stream);
+/* coarse_out = P^dagger fine_in (restrictor): one CTA or thread-block cluster per
+ * aggregate, deterministic reduction.  fine_in: device complex64 [Vf][nspin][ncolor]. */
+int coarse_restrict(const cd_transfer *t, cd_field *coarse_out, const void *fine_in, void *stream);
+/* fine_out = P coarse_in (prolongator: a gather per fine dof).  fine_out: device complex64. */
+int coarse_prolong(const cd_transfer *t, void *fine_out, const cd_field *coarse_in, void *stream);
+
 /* Halo send buffer of `in` in the canonical wire order (R13): packs on `stream`
  * and copies to dst (host or device).  *bytes receives the size; dst may be NULL to query. */
 int coarse_halo_pack(cd_context *ctx, const cd_field *in, void *dst, int dst_on_device, size_t *bytes,

@@ -42,7 +42,9 @@ EXPORTS = (
     "coarse_dslash_apply_dagger", "coarse_halo_pack", "cd_flush_l2", "cd_halo_plan_create",
     "coarse_dslash_apply_chain", "coarse_field_bytes_mrhs", "coarse_field_alloc_mrhs", "coarse_dslash_apply_mrhs",
     "coarse_links_compress_hermitian", "coarse_field_bytes_parity", "coarse_field_alloc_parity",
-    "coarse_links_prepare_eo", "coarse_dslash_apply_eo",
+    "coarse_links_prepare_eo", "coarse_dslash_apply_eo", "coarse_transfer_create", "coarse_transfer_free",
+    "coarse_transfer_fine_bytes", "coarse_transfer_read_basis", "coarse_transfer_orthonormalise", "coarse_restrict",
+    "coarse_prolong",
 )
 
 
@@ -64,6 +66,11 @@ class HaloPlan(ctypes.Structure):
                 ("record_bytes", ctypes.c_int64), ("scale_bytes", ctypes.c_int64),
                 ("block_offset", (ctypes.c_int64 * 2) * 4), ("block_bytes", ctypes.c_int64 * 4),
                 ("total_bytes", ctypes.c_int64)]
+
+
+class _TransferDesc(ctypes.Structure):
+    """cd_transfer_desc (include/coarse_dslash.h)."""
+    _fields_ = [("block", ctypes.c_int32 * 4), ("nspin", ctypes.c_int32), ("ncolor", ctypes.c_int32)]
 
 
 def _load():
@@ -112,6 +119,13 @@ def _load():
         "coarse_field_alloc_parity": ([P, I, I, P, SZ, PP], I),
         "coarse_links_prepare_eo": ([P, P, PP], I),
         "coarse_dslash_apply_eo": ([P, P, P, I, P], I),
+        "coarse_transfer_create": ([P, ctypes.POINTER(_TransferDesc), P, I, I, P, PP], I),
+        "coarse_transfer_free": ([P], I),
+        "coarse_transfer_fine_bytes": ([P], SZ),
+        "coarse_transfer_read_basis": ([P, P, I, P], I),
+        "coarse_transfer_orthonormalise": ([P, P], I),
+        "coarse_restrict": ([P, P, P, P], I),
+        "coarse_prolong": ([P, P, P, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -296,6 +310,11 @@ class Context:
                                         _stream(stream)))
         return buf[:n.value].tobytes()
 
+    def transfer(self, block, nspin, ncolor, basis, stream=None):
+        """Prolongator / restrictor for aggregates `block` of a fine grid with nspin x ncolor dofs per
+        site; basis: complex [Vf, nspin, ncolor, Nvec] (numpy or torch, host or device)."""
+        return Transfer(self, block, nspin, ncolor, basis, stream)
+
     def flush_l2(self, nbytes=512 << 20, stream=None):
         _check(lib.cd_flush_l2(self.handle, nbytes, _stream(stream)))
 
@@ -426,6 +445,65 @@ class Links:
     def close(self):
         if self.handle:
             _check(lib.coarse_links_free(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Transfer:
+    """P and R = P^dagger between a fine lattice (local dims x block) and this context's lattice."""
+
+    def __init__(self, ctx: Context, block, nspin, ncolor, basis, stream=None):
+        self.ctx = ctx
+        self.block = tuple(int(b) for b in block)
+        self.nspin, self.ncolor = int(nspin), int(ncolor)
+        self.fine_dims = tuple(l * b for l, b in zip(ctx.local_dims, self.block))
+        self.Vf = int(np.prod(self.fine_dims))
+        d = _TransferDesc((ctypes.c_int32 * 4)(*self.block), self.nspin, self.ncolor)
+        if isinstance(basis, np.ndarray):
+            basis = np.ascontiguousarray(basis)
+        p, dev, keep = _ptr(basis)
+        out = ctypes.c_void_p()
+        _check(lib.coarse_transfer_create(ctx.handle, ctypes.byref(d), p, dev, CD_C128 if _is_c128(basis) else CD_C64,
+                                          _stream(stream), ctypes.byref(out)))
+        _sync(stream)
+        del keep
+        self.handle = out
+
+    def fine_field(self):
+        """A device complex64 fine field [Vf, nspin, ncolor] (torch)."""
+        import torch
+        return torch.zeros((self.Vf, self.nspin, self.ncolor), dtype=torch.complex64, device="cuda")
+
+    def orthonormalise(self, stream=None):
+        _check(lib.coarse_transfer_orthonormalise(self.handle, _stream(stream)))
+
+    def read_basis(self, stream=None):
+        out = np.empty((self.Vf, self.nspin, self.ncolor, self.ctx.nvec), np.complex64)
+        _check(lib.coarse_transfer_read_basis(self.handle, out.ctypes.data, 0, _stream(stream)))
+        return out
+
+    def restrict(self, coarse_out: Field, fine_in, stream=None):
+        """coarse_out = P^dagger fine_in (fine_in: device complex64 [Vf, nspin, ncolor])."""
+        p, dev, _ = _ptr(fine_in)
+        if not dev:
+            raise ValueError("fine_in must be device memory")
+        _check(lib.coarse_restrict(self.handle, coarse_out.handle, p, _stream(stream)))
+
+    def prolong(self, fine_out, coarse_in: Field, stream=None):
+        """fine_out = P coarse_in (fine_out: device complex64 [Vf, nspin, ncolor])."""
+        p, dev, _ = _ptr(fine_out)
+        if not dev:
+            raise ValueError("fine_out must be device memory")
+        _check(lib.coarse_prolong(self.handle, p, coarse_in.handle, _stream(stream)))
+
+    def close(self):
+        if self.handle:
+            _check(lib.coarse_transfer_free(self.handle))
             self.handle = None
 
     def __del__(self):

@@ -1275,4 +1275,134 @@ int cd_flush_l2(cd_context *c, size_t bytes, void *stream)
     API_END
 }
 
+// ------------------------------------------------------------------ transfer operators (NEXT-4)
+int coarse_transfer_create(cd_context *c, const cd_transfer_desc *d, const void *basis, int src_on_device,
+                           cd_host_dtype dt, void *stream, cd_transfer **out)
+{
+    API_BEGIN
+    if (!c || !d || !basis || !out) return fail(CD_ERR_INVALID, "ctx/desc/basis/out is NULL");
+    if (dt != CD_C64 && dt != CD_C128) return fail(CD_ERR_INVALID, "bad dtype");
+    if (d->nspin != 2 && d->nspin != 4) return fail(CD_ERR_UNSUPPORTED, "nspin must be 2 or 4");
+    if (d->ncolor < 1 || d->ncolor > 256) return fail(CD_ERR_INVALID, "ncolor must be in [1, 256]");
+    TGeom t{};
+    t.c = c->kg;
+    t.Bvol = 1;
+    int64_t Vf = 1;
+    for (int mu = 0; mu < 4; mu++) {
+        if (d->block[mu] < 1) return fail(CD_ERR_INVALID, "block dims must be >= 1");
+        t.B[mu] = d->block[mu];
+        t.Lf[mu] = c->local[mu] * d->block[mu];
+        t.Bvol *= d->block[mu];
+        Vf *= t.Lf[mu];
+    }
+    t.nf = d->nspin * d->ncolor;
+    if (Vf * t.nf * c->nvec >= ((int64_t)1 << 40) || Vf >= ((int64_t)1 << 31))
+        return fail(CD_ERR_INVALID, "fine lattice too large");
+    t.Vf = (int)Vf;
+    const size_t n = (size_t)Vf * t.nf * c->nvec;
+    cudaStream_t s = S(stream);
+    void *W = nullptr;
+    CUDA_TRY(cudaMalloc(&W, n * 8), "cudaMalloc(basis)");
+    cudaError_t e = cudaSuccess;
+    if (dt == CD_C64) {
+        e = cudaMemcpyAsync(W, basis, n * 8, src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s);
+    } else {
+        const void *src = basis;
+        void *stage = nullptr;
+        if (!src_on_device) {
+            e = cudaMallocAsync(&stage, n * 16, s);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(stage, basis, n * 16, cudaMemcpyHostToDevice, s);
+            src = stage;
+        }
+        if (e == cudaSuccess) e = launch_c128_to_c64(src, W, (int64_t)n, s);
+        if (stage) cudaFreeAsync(stage, s);
+    }
+    if (e != cudaSuccess) {
+        cudaFree(W);
+        return cuda_fail(e, "basis upload");
+    }
+    *out = new cd_transfer{c, {d->block[0], d->block[1], d->block[2], d->block[3]}, d->nspin, d->ncolor, W, n * 8, t};
+    return CD_OK;
+    API_END
+}
+
+int coarse_transfer_free(cd_transfer *t)
+{
+    API_BEGIN
+    if (!t) return fail(CD_ERR_INVALID, "transfer is NULL");
+    cudaFree(t->W);
+    delete t;
+    return CD_OK;
+    API_END
+}
+
+size_t coarse_transfer_fine_bytes(const cd_transfer *t)
+{
+    return t ? (size_t)t->tg.Vf * t->tg.nf * 8 : 0;
+}
+
+int coarse_transfer_read_basis(const cd_transfer *t, void *dst, int dst_on_device, void *stream)
+{
+    API_BEGIN
+    if (!t || !dst) return fail(CD_ERR_INVALID, "transfer/dst is NULL");
+    CUDA_TRY(cudaMemcpyAsync(dst, t->W, t->wbytes, dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                             S(stream)),
+             "cudaMemcpyAsync(basis)");
+    if (!dst_on_device) CUDA_TRY(cudaStreamSynchronize(S(stream)), "cudaStreamSynchronize");
+    return CD_OK;
+    API_END
+}
+
+int coarse_transfer_orthonormalise(cd_transfer *t, void *stream)
+{
+    API_BEGIN
+    if (!t) return fail(CD_ERR_INVALID, "transfer is NULL");
+    if ((int64_t)t->tg.Bvol * (t->tg.nf / 2) < t->ctx->nvec)
+        return fail(CD_ERR_INVALID, "aggregate has fewer rows per chirality than Nvec columns");
+    if (t->tg.Bvol * (int64_t)sizeof(int) > 200 * 1024) return fail(CD_ERR_UNSUPPORTED, "aggregate too large");
+    cudaStream_t s = S(stream);
+    int *flag = nullptr;
+    CUDA_TRY(cudaMallocAsync(&flag, sizeof(int), s), "cudaMallocAsync");
+    CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), s), "cudaMemsetAsync");
+    CUDA_TRY(launch_orthonormalise(t->ctx->nvec, t->W, t->tg, flag, s), "orthonormalise kernel");
+    int h = 0;
+    CUDA_TRY(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
+    CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    cudaFree(flag);
+    if (h) return fail(CD_ERR_INVALID, "rank-deficient aggregate block (DESIGN.md R21)");
+    return CD_OK;
+    API_END
+}
+
+static int check_transfer(const cd_transfer *t, const cd_field *f, const void *fine)
+{
+    if (!t || !f || !fine) return fail(CD_ERR_INVALID, "transfer/field/fine is NULL");
+    if (f->ctx != t->ctx) return fail(CD_ERR_MISMATCH, "field from another context");
+    if (f->nrhs != 1 || f->parity >= 0) return fail(CD_ERR_INVALID, "needs an ordinary full-lattice coarse field");
+    return CD_OK;
+}
+
+int coarse_restrict(const cd_transfer *t, cd_field *coarse_out, const void *fine_in, void *stream)
+{
+    API_BEGIN
+    int r = check_transfer(t, coarse_out, fine_in);
+    if (r != CD_OK) return r;
+    const int cl = restrict_cluster_size(t->tg, t->ctx->num_sms);
+    CUDA_TRY(launch_restrict(coarse_out->prec, t->ctx->nvec, cl, t->W, fine_in, coarse_out->base, t->tg, S(stream)),
+             "restrict kernel");
+    return CD_OK;
+    API_END
+}
+
+int coarse_prolong(const cd_transfer *t, void *fine_out, const cd_field *coarse_in, void *stream)
+{
+    API_BEGIN
+    int r = check_transfer(t, coarse_in, fine_out);
+    if (r != CD_OK) return r;
+    CUDA_TRY(launch_prolong(coarse_in->prec, t->ctx->nvec, t->W, coarse_in->base, fine_out, t->tg, S(stream)),
+             "prolong kernel");
+    return CD_OK;
+    API_END
+}
+
 }  // extern "C"

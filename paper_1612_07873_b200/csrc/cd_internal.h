@@ -60,6 +60,16 @@ struct KGeom {
     int F[4];               // face sites of dim mu
 };
 
+// Transfer-operator geometry: fine lattice = coarse local lattice x block.
+struct TGeom {
+    KGeom c;     // coarse local lattice
+    int B[4];    // aggregate (block) dims
+    int Bvol;    // fine sites per aggregate
+    int Lf[4];   // fine local dims
+    int Vf;      // fine local volume
+    int nf;      // fine dofs per site = Ns * Nc
+};
+
 struct Comm;  // comm.cpp
 
 struct TuneKey {
@@ -130,6 +140,15 @@ struct cd_links {
     void *tbuf;       // eo: odd half-field scratch t_o (fp32)
 };
 
+struct cd_transfer {
+    cd_context *ctx;
+    int block[4];
+    int nspin, ncolor;
+    void *W;          // basis, fp32 complex [Vf][nf][Nvec]
+    size_t wbytes;
+    cd::TGeom tg;
+};
+
 namespace cd {
 
 // ---- launchers implemented in .cu files (return cudaError_t of the launch)
@@ -185,6 +204,13 @@ cudaError_t launch_hermdev(cd_precision p, int nv, const void *full, const KGeom
 cudaError_t launch_mrhs(int nvec, const void *links, const void *in, void *out, const KGeom &g, int nrhs, int dagger,
                         cudaStream_t s);
 cudaError_t launch_flush(void *buf, size_t bytes, cudaStream_t s);
+int restrict_cluster_size(const TGeom &t, int num_sms);
+cudaError_t launch_restrict(cd_precision pc, int nvec, int cl, const void *W, const void *vf, void *vc, const TGeom &t,
+                            cudaStream_t s);
+cudaError_t launch_prolong(cd_precision pc, int nvec, const void *W, const void *vc, void *vf, const TGeom &t,
+                           cudaStream_t s);
+cudaError_t launch_orthonormalise(int nvec, void *W, const TGeom &t, int *fail, cudaStream_t s);
+cudaError_t launch_c128_to_c64(const void *in, void *out, int64_t n, cudaStream_t s);
 
 void count_launch(int n = 1);
 

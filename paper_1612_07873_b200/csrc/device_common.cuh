@@ -171,6 +171,27 @@ __device__ __forceinline__ uint4 neg_chunk(uint4 v)
     return v;
 }
 
+// Thread-block cluster helpers (DSMEM reads + full-cluster barrier).
+__device__ __forceinline__ unsigned cluster_rank()
+{
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint4 ld_dsmem(const void *local_ptr, unsigned cta)
+{
+    uint32_t la = (uint32_t)__cvta_generic_to_shared(local_ptr), ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(cta));
+    uint4 v;
+    asm volatile("ld.shared::cluster.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(ra)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void cluster_sync_all()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // Site decode (Listing 2, x0 fastest) with host-computed magic numbers.
 __device__ __forceinline__ void decode(const KGeom &g, int s, int x[4])
 {

@@ -898,25 +898,6 @@ struct ClusterCfg {
     static_assert(THREADS >= 9 * (Q::VREC / 16), "one 16-B neighbour chunk per thread");
 };
 
-__device__ __forceinline__ unsigned cluster_rank()
-{
-    unsigned r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ uint4 ld_dsmem(const void *local_ptr, unsigned cta)
-{
-    uint32_t la = (uint32_t)__cvta_generic_to_shared(local_ptr), ra;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(cta));
-    uint4 v;
-    asm volatile("ld.shared::cluster.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(ra)
-                 : "memory");
-    return v;
-}
-__device__ __forceinline__ void cluster_sync_all()
-{
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
 
 template <cd_precision P, int NV, int NW>
 __global__ void __launch_bounds__(ClusterCfg<P, NV, NW>::THREADS, 1) dslash_cluster_chain(ApplyArgs a, int n)

@@ -549,3 +549,90 @@ def test_even_odd_singular_detected():
         L.prepare_eo()
     with pytest.raises(ValueError):
         oracle.schur_apply(dims, Lh, synth.vector(dims, N))
+
+
+# ---------------------------------------------------------------- NEXT-4: prolongator / restrictor
+TRANSFER_CASES = [
+    ((2, 2, 2, 2), (2, 2, 2, 2), 4, 3, 24),      # Wilson fine grid, one CTA per aggregate
+    ((1, 1, 2, 2), (4, 4, 2, 4), 4, 3, 24),      # few aggregates -> 4-CTA clusters
+    ((2, 1, 1, 1), (4, 4, 4, 4), 4, 3, 32),      # 8-CTA clusters, Nvec 32
+    ((3, 1, 1, 1), (1, 1, 1, 5), 4, 3, 24),      # ragged: Vf = 15 fine sites
+    ((2, 2, 1, 2), (2, 1, 2, 2), 2, 24, 32),     # a coarse level as the fine grid (Ns 2, Nc 24)
+    ((2, 1, 2, 1), (2, 2, 1, 2), 2, 5, 24),      # generic kernel path, odd rows per chirality
+    ((1, 2, 1, 2), (2, 2, 2, 1), 4, 2, 24),      # generic kernel path, Ns 4
+]
+
+
+def _transfer_inputs(cdims, block, Ns, Nc, nvec):
+    fd = oracle.fine_dims(cdims, block)
+    Vf, nf = vol(fd), Ns * Nc
+    W0 = synth.vector(fd, nf * nvec, tag=5).reshape(Vf, Ns, Nc, nvec)
+    vf = synth.vector(fd, nf, tag=6).reshape(Vf, Ns, Nc)
+    return fd, W0, vf
+
+
+@pytest.mark.parametrize("cdims,block,Ns,Nc,nvec", TRANSFER_CASES)
+def test_transfer_restrict_prolong(cdims, block, Ns, Nc, nvec):
+    """R = P^dagger and P against the oracle on an orthonormalised basis; fp32 coarse fields
+    (rel-L2 <= 1e-5) and fp16 coarse fields (restrict <= 5e-3; prolong of the stored fp16 field)."""
+    import torch
+    fd, W0, vf = _transfer_inputs(cdims, block, Ns, Nc, nvec)
+    W = oracle.block_orthonormalise(cdims, block, Ns, Nc, nvec, W0)
+    ctx = cd.Context(cdims, nvec)
+    T = ctx.transfer(block, Ns, Nc, W)
+    np.testing.assert_array_equal(T.read_basis(), W.astype(np.complex64))
+    fin = torch.from_numpy(vf.astype(np.complex64)).cuda()
+    ref_r = oracle.restrict(cdims, block, Ns, Nc, nvec, W, vf)
+    vc = synth.vector(cdims, 2 * nvec, tag=7)
+    ref_p = oracle.prolong(cdims, block, Ns, Nc, nvec, W, vc)
+    for prec, tol in (("fp32", 1e-5), ("fp16", 5e-3)):
+        c = ctx.field(prec)
+        T.restrict(c, fin)
+        assert rel_l2(c.export(), ref_r) <= tol, prec
+        c.import_(vc)
+        fout = T.fine_field()
+        T.prolong(fout, c)
+        want = oracle.prolong(cdims, block, Ns, Nc, nvec, W, c.export()) if prec == "fp16" else ref_p
+        assert rel_l2(fout.cpu().numpy(), want) <= 1e-5, prec
+    # R P = I on the orthonormal basis (coarse -> fine -> coarse)
+    c, c2 = ctx.field("fp32"), ctx.field("fp32")
+    c.import_(vc)
+    fout = T.fine_field()
+    T.prolong(fout, c)
+    T.restrict(c2, fout)
+    assert rel_l2(c2.export(), vc) <= 1e-5
+
+
+def test_transfer_restrict_bitwise_reproducible():
+    """Fixed-order reductions (no atomics): two restricts give identical bytes, clusters included."""
+    import torch
+    cdims, block, Ns, Nc, nvec = (1, 1, 2, 2), (4, 4, 2, 4), 4, 3, 24
+    fd, W0, vf = _transfer_inputs(cdims, block, Ns, Nc, nvec)
+    ctx = cd.Context(cdims, nvec)
+    T = ctx.transfer(block, Ns, Nc, W0)
+    fin = torch.from_numpy(vf.astype(np.complex64)).cuda()
+    a, b = ctx.field("fp32"), ctx.field("fp32")
+    T.restrict(a, fin)
+    T.restrict(b, fin)
+    assert a.read_stored() == b.read_stored()
+
+
+@pytest.mark.parametrize("cdims,block,Ns,Nc,nvec", TRANSFER_CASES[:3] + TRANSFER_CASES[4:])
+def test_transfer_orthonormalise(cdims, block, Ns, Nc, nvec):
+    """Device block Gram-Schmidt == the oracle's within fp32 storage rounding."""
+    fd, W0, _ = _transfer_inputs(cdims, block, Ns, Nc, nvec)
+    ctx = cd.Context(cdims, nvec)
+    T = ctx.transfer(block, Ns, Nc, W0)
+    T.orthonormalise()
+    ref = oracle.block_orthonormalise(cdims, block, Ns, Nc, nvec, W0)
+    assert rel_l2(T.read_basis(), ref) <= 1e-5
+
+
+def test_transfer_orthonormalise_rank_deficient():
+    cdims, block, Ns, Nc, nvec = (1, 1, 1, 2), (1, 1, 2, 2), 4, 3, 24
+    fd, W0, _ = _transfer_inputs(cdims, block, Ns, Nc, nvec)
+    W0[:, :, :, 5] = W0[:, :, :, 2] * (0.5 + 0.25j)
+    ctx = cd.Context(cdims, nvec)
+    T = ctx.transfer(block, Ns, Nc, W0)
+    with pytest.raises(cd.CDError):
+        T.orthonormalise()

@@ -43,5 +43,23 @@ for prec in ("fp32", "fp16"):
         C, _ = L.compress_hermitian()
         ctx.set_option(cd.CD_OPT_VARIANT, -1)
         C.apply(b, a)
+    if which in ("all", "eo") and prec == "fp32":
+        E = L.prepare_eo()
+        xe, ye = ctx.field("fp32", parity=0), ctx.field("fp32", parity=0)
+        xe.import_(torch.randn(ctx.V // 2, ctx.N, dtype=torch.complex64))
+        E.apply_eo(ye, xe)
+        E.apply_eo(xe, ye, dagger=True)
+    if which in ("all", "transfer"):
+        for cdims, block, ns, nc in (((2, 1, 1, 1), (4, 4, 2, 4), 4, 3), ((2, 2, 2, 2), (1, 1, 1, 1), 2, 24),
+                                     ((1, 1, 1, 2), (2, 2, 1, 2), 2, 5)):
+            tc = cd.Context(cdims, 24)
+            T = tc.transfer(block, ns, nc, torch.randn(tc.V * int(torch.tensor(block).prod()), ns, nc, 24,
+                                                       dtype=torch.complex64, device="cuda"))
+            T.orthonormalise()
+            f = T.fine_field()
+            c = tc.field(prec)
+            c.generate()
+            T.prolong(f, c)
+            T.restrict(c, f)
 torch.cuda.synchronize()
 print("sanitize run ok")
