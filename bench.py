@@ -248,6 +248,47 @@ def extras(cd, perfmodel, torch, other_prec="fp16"):
     out["8^4_fp16_mrhs128"] = {"us_per_apply": round(us, 1), "us_per_rhs": round(us / 128, 3),
                                "TFLOPS": round(perfmodel.flops_per_site(nvec) * V * 128 / us / 1e6, 1),
                                "note": "coarse_dslash_apply_mrhs, tcgen05.mma kind::f16, fp32 accumulators in TMEM"}
+    del L, a, b, ctx
+    # hermiticity-compressed links (5 matrices / site) and the even-odd Schur operator, fp32, 8^4
+    ctx = cd.Context(WORKLOAD["dims"], nvec)
+    L = ctx.links_generate("fp32", kind="hermitian", scale_log2=-4)
+    C, _ = L.compress_hermitian(check=False)
+    a, b = ctx.field("fp32"), ctx.field("fp32")
+    a.generate()
+    C.apply(b, a)
+    torch.cuda.synchronize()
+    us = _events_us(torch, lambda n: [C.apply(b, a) for _ in range(n)], 200)
+    out["8^4_fp32_compressed"] = {"us_per_apply": round(us, 2),
+                                  "GBs_5matrix": round((5 * 48 * 48 + 10 * 48) * 8 * V / us / 1e3, 1),
+                                  "note": "coarse_links_compress_hermitian: X + 4 forward links per site"}
+    del C
+    E = L.prepare_eo()
+    xe, ye = ctx.field("fp32", parity=0), ctx.field("fp32", parity=0)
+    xe.import_(torch.randn(V // 2, 48, dtype=torch.complex64))
+    E.apply_eo(ye, xe)
+    torch.cuda.synchronize()
+    us = _events_us(torch, lambda n: [E.apply_eo(ye, xe) for _ in range(n)], 200)
+    out["8^4_fp32_even_odd_schur"] = {"us_per_apply": round(us, 2),
+                                      "GBs": round((V // 2) * (17 * 48 * 48 + 19 * 48) * 8 / us / 1e3, 1),
+                                      "note": "coarse_dslash_apply_eo: M_ee = X_e - D_eo X_o^-1 D_oe (two kernels)"}
+    del E, L, a, b, xe, ye, ctx
+    # prolongator / restrictor: Wilson 32^4 fine grid -> 8^4 coarse, 4^4 aggregates, Nvec 24
+    ctx = cd.Context(WORKLOAD["dims"], nvec)
+    Vf = V * 256
+    T = ctx.transfer((4, 4, 4, 4), 4, 3, torch.randn(Vf, 4, 3, nvec, dtype=torch.complex64, device="cuda"))
+    f = T.fine_field()
+    c = ctx.field("fp32")
+    c.generate()
+    T.prolong(f, c)
+    T.restrict(c, f)
+    torch.cuda.synchronize()
+    nbytes = Vf * 12 * nvec * 8 + Vf * 12 * 8 + V * 48 * 8
+    us_p = _events_us(torch, lambda n: [T.prolong(f, c) for _ in range(n)], 20)
+    us_r = _events_us(torch, lambda n: [T.restrict(c, f) for _ in range(n)], 20)
+    out["transfer_32^4_to_8^4"] = {"us_prolong": round(us_p, 1), "GBs_prolong": round(nbytes / us_p / 1e3, 1),
+                                   "us_restrict": round(us_r, 1), "GBs_restrict": round(nbytes / us_r / 1e3, 1),
+                                   "note": "coarse_prolong / coarse_restrict, fp32 basis 2.4 GB"}
+    del T, f, c, ctx
     return out
 
 
