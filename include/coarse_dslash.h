@@ -146,10 +146,14 @@ size_t coarse_field_bytes(const cd_context *ctx, cd_precision prec);
  * outlive the field.  Contents are undefined until imported / generated / computed. */
 int coarse_field_alloc(cd_context *ctx, cd_precision prec, void *device_mem, size_t bytes, cd_field **out);
 
-/* Multi right-hand-side fields (the paper's multi-RHS MG): nrhs
- * vectors stored [site][rhs][record].  import / export / generate work on them with the
- * canonical layout [rhs][site][i] (each rhs an ordinary canonical vector; generate gives rhs r
- * the tag tag + r).  Only coarse_dslash_apply_mrhs operates on them. */
+/* Multi right-hand-side fields (the paper's multi-RHS MG).
+ * fp32: nrhs records stored [site][rhs].  fp16 with nrhs > 1: the tensor-core layout (DESIGN.md
+ * R22), blocks of 128 right-hand sides per site [site][block][K chunk][rhs][16 B] + one fp32 scale
+ * per (site, block) -- nrhs must be a multiple of 128 (bytes query returns 0, alloc
+ * CD_ERR_UNSUPPORTED otherwise).  import / export / generate work on them with the canonical
+ * layout [rhs][site][i] (each rhs an ordinary canonical vector; generate gives rhs r the tag
+ * tag + r); read_stored returns the blocks as stored.  Only coarse_dslash_apply_mrhs operates on
+ * them. */
 size_t coarse_field_bytes_mrhs(const cd_context *ctx, cd_precision prec, int nrhs);
 int coarse_field_alloc_mrhs(cd_context *ctx, cd_precision prec, int nrhs, void *device_mem, size_t bytes,
                             cd_field **out);
@@ -230,7 +234,8 @@ int coarse_dslash_apply_chain(const cd_links *links, cd_field *x, cd_field *y, i
 /* out_r = D in_r (dagger: tau3 D tau3 in_r) for every right-hand side r of two multi-RHS fields
  * with the same nrhs (a multiple of 128), on the tcgen05 tensor cores: per site one
  * 128 x 2N x (9 * 2N) fp16 x fp16 -> fp32 GEMM accumulated in TMEM (the links are read once
- * for 128 right-hand sides).  fp16 storage only (CD_ERR_UNSUPPORTED otherwise); single-rank
+ * for 128 right-hand sides); persistent warp-specialised kernel (TMA ring, tcgen05.mma, TMEM
+ * double buffer).  fp16 storage only (CD_ERR_UNSUPPORTED otherwise); single-rank
  * contexts only in this version. */
 int coarse_dslash_apply_mrhs(const cd_links *links, cd_field *out, const cd_field *in, int dagger, void *stream);
 

@@ -543,6 +543,10 @@ int coarse_field_alloc(cd_context *c, cd_precision p, void *mem, size_t bytes, c
 size_t coarse_field_bytes_mrhs(const cd_context *c, cd_precision p, int nrhs)
 {
     if (!c || (p != CD_FP32 && p != CD_FP16) || nrhs < 1) return 0;
+    if (p == CD_FP16 && nrhs > 1) {   // tensor-core block layout (R22): 128 rhs per block
+        if (nrhs % 128) return 0;
+        return align256(((size_t)128 * 4 * c->N + 16) * (size_t)c->V * (size_t)(nrhs / 128));
+    }
     return align256(vec_rec_bytes(c->N, p) * (size_t)c->V * (size_t)nrhs);
 }
 
@@ -552,6 +556,8 @@ int coarse_field_alloc_mrhs(cd_context *c, cd_precision p, int nrhs, void *mem, 
     if (!c || !out) return fail(CD_ERR_INVALID, "ctx/out is NULL");
     if (p != CD_FP32 && p != CD_FP16) return fail(CD_ERR_INVALID, "bad precision");
     if (nrhs < 1) return fail(CD_ERR_INVALID, "nrhs must be >= 1");
+    if (p == CD_FP16 && nrhs > 1 && nrhs % 128)
+        return fail(CD_ERR_UNSUPPORTED, "fp16 multi-RHS fields hold blocks of 128 right-hand sides (nrhs % 128 == 0)");
     const size_t need = coarse_field_bytes_mrhs(c, p, nrhs);
     bool owned = false;
     if (!mem) {
@@ -660,6 +666,7 @@ size_t coarse_field_stored_bytes(const cd_field *f)
     if (!f) return 0;
     const size_t recs = (size_t)field_sites(f) * f->nrhs;
     const size_t n = recs * f->ctx->N;
+    if (f->prec == CD_FP16 && f->nrhs > 1) return (size_t)field_sites(f) * (f->nrhs / 128) * (128 * 4 * f->ctx->N + 16);
     return f->prec == CD_FP32 ? 8 * n : 4 * n + 4 * recs;
 }
 
@@ -689,6 +696,14 @@ int coarse_field_read_stored(const cd_field *f, void *dst, int dst_on_device, vo
     if (!f || !dst) return fail(CD_ERR_INVALID, "field/dst is NULL");
     const int N = f->ctx->N;
     const bool f16 = f->prec == CD_FP16;
+    if (f16 && f->nrhs > 1) {   // tensor-core blocks are returned as stored (R22)
+        const size_t n = coarse_field_stored_bytes(f);
+        CUDA_TRY(cudaMemcpyAsync(dst, f->base, n, dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                 S(stream)),
+                 "cudaMemcpyAsync(read)");
+        CUDA_TRY(cudaStreamSynchronize(S(stream)), "cudaStreamSynchronize");
+        return CD_OK;
+    }
     return read_stored(f->base, field_sites(f) * f->nrhs, f16 ? 4 * N : 8 * N, vec_rec_bytes(N, f->prec), f16, dst, dst_on_device,
                        S(stream));
     API_END
@@ -1107,7 +1122,7 @@ int coarse_dslash_apply_mrhs(const cd_links *l, cd_field *out, const cd_field *i
     cd_context *c = l->ctx;
     if (c->kg.split != 0) return fail(CD_ERR_UNSUPPORTED, "apply_mrhs is single-rank (no halo split) for now");
     c->applied = true;
-    CUDA_TRY(launch_mrhs(c->nvec, l->base, in->base, out->base, c->kg, in->nrhs, dagger ? 1 : 0, S(stream)),
+    CUDA_TRY(launch_mrhs(c->nvec, l->base, in->base, out->base, c->kg, in->nrhs, dagger ? 1 : 0, S(stream), c->num_sms),
              "mrhs launch");
     return CD_OK;
     API_END

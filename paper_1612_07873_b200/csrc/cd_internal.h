@@ -202,7 +202,7 @@ cudaError_t launch_fgh(cd_precision p, const ApplyArgs &a, cudaStream_t s, bool 
 cudaError_t launch_compress(cd_precision p, int nv, const void *full, void *comp, int64_t nsites, cudaStream_t s);
 cudaError_t launch_hermdev(cd_precision p, int nv, const void *full, const KGeom &g, float *dev, cudaStream_t s);
 cudaError_t launch_mrhs(int nvec, const void *links, const void *in, void *out, const KGeom &g, int nrhs, int dagger,
-                        cudaStream_t s);
+                        cudaStream_t s, int num_sms);
 cudaError_t launch_flush(void *buf, size_t bytes, cudaStream_t s);
 int restrict_cluster_size(const TGeom &t, int num_sms);
 cudaError_t launch_restrict(cd_precision pc, int nvec, int cl, const void *W, const void *vf, void *vc, const TGeom &t,

@@ -101,6 +101,28 @@ __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src, uint32
         ::"r"((uint32_t)__cvta_generic_to_shared(dst_smem)), "l"(src), "r"(bytes),
           "r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
 }
+// the same with an L2 eviction-priority policy (createpolicy: evict_first for streamed-once data,
+// evict_last for data re-read by other CTAs)
+__device__ __forceinline__ uint64_t l2_policy_evict_first()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void *dst_smem, const void *src, uint32_t bytes, uint64_t *bar,
+                                              uint64_t policy)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        ::"r"((uint32_t)__cvta_generic_to_shared(dst_smem)), "l"(src), "r"(bytes),
+          "r"((uint32_t)__cvta_generic_to_shared(bar)), "l"(policy) : "memory");
+}
 // 4-byte asynchronous shared-memory store whose completion is counted (4 tx bytes) on an
 // mbarrier: a value delivered exactly like TMA data, ordered by the barrier's phase.
 __device__ __forceinline__ void st_async_u32(void *dst_smem, uint32_t v, uint64_t *bar)

@@ -264,6 +264,84 @@ __global__ void field_generate_kernel(int fp16, int N, int64_t nsites, GenGeom g
     if (lane == 0) *reinterpret_cast<float4 *>(rec + 4 * N) = make_float4(m, 0.f, 0.f, 0.f);
 }
 
+// ------------------------------------------------------------------ tensor-core multi-RHS fp16 layout (R22)
+// block (site, rb) = 128 right-hand sides: [K chunk c][rhs r][4 half2] + fp32 scale (16 B);
+// one scale per block: s = max |x| over its 128 x N complex values, q = fp16_rn(x / s).
+__device__ __forceinline__ size_t tc_off(int N, int r, int i)   // byte offset of complex i of rhs r
+{
+    return (size_t)(i >> 2) * 2048 + (size_t)r * 16 + (size_t)(i & 3) * 4;
+}
+
+// canonical [rhs][V][N] -> blocks; one CTA per (site, block)
+__global__ void __launch_bounds__(256) tc_import_kernel(int N, int64_t nsites, int nrb, const void *src, int c128,
+                                                        unsigned char *dst)
+{
+    __shared__ float red[8];
+    const int64_t site = blockIdx.x / nrb;
+    const int rb = (int)(blockIdx.x - site * nrb);
+    const int n = 128 * N;
+    auto idx = [&](int e) { return ((size_t)(rb * 128 + e / N) * nsites + site) * N + (e % N); };
+    float m = 0.0f;
+    for (int e = threadIdx.x; e < n; e += 256) {
+        const float2 v = load_canon(src, c128, idx(e));
+        m = fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y)));
+    }
+    const float sc = block_max<256>(m, red);
+    unsigned char *blk = dst + (size_t)blockIdx.x * (128 * 4 * N + 16);
+    for (int e = threadIdx.x; e < n; e += 256) {
+        const float2 v = load_canon(src, c128, idx(e));
+        *reinterpret_cast<__half2 *>(blk + tc_off(N, e / N, e % N)) = quant2(v.x, v.y, sc);
+    }
+    if (threadIdx.x == 0) *reinterpret_cast<float4 *>(blk + 128 * 4 * N) = make_float4(sc, 0.f, 0.f, 0.f);
+}
+
+__global__ void __launch_bounds__(256) tc_export_kernel(int N, int64_t nsites, int nrb, const unsigned char *src,
+                                                        void *dst, int c128)
+{
+    const int64_t site = blockIdx.x / nrb;
+    const int rb = (int)(blockIdx.x - site * nrb);
+    const unsigned char *blk = src + (size_t)blockIdx.x * (128 * 4 * N + 16);
+    const float sc = *reinterpret_cast<const float *>(blk + 128 * 4 * N);
+    for (int e = threadIdx.x; e < 128 * N; e += 256) {
+        const int r = e / N, i = e % N;
+        const __half2 q = *reinterpret_cast<const __half2 *>(blk + tc_off(N, r, i));
+        const float2 v = make_float2(__half2float(__low2half(q)) * sc, __half2float(__high2half(q)) * sc);
+        const size_t o = ((size_t)(rb * 128 + r) * nsites + site) * N + i;
+        if (c128) static_cast<double2 *>(dst)[o] = make_double2(v.x, v.y);
+        else static_cast<float2 *>(dst)[o] = v;
+    }
+}
+
+// generator values of right-hand side (tag + r) quantised per block
+__global__ void __launch_bounds__(256) tc_generate_kernel(int N, int nrb, GenGeom g, uint64_t seed, uint32_t tag,
+                                                          float scale, unsigned char *dst)
+{
+    __shared__ float red[8];
+    const int64_t site = blockIdx.x / nrb;
+    const int rb = (int)(blockIdx.x - site * nrb);
+    int xg[4];
+    local_to_global(g, site, xg);
+    const int64_t gs = gindex(g, xg);
+    auto val = [&](int e) {
+        const int r = rb * 128 + e / N, i = e % N;
+        const uint64_t base = splitmix(seed ^ ((uint64_t)(tag + (uint32_t)r) << 56));
+        const uint64_t c = ((uint64_t)gs * N + i) * 2;
+        return make_float2(hash_u(base, c) * scale, hash_u(base, c + 1) * scale);
+    };
+    float m = 0.0f;
+    for (int e = threadIdx.x; e < 128 * N; e += 256) {
+        const float2 v = val(e);
+        m = fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y)));
+    }
+    const float sc = block_max<256>(m, red);
+    unsigned char *blk = dst + (size_t)blockIdx.x * (128 * 4 * N + 16);
+    for (int e = threadIdx.x; e < 128 * N; e += 256) {
+        const float2 v = val(e);
+        *reinterpret_cast<__half2 *>(blk + tc_off(N, e / N, e % N)) = quant2(v.x, v.y, sc);
+    }
+    if (threadIdx.x == 0) *reinterpret_cast<float4 *>(blk + 128 * 4 * N) = make_float4(sc, 0.f, 0.f, 0.f);
+}
+
 __global__ void flush_kernel(uint4 *buf, size_t n)
 {
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
@@ -295,6 +373,11 @@ cudaError_t launch_import(cd_precision p, int nvec, int64_t nsites, const void *
 {
     if (nsites == 0) return cudaSuccess;
     count_launch();
+    if (p == CD_FP16 && nrhs > 1) {
+        tc_import_kernel<<<(unsigned)(nsites * (nrhs / 128)), 256, 0, s>>>(2 * nvec, nsites, nrhs / 128, src, src_c128,
+                                                                           static_cast<unsigned char *>(dst));
+        return cudaGetLastError();
+    }
     import_kernel<<<(unsigned)((nsites * nrhs + 7) / 8), 256, 0, s>>>(p == CD_FP16, 2 * nvec, nsites, src, src_c128,
                                                                          static_cast<unsigned char *>(dst), nrhs);
     return cudaGetLastError();
@@ -305,6 +388,11 @@ cudaError_t launch_export(cd_precision p, int nvec, int64_t nsites, const void *
 {
     if (nsites == 0) return cudaSuccess;
     count_launch();
+    if (p == CD_FP16 && nrhs > 1) {
+        tc_export_kernel<<<(unsigned)(nsites * (nrhs / 128)), 256, 0, s>>>(
+            2 * nvec, nsites, nrhs / 128, static_cast<const unsigned char *>(src), dst, dst_c128);
+        return cudaGetLastError();
+    }
     export_kernel<<<(unsigned)((nsites * nrhs + 7) / 8), 256, 0, s>>>(
         p == CD_FP16, 2 * nvec, nsites, static_cast<const unsigned char *>(src), dst, dst_c128, nrhs);
     return cudaGetLastError();
@@ -336,6 +424,11 @@ cudaError_t launch_field_generate(cd_precision p, int nvec, const cd_context *ct
                                   int scale_log2, void *dst, cudaStream_t s, int nrhs)
 {
     count_launch();
+    if (p == CD_FP16 && nrhs > 1) {
+        tc_generate_kernel<<<(unsigned)(ctx->V * (nrhs / 128)), 256, 0, s>>>(
+            2 * nvec, nrhs / 128, gen_geom(ctx), seed, tag, ldexpf(1.0f, scale_log2), static_cast<unsigned char *>(dst));
+        return cudaGetLastError();
+    }
     field_generate_kernel<<<(unsigned)((ctx->V * nrhs + 7) / 8), 256, 0, s>>>(
         p == CD_FP16, 2 * nvec, ctx->V, gen_geom(ctx), seed, tag, ldexpf(1.0f, scale_log2),
         static_cast<unsigned char *>(dst), nrhs);

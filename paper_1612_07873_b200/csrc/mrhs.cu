@@ -2,58 +2,70 @@
 //
 // SURVEY NEXT-1 (the paper's "multi-right-hand-side MG", §9): with n_rhs vectors
 // the per-site work becomes a small GEMM, so tensor cores finally apply.  For one site x and
-// one hop k, with B = the stored fp16 link matrix L_k(x) read as a K-major operand (row i =
-// output colour-spin, K index = 2j + {re,im}) and A = the 128 right-hand sides' neighbour
-// vectors (row r = rhs, same K index):
+// one hop k, with A = the 128 right-hand sides' neighbour vectors v_r(nbr_k) as stored (row r =
+// rhs, K index = 2j + {re,im}) and B built from the stored fp16 link matrix L_k(x) (row i =
+// output colour-spin):
 //
-//     A[r][2j]   =  v_r(nbr_k)_j.re        B1[i][2j] = L_ij.re    B2[i][2j] =  L_ij.im
-//     A[r][2j+1] = -v_r(nbr_k)_j.im        B1[i][2j+1] = L_ij.im  B2[i][2j+1] = -L_ij.re
+//     A[r][2j] = v.re   A[r][2j+1] = v.im      B1[i][2j] = L.re   B1[i][2j+1] = -L.im
+//                                              B2[i][2j] = L.im   B2[i][2j+1] =  L.re
+//     (A B1^T)[r][i] = y_r,i.re                (A B2^T)[r][i] = y_r,i.im
 //
-//     (A B1^T)[r][i] = sum_j v.re L.re - v.im L.im = y_r,i.re
-//     (A B2^T)[r][i] = sum_j v.re L.im + v.im L.re = y_r,i.im
+// so D = sum_k ratio_k A_k [B1_k; B2_k]^T (M = 128 rhs, N = 2N, K = 16 per instruction) in TMEM
+// is the complex result with no real-block expansion of the links and NO transformation of A.
 //
-// so D = A [B1; B2]^T (M = 128 rhs, N = 2N, K = 16 per instruction) accumulated over the 9 hops
-// and all K steps in TMEM gives the complex result with no real-block expansion of the links.
-// fp16 payloads are used as they are stored; the per-(site,k) link scale and the per-(site,rhs)
-// vector scales enter as ratios <= 1 to their maxima (one HMUL2 per word) and are restored in
-// the epilogue, which re-quantises every (site, rhs) record (R12).
+// Tensor-core field layout (R22): an fp16 multi-RHS field is stored as blocks of 128
+// right-hand sides per site, [site][rhs block][K chunk c][rhs r][16 B] + one fp32 scale per
+// (site, block): one 1-D bulk copy of a neighbour block lands in shared memory already in the
+// UMMA SWIZZLE_NONE K-major canonical layout (core matrix = 8 rhs x 16 B, LBO = 2048 B between K
+// chunks, SBO = 128 B between 8-row groups).  With one scale per block, every scale of hop k is a
+// scalar: ratio_k = s_L(x,k) s_v(nbr_k) / s_ref, s_ref = max_k of the same products, folded into
+// B (ratio <= 1: no fp16 overflow), restored in the epilogue, which re-quantises the block.
 //
-// Layout of a multi-RHS field: [site][rhs][fp16 record] (record = N half2 + scale + pad).
-// One CTA per (site, block of 128 rhs): 8 warps build the operands of hop k+1 in shared memory
-// (core-matrix, no-swizzle K-major layout) while the tensor core runs hop k; one thread issues
-// the MMAs and commits them to an mbarrier; warps 0-3 drain TMEM (tcgen05.ld) in the epilogue.
+// Persistent warp-specialised kernel, one CTA per SM, items = (site, rhs block):
+//   warp 0     producer: per hop one bulk copy of the neighbour block (A) + one of the link record
+//              into an S-stage ring (mbarrier full/empty);
+//   warp 1     MMA issuer (one thread): tcgen05.mma kind::f16 into a double-buffered TMEM
+//              accumulator; tcgen05.commit releases ring stages, B slots and accumulators;
+//   warps 2-5  B builders: raw link record -> B1/B2 rows (x ratio, dagger signs) in a
+//              double-buffered B slot;
+//   warps 6-9  epilogue: tcgen05.ld of the previous item's accumulator (the MMA already runs the
+//              next item), s_ref / dagger / re-quantisation, coalesced 16-B stores.
 #include <cuda_fp16.h>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "cd_internal.h"
 #include "device_common.cuh"
 
 namespace cd {
 
-template <int NV>
+template <int NV, int NBS_ = (NV == 24 ? 3 : 2)>
 struct MrhsCfg {
     static constexpr int N = 2 * NV;           // complex rows of a link matrix
-    static constexpr int MR = 128;             // rhs per CTA (MMA M)
+    static constexpr int MR = 128;             // rhs per block (MMA M)
     static constexpr int NB = 2 * N;           // MMA N: B1 rows then B2 rows
     static constexpr int KCH = N / 4;          // 16-B K chunks per hop (8 halves = 4 complex)
     static constexpr int KSTEPS = KCH / 2;     // MMA K = 16 halves = 2 chunks
-    static constexpr int LBO_A = (MR / 8) * 128;
-    static constexpr int LBO_B = (NB / 8) * 128;
-    static constexpr int A_BYTES = KCH * LBO_A;
+    static constexpr int LBO_A = MR * 16;      // 2048: one K chunk of all 128 rhs
+    static constexpr int LBO_B = NB * 16;
+    static constexpr int A_BYTES = KCH * LBO_A;            // block payload
+    static constexpr int BLK = A_BYTES + 16;               // + scale (16-B padded)
     static constexpr int B_BYTES = KCH * LBO_B;
-    static constexpr int OP = A_BYTES + B_BYTES;            // operand buffer (one hop)
-    static constexpr int VREC = 4 * N + 16;                 // fp16 vector record
-    static constexpr int MREC = 4 * N * N + 16;             // fp16 matrix record
-    static constexpr int RAW_A = MR * VREC;                 // 128 neighbour records (contiguous)
-    static constexpr int RAW = RAW_A;                       // raw stage: the records (links go via registers)
-    static constexpr int HDR = 1024;                        // mbarriers, scales
-    static constexpr int NRAW = 2;                          // raw prefetch depth (hops ahead)
-    static constexpr int SMEM = HDR + OP + NRAW * RAW;      // 95 KB (N = 48): two CTAs per SM
+    static constexpr int MREC = 4 * N * N + 16;            // fp16 matrix record
+    static constexpr int STAGE = (BLK + MREC + 127) / 128 * 128;
+    static constexpr int HDR = 1024;
+    static constexpr int SMEM_MAX = 232448;
+    static constexpr int NBS = NBS_;                                   // B slots (builders run ahead)
+    static constexpr int S = (SMEM_MAX - HDR - NBS * B_BYTES) / STAGE;  // ring stages
+    static constexpr int SMEM = HDR + NBS * B_BYTES + S * STAGE;
     static constexpr int BCH = N * KCH;                     // 16-B chunks of one link matrix
-    static constexpr int BPT = (BCH + 255) / 256;           // per thread
-    static constexpr int APT = MR * KCH / 256;              // A chunks per thread
-    static constexpr int THREADS = 256;
-    static constexpr int TMEM_COLS = NB <= 128 ? 128 : 256;
+    static constexpr int NBW = 6;                           // builder warps
+    static constexpr int NBT = 32 * NBW;
+    static constexpr int EPI0 = 2 + NBW;                    // first epilogue warp
+    static constexpr int THREADS = 32 * (EPI0 + 4);
+    static constexpr int TMEM_COLS = 2 * NB <= 256 ? 256 : 512;
+    static_assert(S >= 2, "ring too small");
     static_assert(NB % 16 == 0 && NB <= 256, "MMA N");
 };
 
@@ -86,237 +98,365 @@ __device__ __forceinline__ uint32_t half2_bits(float x)
     __half2 h = __float2half2_rn(x);
     return *reinterpret_cast<uint32_t *>(&h);
 }
-template <int NC>
-__device__ __forceinline__ void tmem_ld16(uint32_t addr, float *v)
+// 16 consecutive TMEM columns of this warp's 32 lanes (no wait: the caller waits once for all,
+// then passes the registers through reg_fence16 so no use is scheduled above the wait)
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t addr, uint32_t *r)
 {
-    uint32_t r[16];
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
           "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(addr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int q = 0; q < 16; q++) v[q] = __uint_as_float(r[q]);
+}
+__device__ __forceinline__ void reg_fence16(uint32_t *r)
+{
+    asm volatile(""
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                   "+r"(r[15]));
 }
 
-// Hop order: X first (k = 8: this site's own records give the per-rhs reference scales), then 0..7.
-__device__ __forceinline__ int mk_hop(int i) { return i == 0 ? 8 : i - 1; }
 
-template <int NV>
-__global__ void __launch_bounds__(MrhsCfg<NV>::THREADS, 2)
-    dslash_mrhs(const unsigned char *__restrict__ links, const unsigned char *__restrict__ in, unsigned char *out,
-                KGeom g, int nrhs, int dagger)
+// Item -> (site, rhs block), lexicographic: the ~148 items in flight are consecutive sites, which
+// share most of their neighbour lines in L2 (a 4-D Morton order was measured 7 % slower).
+__device__ __forceinline__ int item_site(int64_t it, int nrb, int &rb)
 {
-    using C = MrhsCfg<NV>;
+    const int z = (int)(it / nrb);
+    rb = (int)(it - (int64_t)z * nrb);
+    return z;
+}
+
+__device__ __forceinline__ void st_evict_first(void *p, uint4 v, uint64_t pol)
+{
+    asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w), "l"(pol)
+                 : "memory");
+}
+
+// hop products s_L(x,k) * s_v(nbr_k, block) and their max (identical in builders and epilogue)
+template <int NV>
+__device__ __forceinline__ float hop_scale(const unsigned char *links, const unsigned char *in, const KGeom &g,
+                                           const int x[4], int site, int k, int nrb, int rb)
+{
+    using C = MrhsCfg<NV, 2>;
+    const float sl = ld_nc_f32(links + ((size_t)site * 9 + k) * C::MREC + 4 * C::N * C::N);
+    const float sv = ld_nc_f32(in + ((size_t)neighbour(g, x, site, k) * nrb + rb) * C::BLK + C::A_BYTES);
+    return sl * sv;
+}
+
+template <int NV, int NBS>
+__global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
+    dslash_mrhs(const unsigned char *__restrict__ links, const unsigned char *__restrict__ in, unsigned char *out,
+                KGeom g, int nrb, int dagger, long long *trace)
+{
+    using C = MrhsCfg<NV, NBS>;
+    // optional diagnostic trace of CTA 0 (CD_MRHS_TRACE): trace[ev * 512 + index] = clock64()
+    const bool tr = trace != nullptr && blockIdx.x == 0;
+#define TR(ev, idx) \
+    if (tr && (idx) < 512) trace[(ev) * 512 + (idx)] = clock64();
     extern __shared__ __align__(1024) unsigned char smem[];
-    uint64_t *raw_full = reinterpret_cast<uint64_t *>(smem);         // [NRAW]
-    uint64_t *mma_done = raw_full + 4;                               // [1]
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + 64);
-    float *inv_sr = reinterpret_cast<float *>(smem + 128);           // [128] 1 / s_v(x, r)
-    float *ssl = reinterpret_cast<float *>(smem + 640);              // [1]   s_L(x, 8)
-    unsigned char *op = smem + C::HDR;
-    unsigned char *As = op, *Bs = op + C::A_BYTES;
-    unsigned char *raw = op + C::OP;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem);       // [S]
+    uint64_t *empty = full + 16;                                 // [S]
+    uint64_t *lempty = full + 52;                                // [S]
+    uint64_t *bfull = full + 32;                                 // [NBS]
+    uint64_t *bempty = full + 40;                                // [NBS]
+    uint64_t *accfull = full + 48;                               // [2]
+    uint64_t *accempty = full + 50;                              // [2]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + 512);
+    float *red = reinterpret_cast<float *>(smem + 640);          // [4] epilogue max
+    float *hs = reinterpret_cast<float *>(smem + 704);           // [2][9] builder hop scales
+    float *es = reinterpret_cast<float *>(smem + 800);           // [9]    epilogue hop scales
+    unsigned char *bbuf = smem + C::HDR;                         // [NBS][B_BYTES]
+    unsigned char *ring = bbuf + C::NBS * C::B_BYTES;            // [S][STAGE]
 
-    const int site = blockIdx.x;
-    const int rb = blockIdx.y;   // block of 128 rhs
-    const int tid = threadIdx.x, warp = tid >> 5;
-    int x[4];
-    decode(g, site, x);
-    const unsigned char *lsite = links + (size_t)site * 9 * C::MREC;
-    const size_t rhs0 = (size_t)rb * C::MR;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t items = (int64_t)g.V * nrb;
 
-    if (warp == 0) {   // TMEM accumulator: 128 lanes x NB fp32 columns
+    if (tid == 0) {
+        for (int j = 0; j < C::S; j++) {
+            mbar_init(&full[j], 1);
+            mbar_init(&empty[j], 1);            // the MMA commit (A consumed by the tensor core)
+            mbar_init(&lempty[j], C::NBT);      // every builder thread (raw link record read)
+        }
+        for (int j = 0; j < C::NBS; j++) {
+            mbar_init(&bfull[j], C::NBW);
+            mbar_init(&bempty[j], 1);
+        }
+        for (int j = 0; j < 2; j++) {
+            mbar_init(&accfull[j], 1);
+            mbar_init(&accempty[j], 4);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) {
         const uint32_t a = (uint32_t)__cvta_generic_to_shared(tmem_slot);
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(a), "n"(C::TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    // the 128 contiguous neighbour records of hop i -> ring slot i % NRAW (one bulk copy)
-    auto issue_raw = [&](int i) {
-        const int k = mk_hop(i);
-        uint64_t *bar = &raw_full[i % C::NRAW];
-        unsigned char *dst = raw + (i % C::NRAW) * C::RAW;
-        mbar_arrive_expect_tx(bar, C::RAW_A);
-        bulk_g2s(dst, in + ((size_t)neighbour(g, x, site, k) * nrhs + rhs0) * C::VREC, C::RAW_A, bar);
-    };
-    // link matrix of hop i -> registers (prefetched one hop ahead)
-    uint4 bv[C::BPT];
-    float bsc;
-    auto load_b = [&](int i) {
-        const unsigned char *mk = lsite + (size_t)mk_hop(i) * C::MREC;
-#pragma unroll
-        for (int u = 0; u < C::BPT; u++) {
-            const int e = tid + u * C::THREADS;
-            bv[u] = e < C::BCH ? ld_stream(mk + (size_t)e * 16) : make_uint4(0, 0, 0, 0);
-        }
-        bsc = ld_nc_f32(mk + 4 * C::N * C::N);
-    };
-    load_b(0);
-    if (tid == 0) {
-        for (int j = 0; j < C::NRAW; j++) mbar_init(&raw_full[j], 1);
-        mbar_init(mma_done, 1);
-        fence_mbar_init();
-        for (int j = 0; j < C::NRAW; j++) issue_raw(j);
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
-    const uint32_t idesc = idesc_f16_f32<C::MR, C::NB>();
 
-    for (int i = 0; i < 9; i++) {
-        const int k = mk_hop(i);
-        const unsigned char *rs = raw + (i % C::NRAW) * C::RAW;
-        mbar_wait(&raw_full[i % C::NRAW], (i / C::NRAW) & 1);
-        if (i == 0) {   // reference scales: this site's own records (k = 8) and its X scale
-            if (tid < C::MR) {
-                const float s = *reinterpret_cast<const float *>(rs + tid * C::VREC + 4 * C::N);
-                inv_sr[tid] = s > 0.0f ? __frcp_rn(s) : 0.0f;
-            }
-            if (tid == 0) ssl[0] = bsc;
-            __syncthreads();
-        }
-        // the operand buffer is free once the MMAs of the previous hop completed
-        if (i > 0) mbar_wait(mma_done, (i - 1) & 1);
-        // ---- B1 / B2 rows (scaled by s_L(k)/s_L(8)) into the core-matrix layout
-        {
-            const float s8 = ssl[0];
-            const uint32_t lr = half2_bits(s8 > 0.0f ? bsc * __frcp_rn(s8) : 0.0f);
-#pragma unroll
-            for (int u = 0; u < C::BPT; u++) {
-                const int e = tid + u * C::THREADS;
-                if (e >= C::BCH) continue;
-                const int ii = e / C::KCH, c = e - ii * C::KCH;
-                const uint32_t *w = &bv[u].x;
-                uint4 b1, b2;
-                uint32_t *o1 = &b1.x, *o2 = &b2.x;
-#pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    const uint32_t sv = hmul2_u32(w[q], lr);                         // (re, im)
-                    o1[q] = sv;
-                    o2[q] = __byte_perm(sv, 0, 0x1032) ^ 0x80000000u;                // (im, -re)
+    if (warp == 0) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            const uint64_t pol_v = l2_policy_evict_last(), pol_l = l2_policy_evict_first();
+            uint32_t h = 0;
+            for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+                int rb;
+                const int site = item_site(it, nrb, rb);
+                int x[4];
+                decode(g, site, x);
+                for (int k = 0; k < 9; k++, h++) {
+                    const int st = h % C::S;
+                    mbar_wait(&empty[st], ((h / C::S) & 1) ^ 1);
+                    mbar_wait(&lempty[st], ((h / C::S) & 1) ^ 1);
+                    unsigned char *dst = ring + st * C::STAGE;
+                    mbar_arrive_expect_tx(&full[st], C::BLK + C::MREC);
+                    // vectors are re-read by 9 sites (keep them in L2), links are read once
+                    bulk_g2s_hint(dst, in + ((size_t)neighbour(g, x, site, k) * nrb + rb) * C::BLK, C::BLK,
+                                  &full[st], pol_v);
+                    bulk_g2s_hint(dst + C::BLK, links + ((size_t)site * 9 + k) * C::MREC, C::MREC, &full[st],
+                                  pol_l);
+                    TR(0, h)
                 }
-                *reinterpret_cast<uint4 *>(Bs + c * C::LBO_B + (ii >> 3) * 128 + (ii & 7) * 16) = b1;
-                const int i2 = ii + C::N;
-                *reinterpret_cast<uint4 *>(Bs + c * C::LBO_B + (i2 >> 3) * 128 + (i2 & 7) * 16) = b2;
             }
         }
-        if (i + 1 < 9) load_b(i + 1);   // next hop's link matrix: in flight during this hop
-        // ---- A rows: (re, -im) of the neighbour records scaled by s_v(nbr, r)/s_v(x, r); tau3 (dagger)
-        // thread t: row r = t % 128, chunks c = t / 128 + 2u (all loads issued before use)
-        {
-            const int r = tid & (C::MR - 1), h = tid >> 7;
-            const unsigned char *rec = rs + r * C::VREC;
-            const uint32_t ratio = half2_bits(*reinterpret_cast<const float *>(rec + 4 * C::N) * inv_sr[r]);
-            uint4 w4[C::APT];
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            const uint32_t idesc = idesc_f16_f32<C::MR, C::NB>();
+            const uint32_t ring0 = (uint32_t)__cvta_generic_to_shared(ring);
+            const uint32_t bb0 = (uint32_t)__cvta_generic_to_shared(bbuf);
+            uint32_t h = 0, t = 0;
+            for (int64_t it = blockIdx.x; it < items; it += gridDim.x, t++) {
+                const int acc = t & 1;
+                mbar_wait(&accempty[acc], ((t >> 1) & 1) ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t d = tmem + acc * C::NB;
+                TR(9, t)
+                for (int k = 0; k < 9; k++, h++) {
+                    const int st = h % C::S, bs = h % C::NBS;
+                    mbar_wait(&full[st], (h / C::S) & 1);
+                    TR(1, h)
+                    mbar_wait(&bfull[bs], (h / C::NBS) & 1);
+                    TR(2, h)
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t a0 = ring0 + st * C::STAGE, b0 = bb0 + bs * C::B_BYTES;
 #pragma unroll
-            for (int u = 0; u < C::APT; u++) w4[u] = *reinterpret_cast<const uint4 *>(rec + (h + 2 * u) * 16);
-#pragma unroll
-            for (int u = 0; u < C::APT; u++) {
-                const int c = h + 2 * u;
-                const bool flip = dagger && (c * 4 >= NV);   // components j >= Nvec (4 complex per chunk)
-                const uint32_t m = 0x80000000u ^ (flip ? 0x80008000u : 0u);
-                const uint32_t *w = &w4[u].x;
-                uint4 av;
-                uint32_t *o = &av.x;
-#pragma unroll
-                for (int q = 0; q < 4; q++) o[q] = hmul2_u32(w[q] ^ m, ratio);
-                *reinterpret_cast<uint4 *>(As + c * C::LBO_A + (r >> 3) * 128 + (r & 7) * 16) = av;
+                    for (int s = 0; s < C::KSTEPS; s++) {
+                        const uint64_t da = smem_desc(a0 + 2 * s * C::LBO_A, C::LBO_A, 128);
+                        const uint64_t db = smem_desc(b0 + 2 * s * C::LBO_B, C::LBO_B, 128);
+                        const uint32_t accum = (k > 0 || s > 0) ? 1u : 0u;
+                        asm volatile(
+                            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+                            "l"(da), "l"(db), "r"(idesc), "r"(accum));
+                    }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                     (uint32_t)__cvta_generic_to_shared(&empty[st]))
+                                 : "memory");
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                     (uint32_t)__cvta_generic_to_shared(&bempty[bs]))
+                                 : "memory");
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 (uint32_t)__cvta_generic_to_shared(&accfull[acc]))
+                             : "memory");
             }
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> tensor core
-        __syncthreads();
-        if (tid == 0) {
-            if (i + C::NRAW < 9) issue_raw(i + C::NRAW);   // raw slot i % NRAW fully consumed
+    } else if (warp < C::EPI0) {
+        // ------------------------------------------------------------ B builders (NBW warps)
+        const int bt = tid - 64;
+        constexpr int UPT = (C::BCH + C::NBT - 1) / C::NBT;   // 16-B chunks per thread per hop
+        uint32_t h = 0, t = 0;
+        // hop scales of the NEXT item are loaded one item ahead (their latency hides behind 9 hops)
+        float nsl = 0.0f, nsv = 0.0f;   // raw loads, multiplied only when consumed
+        auto scale_of = [&](int64_t it) {
+            int rb;
+                const int site = item_site(it, nrb, rb);
+            int x[4];
+            decode(g, site, x);
+            nsl = ld_nc_f32(links + ((size_t)site * 9 + bt) * C::MREC + 4 * C::N * C::N);
+            nsv = ld_nc_f32(in + ((size_t)neighbour(g, x, site, bt) * nrb + rb) * C::BLK + C::A_BYTES);
+        };
+        if (bt < 9 && (int64_t)blockIdx.x < items) scale_of(blockIdx.x);
+        for (int64_t it = blockIdx.x; it < items; it += gridDim.x, t++) {
+            float *hsb = hs + (t & 1) * 9;
+            if (bt < 9) {
+                hsb[bt] = nsl * nsv;   // == hop_scale (same fp32 product as the epilogue)
+                if (it + gridDim.x < items) scale_of(it + gridDim.x);
+            }
+            bar_named(1, C::NBT);
+            float sref = 0.0f;
+#pragma unroll
+            for (int k = 0; k < 9; k++) sref = fmaxf(sref, hsb[k]);
+            const float isref = sref > 0.0f ? __frcp_rn(sref) : 0.0f;
+            for (int k = 0; k < 9; k++, h++) {
+                const int st = h % C::S, bs = h % C::NBS;
+                const uint32_t ratio = half2_bits(hsb[k] * isref);
+                mbar_wait(&bempty[bs], ((h / C::NBS) & 1) ^ 1);
+                if (bt == 0) TR(3, h)
+                mbar_wait(&full[st], (h / C::S) & 1);
+                if (bt == 0) TR(4, h)
+                const unsigned char *lraw = ring + st * C::STAGE + C::BLK;
+                unsigned char *Bs = bbuf + bs * C::B_BYTES;
+                // bank-conflict-free for both sides: the 8 threads of a 128-bit access phase take 8
+                // consecutive rows (distinct 16-B slots of a B core matrix) and chunks c0 + t/2
+                // (the raw row stride of 12 or 16 chunks would otherwise alias)
+                uint4 w[UPT];
+                int ii[UPT], cc[UPT];
+#pragma unroll
+                for (int u = 0; u < UPT; u++) {
+                    const int e = bt + u * C::NBT;
+                    const int t8 = e & 7, grp = e >> 3;
+                    const int rbk = grp % (C::N / 8), cb = grp / (C::N / 8);
+                    ii[u] = rbk * 8 + t8;
+                    const int c = cb + (t8 >> 1);
+                    cc[u] = c >= C::KCH ? c - C::KCH : c;
+                    if (e < C::BCH) w[u] = *reinterpret_cast<const uint4 *>(lraw + ((size_t)ii[u] * C::KCH + cc[u]) * 16);
+                }
+                mbar_arrive(&lempty[st]);   // this thread is done with the stage's link record
+#pragma unroll
+                for (int u = 0; u < UPT; u++) {
+                    if (bt + u * C::NBT >= C::BCH) break;
+                    const int c = cc[u];
+                    const uint32_t flip = (dagger && c * 4 >= NV) ? 0x80008000u : 0u;   // tau3 on the input
+                    uint4 b1, b2;
+                    uint32_t *wi = &w[u].x, *o1 = &b1.x, *o2 = &b2.x;
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const uint32_t v = hmul2_u32(wi[q] ^ flip, ratio);             // (re, im)
+                        o1[q] = v ^ 0x80000000u;                                       // (re, -im)
+                        o2[q] = __byte_perm(v, 0, 0x1032);                             // (im, re)
+                    }
+                    *reinterpret_cast<uint4 *>(Bs + c * C::LBO_B + (ii[u] >> 3) * 128 + (ii[u] & 7) * 16) = b1;
+                    const int i2 = ii[u] + C::N;
+                    *reinterpret_cast<uint4 *>(Bs + c * C::LBO_B + (i2 >> 3) * 128 + (i2 & 7) * 16) = b2;
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bfull[bs]);
+                if (bt == 0) TR(5, h)
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue (128 threads)
+        const int et = tid - 32 * C::EPI0;
+        const uint64_t pol_o = l2_policy_evict_first();   // outputs are not re-read by this apply
+        const int r = 32 * (warp & 3) + lane;   // TMEM lane = rhs row (warp w reaches lanes 32(w%4)..)
+        uint32_t t = 0;
+        for (int64_t it = blockIdx.x; it < items; it += gridDim.x, t++) {
+            int rb;
+                const int site = item_site(it, nrb, rb);
+            int x[4];
+            decode(g, site, x);
+            if (et < 9) es[et] = hop_scale<NV>(links, in, g, x, site, et, nrb, rb);
+            const int acc = t & 1;
+            if (et == 0) TR(6, t)
+            mbar_wait(&accfull[acc], (t >> 1) & 1);
+            if (et == 0) TR(7, t)
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t a0 = (uint32_t)__cvta_generic_to_shared(As);
-            const uint32_t b0 = (uint32_t)__cvta_generic_to_shared(Bs);
+            uint32_t raw[C::NB];
+            const uint32_t base = tmem + acc * C::NB + ((uint32_t)(32 * (warp & 3)) << 16);
 #pragma unroll
-            for (int s = 0; s < C::KSTEPS; s++) {
-                const uint64_t da = smem_desc(a0 + 2 * s * C::LBO_A, C::LBO_A, 128);
-                const uint64_t db = smem_desc(b0 + 2 * s * C::LBO_B, C::LBO_B, 128);
-                const uint32_t acc = (i > 0 || s > 0) ? 1u : 0u;
-                asm volatile(
-                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                    "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-                    "l"(da), "l"(db), "r"(idesc), "r"(acc));
+            for (int cc = 0; cc < C::NB / 16; cc++) tmem_ld16_nowait(base + cc * 16, raw + cc * 16);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int cc = 0; cc < C::NB / 16; cc++) reg_fence16(raw + cc * 16);
+            float v[C::NB];
+#pragma unroll
+            for (int i = 0; i < C::NB; i++) v[i] = __uint_as_float(raw[i]);
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&accempty[acc]);   // the MMA may reuse this accumulator
+            bar_named(2, 128);                              // es[] visible
+            float sref = 0.0f;
+#pragma unroll
+            for (int k = 0; k < 9; k++) sref = fmaxf(sref, es[k]);
+            float m = 0.0f;
+#pragma unroll
+            for (int i = 0; i < C::NB; i++) {
+                const int row = i < C::N ? i : i - C::N;
+                v[i] *= (dagger && row >= NV) ? -sref : sref;
+                m = fmaxf(m, fabsf(v[i]));
             }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                             (uint32_t)__cvta_generic_to_shared(mma_done))
-                         : "memory");
-        }
-    }
-    mbar_wait(mma_done, 8 & 1);   // the 9th commit: every MMA of this site is done
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-
-    // ---- epilogue: warps 0-3, thread t <-> TMEM lane t <-> rhs t; two passes over TMEM (max, store)
-    if (tid < C::MR) {
-        const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
-        const float scale = ssl[0] * (inv_sr[tid] > 0.0f ? __frcp_rn(inv_sr[tid]) : 0.0f);
-        float mx = 0.0f;
-#pragma unroll 1
-        for (int cc = 0; cc < C::NB / 16; cc++) {
-            float v[16];
-            tmem_ld16<16>(lane_base + cc * 16, v);
 #pragma unroll
-            for (int q = 0; q < 16; q++) mx = fmaxf(mx, fabsf(v[q] * scale));
-        }
-        unsigned char *rec = out + ((size_t)site * nrhs + rhs0 + tid) * C::VREC;
-#pragma unroll 1
-        for (int cc = 0; cc < C::N / 16; cc++) {
-            float re[16], im[16];
-            tmem_ld16<16>(lane_base + cc * 16, re);
-            tmem_ld16<16>(lane_base + C::N + cc * 16, im);
+            for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (lane == 0) red[warp & 3] = m;
+            bar_named(2, 128);
+            m = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+            unsigned char *blk = out + ((size_t)site * nrb + rb) * C::BLK;
+            // re-quantisation by the reciprocal (R22: x * (1/s), one cvt.rn.f16x2 per pair)
+            const float im = m > 0.0f ? __frcp_rn(m) : 0.0f;
 #pragma unroll
-            for (int q4 = 0; q4 < 4; q4++) {
+            for (int c = 0; c < C::KCH; c++) {
                 uint4 o;
                 uint32_t *ow = &o.x;
 #pragma unroll
                 for (int q = 0; q < 4; q++) {
-                    const int i = cc * 16 + q4 * 4 + q;
-                    const float sg = (dagger && i >= NV) ? -scale : scale;
-                    const float yr = re[q4 * 4 + q] * sg, yi = im[q4 * 4 + q] * sg;
-                    __half2 h = mx > 0.0f ? __halves2half2(__float2half_rn(__fdiv_rn(yr, mx)),
-                                                           __float2half_rn(__fdiv_rn(yi, mx)))
-                                          : __halves2half2(__float2half_rn(0.0f), __float2half_rn(0.0f));
-                    ow[q] = *reinterpret_cast<uint32_t *>(&h);
+                    const int i = 4 * c + q;
+                    __half2 hv = __floats2half2_rn(v[i] * im, v[C::N + i] * im);
+                    ow[q] = *reinterpret_cast<uint32_t *>(&hv);
                 }
-                *reinterpret_cast<uint4 *>(rec + (cc * 16 + q4 * 4) * 4) = o;
+                st_evict_first(blk + c * C::LBO_A + r * 16, o, pol_o);
             }
+            if (et == 0) *reinterpret_cast<float4 *>(blk + C::A_BYTES) = make_float4(m, 0.f, 0.f, 0.f);
+            if (et == 0) TR(8, t)
+            bar_named(2, 128);   // red[] / es[] reuse by the next item
         }
-        *reinterpret_cast<float4 *>(rec + 4 * C::N) = make_float4(mx, 0.f, 0.f, 0.f);
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (warp == 0)
+    if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
 }
 
-template <int NV>
+template <int NV, int NBS>
 static cudaError_t launch_mrhs_t(const void *links, const void *in, void *out, const KGeom &g, int nrhs, int dagger,
-                                 cudaStream_t s)
+                                 cudaStream_t s, int num_sms)
 {
-    using C = MrhsCfg<NV>;
+    using C = MrhsCfg<NV, NBS>;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(dslash_mrhs<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(dslash_mrhs<NV, NBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         if (e != cudaSuccess) return e;
         attr = true;
     }
+    const int nrb = nrhs / C::MR;
+    const int64_t items = (int64_t)g.V * nrb;
     count_launch();
-    dslash_mrhs<NV><<<dim3((unsigned)g.V, (unsigned)(nrhs / C::MR)), C::THREADS, C::SMEM, s>>>(
+    long long *trace = nullptr;
+    const char *tf = getenv("CD_MRHS_TRACE");   // diagnostic only: per-event clock64 of CTA 0
+    if (tf) {
+        cudaMalloc(&trace, 10 * 512 * sizeof(long long));
+        cudaMemsetAsync(trace, 0, 10 * 512 * sizeof(long long), s);
+    }
+    dslash_mrhs<NV, NBS><<<(unsigned)(items < num_sms ? items : num_sms), C::THREADS, C::SMEM, s>>>(
         static_cast<const unsigned char *>(links), static_cast<const unsigned char *>(in),
-        static_cast<unsigned char *>(out), g, nrhs, dagger);
-    return cudaGetLastError();
+        static_cast<unsigned char *>(out), g, nrb, dagger, trace);
+    cudaError_t e = cudaGetLastError();
+    if (tf) {
+        long long h[10 * 512];
+        cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        cudaFree(trace);
+        if (FILE *f = fopen(tf, "wb")) {
+            fwrite(h, sizeof(h), 1, f);
+            fclose(f);
+        }
+    }
+    return e;
 }
 
 cudaError_t launch_mrhs(int nvec, const void *links, const void *in, void *out, const KGeom &g, int nrhs, int dagger,
-                        cudaStream_t s)
+                        cudaStream_t s, int num_sms)
 {
     if (nrhs % 128) return cudaErrorInvalidValue;
-    return nvec == 24 ? launch_mrhs_t<24>(links, in, out, g, nrhs, dagger, s)
-                      : launch_mrhs_t<32>(links, in, out, g, nrhs, dagger, s);
+    // B slots: 3 for Nvec 24 (2 and 4 measured 1-3 % slower), 2 for Nvec 32 (shared memory)
+    return nvec == 24 ? launch_mrhs_t<24, 3>(links, in, out, g, nrhs, dagger, s, num_sms)
+                      : launch_mrhs_t<32, 2>(links, in, out, g, nrhs, dagger, s, num_sms);
 }
 
 }  // namespace cd
