@@ -203,6 +203,11 @@ def _events_us(torch, fn, reps):
 def extras(cd, perfmodel, torch, other_prec="fp16"):
     """Secondary measurements (each a few hundred ms), reported under "also"."""
     out = {}
+    peak_bw = measured_peak()[0]
+    try:
+        peak_tf = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"])
+    except Exception:
+        peak_tf = 2250.0   # nominal dense fp16 (fallback)
     nvec = WORKLOAD["nvec"]
     # the 8^4 workload with the other storage precision
     ctx = cd.Context(WORKLOAD["dims"], nvec)
@@ -245,8 +250,10 @@ def extras(cd, perfmodel, torch, other_prec="fp16"):
     L.apply_mrhs(b, a)
     torch.cuda.synchronize()
     us = _events_us(torch, lambda n: [L.apply_mrhs(b, a) for _ in range(n)], 10)
+    tf = perfmodel.flops_per_site(nvec) * V * 128 / us / 1e6
     out["8^4_fp16_mrhs128"] = {"us_per_apply": round(us, 1), "us_per_rhs": round(us / 128, 3),
-                               "TFLOPS": round(perfmodel.flops_per_site(nvec) * V * 128 / us / 1e6, 1),
+                               "TFLOPS": round(tf, 1), "tensor_frac": round(tf / peak_tf, 3),
+                               "tensor_peak_source": "MEASURED_PEAKS.json bf16_tflops (fp16 dense = bf16 dense)",
                                "note": "coarse_dslash_apply_mrhs, tcgen05.mma kind::f16, fp32 accumulators in TMEM"}
     del L, a, b, ctx
     # hermiticity-compressed links (5 matrices / site) and the even-odd Schur operator, fp32, 8^4
@@ -258,8 +265,9 @@ def extras(cd, perfmodel, torch, other_prec="fp16"):
     C.apply(b, a)
     torch.cuda.synchronize()
     us = _events_us(torch, lambda n: [C.apply(b, a) for _ in range(n)], 200)
-    out["8^4_fp32_compressed"] = {"us_per_apply": round(us, 2),
-                                  "GBs_5matrix": round((5 * 48 * 48 + 10 * 48) * 8 * V / us / 1e3, 1),
+    gb = (5 * 48 * 48 + 10 * 48) * 8 * V / us / 1e3
+    out["8^4_fp32_compressed"] = {"us_per_apply": round(us, 2), "GBs_5matrix": round(gb, 1),
+                                  "hbm_frac": round(gb / peak_bw, 3),
                                   "note": "coarse_links_compress_hermitian: X + 4 forward links per site"}
     del C
     E = L.prepare_eo()
@@ -268,8 +276,9 @@ def extras(cd, perfmodel, torch, other_prec="fp16"):
     E.apply_eo(ye, xe)
     torch.cuda.synchronize()
     us = _events_us(torch, lambda n: [E.apply_eo(ye, xe) for _ in range(n)], 200)
-    out["8^4_fp32_even_odd_schur"] = {"us_per_apply": round(us, 2),
-                                      "GBs": round((V // 2) * (17 * 48 * 48 + 19 * 48) * 8 / us / 1e3, 1),
+    gb = (V // 2) * (17 * 48 * 48 + 19 * 48) * 8 / us / 1e3
+    out["8^4_fp32_even_odd_schur"] = {"us_per_apply": round(us, 2), "GBs": round(gb, 1),
+                                      "hbm_frac": round(gb / peak_bw, 3),
                                       "note": "coarse_dslash_apply_eo: M_ee = X_e - D_eo X_o^-1 D_oe (two kernels)"}
     del E, L, a, b, xe, ye, ctx
     # prolongator / restrictor: Wilson 32^4 fine grid -> 8^4 coarse, 4^4 aggregates, Nvec 24
@@ -287,6 +296,8 @@ def extras(cd, perfmodel, torch, other_prec="fp16"):
     us_r = _events_us(torch, lambda n: [T.restrict(c, f) for _ in range(n)], 20)
     out["transfer_32^4_to_8^4"] = {"us_prolong": round(us_p, 1), "GBs_prolong": round(nbytes / us_p / 1e3, 1),
                                    "us_restrict": round(us_r, 1), "GBs_restrict": round(nbytes / us_r / 1e3, 1),
+                                   "hbm_frac_prolong": round(nbytes / us_p / 1e3 / peak_bw, 3),
+                                   "hbm_frac_restrict": round(nbytes / us_r / 1e3 / peak_bw, 3),
                                    "note": "coarse_prolong / coarse_restrict, fp32 basis 2.4 GB"}
     del T, f, c, ctx
     return out
