@@ -171,6 +171,25 @@ static int cuda_fail(cudaError_t e, const char *what)
 static cudaStream_t S(void *s) { return static_cast<cudaStream_t>(s); }
 static int64_t field_sites(const cd_field *f) { return f->parity < 0 ? f->ctx->V : f->ctx->V / 2; }
 
+// Device allocation owned until release(): early error returns free it (cudaFree synchronises
+// the device, which is fine on these setup-time error paths).
+struct DevBuf {
+    void *p = nullptr;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    ~DevBuf()
+    {
+        if (p) cudaFree(p);
+    }
+    void *release()
+    {
+        void *q = p;
+        p = nullptr;
+        return q;
+    }
+};
+
 // ------------------------------------------------------------------ decomposition + halo plan
 // Geometry checks shared by cd_context_create and cd_halo_plan_create.
 static int check_geometry(const cd_geometry *geom, int nranks, int rank)
@@ -731,14 +750,14 @@ int coarse_links_compress_hermitian(const cd_links *full, double *max_dev, void 
     cudaStream_t s = S(stream);
     if (max_dev) {
         if (full->prec != CD_FP32) return fail(CD_ERR_UNSUPPORTED, "the hermiticity check needs fp32 links");
-        float *d = nullptr;
-        CUDA_TRY(cudaMallocAsync(&d, sizeof(float), s), "cudaMallocAsync");
-        CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(float), s), "cudaMemsetAsync");
-        CUDA_TRY(launch_hermdev(full->prec, c->nvec, full->base, c->kg, d, s), "hermiticity check");
+        DevBuf d;
+        CUDA_TRY(cudaMalloc(&d.p, sizeof(float)), "cudaMalloc");
+        float *dv = static_cast<float *>(d.p);
+        CUDA_TRY(cudaMemsetAsync(dv, 0, sizeof(float), s), "cudaMemsetAsync");
+        CUDA_TRY(launch_hermdev(full->prec, c->nvec, full->base, c->kg, dv, s), "hermiticity check");
         float h = 0.0f;
-        CUDA_TRY(cudaMemcpyAsync(&h, d, sizeof(float), cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
+        CUDA_TRY(cudaMemcpyAsync(&h, dv, sizeof(float), cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
         CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
-        cudaFree(d);
         *max_dev = h;
     }
     cd_links *l = nullptr;
@@ -1068,25 +1087,20 @@ int coarse_links_prepare_eo(const cd_links *full, void *stream, cd_links **out)
     cudaStream_t s = S(stream);
     const size_t mrec = mat_rec_bytes(c->N, CD_FP32);
     const size_t half = (size_t)(c->V / 2);
-    void *even = nullptr, *odd = nullptr, *t = nullptr;
-    int *sing = nullptr;
-    CUDA_TRY(cudaMalloc(&even, align256(half * 9 * mrec)), "cudaMalloc(eo even)");
-    CUDA_TRY(cudaMalloc(&odd, align256(half * 8 * mrec)), "cudaMalloc(eo odd)");
-    CUDA_TRY(cudaMalloc(&t, align256(half * vec_rec_bytes(c->N, CD_FP32))), "cudaMalloc(eo t)");
-    CUDA_TRY(cudaMallocAsync(&sing, sizeof(int), s), "cudaMallocAsync");
-    CUDA_TRY(cudaMemsetAsync(sing, 0, sizeof(int), s), "cudaMemsetAsync");
-    CUDA_TRY(launch_eo_prepare(c->nvec, full->base, even, odd, c->kg, sing, s), "eo prepare");
+    DevBuf even, odd, t, sing;
+    CUDA_TRY(cudaMalloc(&even.p, align256(half * 9 * mrec)), "cudaMalloc(eo even)");
+    CUDA_TRY(cudaMalloc(&odd.p, align256(half * 8 * mrec)), "cudaMalloc(eo odd)");
+    CUDA_TRY(cudaMalloc(&t.p, align256(half * vec_rec_bytes(c->N, CD_FP32))), "cudaMalloc(eo t)");
+    CUDA_TRY(cudaMalloc(&sing.p, sizeof(int)), "cudaMalloc");
+    int *sg = static_cast<int *>(sing.p);
+    CUDA_TRY(cudaMemsetAsync(sg, 0, sizeof(int), s), "cudaMemsetAsync");
+    CUDA_TRY(launch_eo_prepare(c->nvec, full->base, even.p, odd.p, c->kg, sg, s), "eo prepare");
     int hs = 0;
-    CUDA_TRY(cudaMemcpyAsync(&hs, sing, sizeof(int), cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
+    CUDA_TRY(cudaMemcpyAsync(&hs, sg, sizeof(int), cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
     CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
-    cudaFree(sing);
-    if (hs) {
-        cudaFree(even);
-        cudaFree(odd);
-        cudaFree(t);
-        return fail(CD_ERR_INVALID, "a diagonal block X on an odd site is singular");
-    }
-    *out = new cd_links{c, CD_FP32, even, align256(half * 9 * mrec), 0, 1, odd, t};
+    if (hs) return fail(CD_ERR_INVALID, "a diagonal block X on an odd site is singular");
+    void *ev = even.release(), *od = odd.release(), *tb = t.release();
+    *out = new cd_links{c, CD_FP32, ev, align256(half * 9 * mrec), 0, 1, od, tb};
     return CD_OK;
     API_END
 }
@@ -1376,14 +1390,14 @@ int coarse_transfer_orthonormalise(cd_transfer *t, void *stream)
         return fail(CD_ERR_INVALID, "aggregate has fewer rows per chirality than Nvec columns");
     if (t->tg.Bvol * (int64_t)sizeof(int) > 200 * 1024) return fail(CD_ERR_UNSUPPORTED, "aggregate too large");
     cudaStream_t s = S(stream);
-    int *flag = nullptr;
-    CUDA_TRY(cudaMallocAsync(&flag, sizeof(int), s), "cudaMallocAsync");
+    DevBuf fb;
+    CUDA_TRY(cudaMalloc(&fb.p, sizeof(int)), "cudaMalloc");
+    int *flag = static_cast<int *>(fb.p);
     CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), s), "cudaMemsetAsync");
     CUDA_TRY(launch_orthonormalise(t->ctx->nvec, t->W, t->tg, flag, s), "orthonormalise kernel");
     int h = 0;
     CUDA_TRY(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
     CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
-    cudaFree(flag);
     if (h) return fail(CD_ERR_INVALID, "rank-deficient aggregate block (DESIGN.md R21)");
     return CD_OK;
     API_END
