@@ -242,7 +242,9 @@ int coarse_dslash_apply_mrhs(const cd_links *links, cd_field *out, const cd_fiel
 /* ------------------------------------------------------------------ even-odd
  * Red-black preconditioning (§3.3; used on all MG levels): the Schur
  * complement on the even sites,  M_ee v_e = X_e v_e - D_eo X_o^{-1} D_oe v_e,  site parity
- * (x0+x1+x2+x3) mod 2.  Needs every local L_mu even and a single rank; fp32 storage.
+ * (x0+x1+x2+x3) mod 2.  Needs every LOCAL L_mu even; fp32 storage.  Multi-rank contexts: each
+ * stage packs its input's face sites, exchanges them (NCCL, same wire format as the full
+ * operator) overlapped with the interior kernel, then adds the remote hops (collective).
  * Parity fields hold the V/2 sites of one parity in half-index order h = s >> 1 (canonical
  * import/export layout [V/2][N]). */
 size_t coarse_field_bytes_parity(const cd_context *ctx, cd_precision prec);

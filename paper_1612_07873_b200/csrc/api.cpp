@@ -1039,11 +1039,25 @@ int coarse_dslash_apply_dagger(const cd_links *l, cd_field *out, const cd_field 
 }
 
 // ------------------------------------------------------------------ even-odd (NEXT-3)
+// Even local extents: local parity == global parity (the rank origins are even) and every x0
+// pair holds one site of each parity.
 static bool eo_geometry_ok(const cd_context *c)
 {
     for (int mu = 0; mu < 4; mu++)
         if (c->local[mu] % 2) return false;
-    return c->kg.split == 0;
+    return true;
+}
+
+struct EoExchange {
+    cd_context *c;
+    int status = CD_OK;
+    std::string err;
+};
+static cudaError_t eo_exchange(void *p)
+{
+    EoExchange *x = static_cast<EoExchange *>(p);
+    x->status = halo_exchange(x->c, ctx_plan(x->c, CD_FP32), x->c->comm_stream, x->err);
+    return x->status == CD_OK ? cudaSuccess : cudaErrorUnknown;
 }
 
 size_t coarse_field_bytes_parity(const cd_context *c, cd_precision p)
@@ -1058,7 +1072,7 @@ int coarse_field_alloc_parity(cd_context *c, cd_precision p, int parity, void *m
     if (!c || !out) return fail(CD_ERR_INVALID, "ctx/out is NULL");
     if (p != CD_FP32 && p != CD_FP16) return fail(CD_ERR_INVALID, "bad precision");
     if (parity != 0 && parity != 1) return fail(CD_ERR_INVALID, "parity must be 0 (even) or 1 (odd)");
-    if (!eo_geometry_ok(c)) return fail(CD_ERR_UNSUPPORTED, "even-odd needs every local L_mu even, single rank");
+    if (!eo_geometry_ok(c)) return fail(CD_ERR_UNSUPPORTED, "even-odd needs every local L_mu even");
     const size_t need = coarse_field_bytes_parity(c, p);
     bool owned = false;
     if (!mem) {
@@ -1083,7 +1097,7 @@ int coarse_links_prepare_eo(const cd_links *full, void *stream, cd_links **out)
     if (full->compressed || full->eo) return fail(CD_ERR_INVALID, "needs full (uncompressed) links");
     if (full->prec != CD_FP32) return fail(CD_ERR_UNSUPPORTED, "even-odd: fp32 storage only");
     cd_context *c = full->ctx;
-    if (!eo_geometry_ok(c)) return fail(CD_ERR_UNSUPPORTED, "even-odd needs every local L_mu even, single rank");
+    if (!eo_geometry_ok(c)) return fail(CD_ERR_UNSUPPORTED, "even-odd needs every local L_mu even");
     cudaStream_t s = S(stream);
     const size_t mrec = mat_rec_bytes(c->N, CD_FP32);
     const size_t half = (size_t)(c->V / 2);
@@ -1116,9 +1130,38 @@ int coarse_dslash_apply_eo(const cd_links *l, cd_field *out, const cd_field *in,
     if (out->base == in->base) return fail(CD_ERR_INVALID, "out must not alias in");
     cd_context *c = l->ctx;
     c->applied = true;
-    CUDA_TRY(launch_eo_apply(c->nvec, l->base, l->aux, in->base, l->tbuf, out->base, c->kg, dagger ? 1 : 0, S(stream),
-                             c->pdl != 0),
-             "eo apply");
+    if (c->comm) {
+        std::string err;
+        const int r = comm_check(c->comm, err);
+        if (r != CD_OK) return fail(r, err);
+    }
+    EoApply e{};
+    e.even = l->base;
+    e.odd = l->aux;
+    e.in_e = in->base;
+    e.t_o = l->tbuf;
+    e.out_e = out->base;
+    e.dagger = dagger ? 1 : 0;
+    e.s = S(stream);
+    e.pdl = c->pdl != 0;
+    e.halo = c->kg.split != 0 ? 1 : 0;
+    e.g = e.halo ? halo_geom(c, CD_FP32) : c->kg;
+    EoExchange ex{c};
+    if (e.halo) {
+        e.comm_stream = c->comm_stream;
+        e.ev_in = c->ev_in;
+        e.ev_halo = c->ev_halo;
+        e.send = c->send_buf;
+        e.recv = c->recv_buf;
+        e.scratch = c->face_scratch;
+        e.face_sites = c->face_sites;
+        e.n_face = c->n_face;
+        e.exchange = eo_exchange;
+        e.exchange_arg = &ex;
+    }
+    const cudaError_t ce = launch_eo_apply(c->nvec, e);
+    if (ex.status != CD_OK) return fail(ex.status, ex.err);
+    CUDA_TRY(ce, "eo apply");
     return CD_OK;
     API_END
 }

@@ -196,8 +196,27 @@ cudaError_t launch_field_generate(cd_precision p, int nvec, const cd_context *ct
                                   int scale_log2, void *dst, cudaStream_t s, int nrhs = 1);
 cudaError_t launch_eo_prepare(int nvec, const void *full, void *even, void *odd, const KGeom &g, int *singular,
                               cudaStream_t s);
-cudaError_t launch_eo_apply(int nvec, const void *even, const void *odd, const void *in_e, void *t_o, void *out_e,
-                            const KGeom &g, int dagger, cudaStream_t s, bool pdl);
+struct EoApply {              // one even-odd Schur apply (coarse_dslash_apply_eo)
+    const void *even, *odd;   // prepared links: even [V/2][9], odd [V/2][8]
+    const void *in_e;
+    void *t_o, *out_e;
+    KGeom g;                  // halo geometry when split != 0
+    int dagger;
+    cudaStream_t s;
+    bool pdl;
+    // multi-rank (split != 0)
+    int halo;
+    cudaStream_t comm_stream;
+    cudaEvent_t ev_in, ev_halo;
+    void *send;
+    const void *recv;
+    float2 *scratch;
+    const int *face_sites;
+    int n_face;
+    cudaError_t (*exchange)(void *);   // posts the halo exchange on comm_stream
+    void *exchange_arg;
+};
+cudaError_t launch_eo_apply(int nvec, const EoApply &e);
 cudaError_t launch_fgh(cd_precision p, const ApplyArgs &a, cudaStream_t s, bool pdl);
 cudaError_t launch_compress(cd_precision p, int nv, const void *full, void *comp, int64_t nsites, cudaStream_t s);
 cudaError_t launch_hermdev(cd_precision p, int nv, const void *full, const KGeom &g, float *dev, cudaStream_t s);

@@ -30,6 +30,14 @@ __device__ __forceinline__ int parity_site(const KGeom &g, int h, int p)
     return 2 * h + (((x[1] + x[2] + x[3]) & 1) != p ? 1 : 0);
 }
 
+__device__ __forceinline__ bool eo_is_face(const KGeom &g, const int x[4])
+{
+#pragma unroll
+    for (int mu = 0; mu < 4; mu++)
+        if (((g.split >> mu) & 1) && (x[mu] == 0 || x[mu] == g.L[mu] - 1)) return true;
+    return false;
+}
+
 // ------------------------------------------------------------------ setup: X_o^{-1} L_k(o)
 template <int NV>
 __global__ void __launch_bounds__(256) eo_prepare_odd(const unsigned char *full, unsigned char *odd_out, KGeom g,
@@ -133,7 +141,8 @@ __global__ void eo_copy_even(const unsigned char *full, unsigned char *even_out,
 // 4 row groups per warp.  fp32.
 template <int NV, int MODE>
 __global__ void __launch_bounds__(288) dslash_parity(const unsigned char *__restrict__ links, const unsigned char *in_self,
-                                                     const unsigned char *in_hop, unsigned char *out, KGeom g, int dagger)
+                                                     const unsigned char *in_hop, unsigned char *out, KGeom g, int dagger,
+                                                     int halo, float2 *scratch)
 {
     using Q = Cfg<CD_FP32, NV>;
     constexpr int ROWS = 16, NRB = Q::N / ROWS, RG = ROWS / Q::R;
@@ -148,7 +157,8 @@ __global__ void __launch_bounds__(288) dslash_parity(const unsigned char *__rest
     const int s = parity_site(g, h, P);
     int x[4];
     decode(g, s, x);
-    const bool active = (MODE == 1) || (k != 8);
+    // multi-rank: remote hops are added by eo_halo once the exchange has landed
+    const bool active = ((MODE == 1) || (k != 8)) && !(halo && remote_hop(g, x, k));
     uint4 Lc[RG][Q::C];
     if (active) {
         const int rec = (k == 8) ? 8 : k;
@@ -164,6 +174,7 @@ __global__ void __launch_bounds__(288) dslash_parity(const unsigned char *__rest
     for (int t = threadIdx.x; t < 9 * Q::VCH; t += 288) {   // the 9 input records (half indices)
         const int kk = t / Q::VCH, e = t - kk * Q::VCH;
         if (kk == 8 && MODE == 0) continue;
+        if (halo && remote_hop(g, x, kk)) continue;
         const unsigned char *src = kk == 8 ? in_self + (size_t)h * Q::VREC
                                            : in_hop + (size_t)(neighbour(g, x, s, kk) >> 1) * Q::VREC;
         *reinterpret_cast<uint4 *>(vs + kk * Q::VREC + e * 16) = ld_nc(src + e * 16);
@@ -190,6 +201,9 @@ __global__ void __launch_bounds__(288) dslash_parity(const unsigned char *__rest
             }
             if (d == 0) part[warp][gg * Q::R + r] = make_float2(hs * re, hs * im);
         }
+    } else if (d == 0) {
+#pragma unroll
+        for (int gg = 0; gg < RG; gg++) part[warp][gg * Q::R + r] = make_float2(0.0f, 0.0f);
     }
     __syncthreads();
     if (threadIdx.x < ROWS) {
@@ -200,8 +214,94 @@ __global__ void __launch_bounds__(288) dslash_parity(const unsigned char *__rest
             yi += part[w][threadIdx.x].y;
         }
         const int row = rb * ROWS + threadIdx.x;
+        if (halo && eo_is_face(g, x)) {   // partial (no output sign yet) for eo_halo
+            scratch[(size_t)s * Q::N + row] = make_float2(yr, yi);
+        } else {
+            const float sg = (MODE == 1 && dagger && row >= NV) ? -1.0f : 1.0f;
+            reinterpret_cast<float2 *>(out + (size_t)h * Q::VREC)[row] = make_float2(sg * yr, sg * yi);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ multi-rank halo pieces
+// The half fields travel in the full-field wire format (R13): face records of the
+// other parity are simply not written (never read), so the plan, buffers and NCCL exchange of
+// the full operator are reused unchanged.
+template <int NV>
+__global__ void eo_pack(const unsigned char *half, unsigned char *send, KGeom g, int4 pairs, int parity)
+{
+    using Q = Cfg<CD_FP32, NV>;
+    constexpr int PREC = 8 * Q::N, CPR = PREC / 16;
+    const int mu = (&pairs.x)[blockIdx.y >> 1], blk = blockIdx.y & 1;
+    const int F = g.F[mu];
+    int o3[3], n = 0;
+    for (int nu = 0; nu < 4; nu++)
+        if (nu != mu) o3[n++] = nu;
+    unsigned char *dst = send + g.blk_off[mu][blk];
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < F * CPR; e += gridDim.x * blockDim.x) {
+        const int f = e / CPR, ch = e - f * CPR;
+        int x[4];
+        int t = f;
+        x[o3[0]] = t % g.L[o3[0]];
+        t /= g.L[o3[0]];
+        x[o3[1]] = t % g.L[o3[1]];
+        x[o3[2]] = t / g.L[o3[1]];
+        x[mu] = blk == 0 ? g.L[mu] - 1 : 0;
+        if (((x[0] + x[1] + x[2] + x[3]) & 1) != parity) continue;
+        const unsigned char *rec = half + (size_t)(encode(g, x) >> 1) * Q::VREC;
+        *reinterpret_cast<uint4 *>(dst + (size_t)f * PREC + ch * 16) = *reinterpret_cast<const uint4 *>(rec + ch * 16);
+    }
+}
+
+// one CTA per face site of the output parity: partial + the remote hops, then the final store
+template <int NV, int MODE>
+__global__ void __launch_bounds__(32 * (2 * NV / 4)) eo_halo(const unsigned char *__restrict__ links,
+                                                              const unsigned char *__restrict__ recv,
+                                                              const int *face_sites, const float2 *scratch,
+                                                              unsigned char *out, KGeom g, int dagger)
+{
+    using Q = Cfg<CD_FP32, NV>;
+    constexpr int NM = MODE == 0 ? 8 : 9;
+    constexpr int P = MODE == 0 ? 1 : 0;
+    constexpr int PREC = 8 * Q::N;
+    const int s = face_sites[blockIdx.x];
+    int x[4];
+    decode(g, s, x);
+    if (((x[0] + x[1] + x[2] + x[3]) & 1) != P) return;
+    const int h = s >> 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r = lane / Q::D, d = lane % Q::D;
+    const int row = warp * Q::R + r;
+    float re = 0.0f, im = 0.0f;
+    for (int k = 0; k < 8; k++) {
+        if (!remote_hop(g, x, k)) continue;
+        const int mu = k >> 1;
+        const int blk = (k & 1) ? 0 : 1;   // +mu hop: block B of the +mu neighbour; -mu hop: block A
+        int o3[3], n = 0;
+        for (int nu = 0; nu < 4; nu++)
+            if (nu != mu) o3[n++] = nu;
+        const int f = (x[o3[2]] * g.L[o3[1]] + x[o3[1]]) * g.L[o3[0]] + x[o3[0]];
+        const unsigned char *vrec = recv + g.blk_off[mu][blk] + (size_t)f * PREC;
+        const unsigned char *m = links + ((size_t)h * NM + k) * Q::MREC;
+#pragma unroll
+        for (int c = 0; c < Q::C; c++) {
+            const int q = d + Q::D * c;
+            uint4 vq = ld_nc(vrec + q * 16);
+            if (MODE == 0 && dagger && q * Q::CPC >= NV) vq = neg_chunk<false>(vq);
+            cmac2(ld_nc(m + row * Q::ROWB + q * 16), vq, re, im);
+        }
+    }
+#pragma unroll
+    for (int o = Q::D / 2; o >= 1; o >>= 1) {
+        re += shfl_xor(re, o);
+        im += shfl_xor(im, o);
+    }
+    if (d == 0) {
+        const float2 p = scratch[(size_t)s * Q::N + row];
+        const float hs = MODE == 1 ? -1.0f : 1.0f;
         const float sg = (MODE == 1 && dagger && row >= NV) ? -1.0f : 1.0f;
-        reinterpret_cast<float2 *>(out + (size_t)h * Q::VREC)[row] = make_float2(sg * yr, sg * yi);
+        reinterpret_cast<float2 *>(out + (size_t)h * Q::VREC)[row] =
+            make_float2(sg * (p.x + hs * re), sg * (p.y + hs * im));
     }
 }
 
@@ -232,47 +332,75 @@ cudaError_t launch_eo_prepare(int nvec, const void *full, void *even, void *odd,
 }
 
 template <int NV>
-static cudaError_t eo_apply_t(const void *even, const void *odd, const void *in_e, void *t_o, void *out_e,
-                              const KGeom &g, int dagger, cudaStream_t s, bool pdl)
+static cudaError_t eo_mode_launch(int mode, const unsigned char *links, const unsigned char *self, const unsigned char *hop,
+                                  unsigned char *out, const KGeom &g, int dagger, int halo, float2 *scratch,
+                                  cudaStream_t s, bool pdl)
 {
     constexpr int NRB = 2 * NV / 16;
-    const unsigned grid = (unsigned)(g.V / 2 * NRB);
-    const unsigned char *ev = static_cast<const unsigned char *>(even), *od = static_cast<const unsigned char *>(odd);
-    const unsigned char *vi = static_cast<const unsigned char *>(in_e);
-    unsigned char *t = static_cast<unsigned char *>(t_o), *y = static_cast<unsigned char *>(out_e);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(g.V / 2 * NRB));
+    cfg.blockDim = dim3(288);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
     KGeom gg = g;
-    int dg = dagger;
+    int dg = dagger, hl = halo;
+    void *args[] = {&links, &self, &hop, &out, &gg, &dg, &hl, &scratch};
+    count_launch();
+    return cudaLaunchKernelExC(&cfg, mode == 0 ? (const void *)dslash_parity<NV, 0> : (const void *)dslash_parity<NV, 1>,
+                               args);
+}
+
+template <int NV>
+static cudaError_t eo_apply_t(const EoApply &e)
+{
+    const unsigned char *ev = static_cast<const unsigned char *>(e.even), *od = static_cast<const unsigned char *>(e.odd);
+    const unsigned char *vi = static_cast<const unsigned char *>(e.in_e);
+    unsigned char *t = static_cast<unsigned char *>(e.t_o), *y = static_cast<unsigned char *>(e.out_e);
+    if (!e.halo) {
+        cudaError_t r = eo_mode_launch<NV>(0, od, nullptr, vi, t, e.g, e.dagger, 0, nullptr, e.s, e.pdl);
+        if (r != cudaSuccess) return r;
+        return eo_mode_launch<NV>(1, ev, vi, t, y, e.g, e.dagger, 0, nullptr, e.s, e.pdl);
+    }
+    // multi-rank: per mode, pack + exchange (comm stream) overlap the interior kernel; the halo
+    // kernel adds the remote hops of the face sites once the exchange landed.
+    int4 pairs = make_int4(0, 0, 0, 0);
+    int np = 0;
+    for (int mu = 0; mu < 4; mu++)
+        if ((e.g.split >> mu) & 1) (&pairs.x)[np++] = mu;
     for (int mode = 0; mode < 2; mode++) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(grid);
-        cfg.blockDim = dim3(288);
-        cfg.stream = s;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
+        const unsigned char *src = mode == 0 ? vi : t;   // the half field the hops read
+        cudaError_t r = cudaEventRecord(e.ev_in, e.s);
+        if (r == cudaSuccess) r = cudaStreamWaitEvent(e.comm_stream, e.ev_in, 0);
+        if (r != cudaSuccess) return r;
         count_launch();
-        cudaError_t e;
-        if (mode == 0) {
-            const unsigned char *self = nullptr;
-            void *args[] = {&od, &self, &vi, &t, &gg, &dg};
-            e = cudaLaunchKernelExC(&cfg, (const void *)dslash_parity<NV, 0>, args);
-        } else {
-            const unsigned char *tc = t;
-            void *args[] = {&ev, &vi, &tc, &y, &gg, &dg};
-            e = cudaLaunchKernelExC(&cfg, (const void *)dslash_parity<NV, 1>, args);
-        }
-        if (e != cudaSuccess) return e;
+        eo_pack<NV><<<dim3(16, 2 * np), 256, 0, e.comm_stream>>>(src, static_cast<unsigned char *>(e.send), e.g, pairs,
+                                                                 mode == 0 ? 0 : 1);
+        if ((r = cudaGetLastError()) != cudaSuccess) return r;
+        if ((r = e.exchange(e.exchange_arg)) != cudaSuccess) return r;
+        if ((r = cudaEventRecord(e.ev_halo, e.comm_stream)) != cudaSuccess) return r;
+        r = mode == 0 ? eo_mode_launch<NV>(0, od, nullptr, vi, t, e.g, e.dagger, 1, e.scratch, e.s, false)
+                      : eo_mode_launch<NV>(1, ev, vi, t, y, e.g, e.dagger, 1, e.scratch, e.s, false);
+        if (r != cudaSuccess) return r;
+        if ((r = cudaStreamWaitEvent(e.s, e.ev_halo, 0)) != cudaSuccess) return r;
+        count_launch();
+        if (mode == 0)
+            eo_halo<NV, 0><<<e.n_face, 32 * (2 * NV / 4), 0, e.s>>>(od, static_cast<const unsigned char *>(e.recv),
+                                                                     e.face_sites, e.scratch, t, e.g, e.dagger);
+        else
+            eo_halo<NV, 1><<<e.n_face, 32 * (2 * NV / 4), 0, e.s>>>(ev, static_cast<const unsigned char *>(e.recv),
+                                                                     e.face_sites, e.scratch, y, e.g, e.dagger);
+        if ((r = cudaGetLastError()) != cudaSuccess) return r;
     }
     return cudaSuccess;
 }
 
-cudaError_t launch_eo_apply(int nvec, const void *even, const void *odd, const void *in_e, void *t_o, void *out_e,
-                            const KGeom &g, int dagger, cudaStream_t s, bool pdl)
+cudaError_t launch_eo_apply(int nvec, const EoApply &e)
 {
-    return nvec == 24 ? eo_apply_t<24>(even, odd, in_e, t_o, out_e, g, dagger, s, pdl)
-                      : eo_apply_t<32>(even, odd, in_e, t_o, out_e, g, dagger, s, pdl);
+    return nvec == 24 ? eo_apply_t<24>(e) : eo_apply_t<32>(e);
 }
 
 }  // namespace cd

@@ -17,11 +17,14 @@ ap.add_argument("--dims", type=int, nargs=4, default=[8, 8, 8, 8])
 ap.add_argument("--nvec", type=int, default=24)
 ap.add_argument("--reps", type=int, default=200)
 ap.add_argument("--json", default=None)
+ap.add_argument("--mask", type=int, default=0, help="CD_OPT_HALO_SELF_MASK: route these dims through the halo path")
 a = ap.parse_args()
 dims = tuple(a.dims)
 V = dims[0] * dims[1] * dims[2] * dims[3]
 N = 2 * a.nvec
 ctx = cd.Context(dims, a.nvec)
+if a.mask:
+    ctx.set_option(cd.CD_OPT_HALO_SELF_MASK, a.mask)
 L = ctx.links_generate("fp32", kind="general", scale_log2=-4)
 torch.cuda.synchronize()
 t0 = torch.cuda.Event(enable_timing=True)
@@ -58,7 +61,7 @@ t_eo = timed(E.apply_eo, xe, ye)
 mb_full = perfmodel.metric_bytes_per_site(a.nvec, "fp32") * V
 # odd kernel: 8 matrices + 8 hop reads + 1 write per odd site; even: 9 + 9 + 1 write + 0 (self is a hop read)
 mb_eo = (V // 2) * ((8 + 9) * N * N + (8 + 1 + 9 + 1) * N) * 8
-row = {"dims": dims, "nvec": a.nvec, "prepare_ms": round(prep_ms, 2), "us_full": round(t_full, 2),
+row = {"dims": dims, "nvec": a.nvec, "halo_mask": a.mask, "prepare_ms": round(prep_ms, 2), "us_full": round(t_full, 2),
        "us_schur": round(t_eo, 2), "schur_over_full": round(t_eo / t_full, 3),
        "full_GBs": round(mb_full / t_full / 1e3, 1), "schur_GBs": round(mb_eo / t_eo / 1e3, 1)}
 print(json.dumps(row), flush=True)

@@ -49,6 +49,13 @@ for prec in ("fp32", "fp16"):
         xe.import_(torch.randn(ctx.V // 2, ctx.N, dtype=torch.complex64))
         E.apply_eo(ye, xe)
         E.apply_eo(xe, ye, dagger=True)
+        hc = cd.Context((2, 2, 2, 4), 24)
+        hc.set_option(cd.CD_OPT_HALO_SELF_MASK, 0b1001)
+        He = hc.links_generate("fp32", kind="hermitian", scale_log2=-4).prepare_eo()
+        he_x, he_y = hc.field("fp32", parity=0), hc.field("fp32", parity=0)
+        he_x.import_(torch.randn(hc.V // 2, hc.N, dtype=torch.complex64))
+        He.apply_eo(he_y, he_x)
+        He.apply_eo(he_x, he_y, dagger=True)
     if which in ("all", "transfer"):
         for cdims, block, ns, nc in (((2, 1, 1, 1), (4, 4, 2, 4), 4, 3), ((2, 2, 2, 2), (1, 1, 1, 1), 2, 24),
                                      ((1, 1, 1, 2), (2, 2, 1, 2), 2, 5)):
