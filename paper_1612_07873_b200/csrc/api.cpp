@@ -749,7 +749,6 @@ int coarse_links_compress_hermitian(const cd_links *full, double *max_dev, void 
     if (c->kg.split != 0) return fail(CD_ERR_UNSUPPORTED, "compressed links are single-rank (no link halo yet)");
     cudaStream_t s = S(stream);
     if (max_dev) {
-        if (full->prec != CD_FP32) return fail(CD_ERR_UNSUPPORTED, "the hermiticity check needs fp32 links");
         DevBuf d;
         CUDA_TRY(cudaMalloc(&d.p, sizeof(float)), "cudaMalloc");
         float *dv = static_cast<float *>(d.p);
@@ -985,8 +984,9 @@ static int do_apply(const cd_links *l, cd_field *out, const cd_field *in, void *
     const bool halo = c->kg.split != 0;
     if (l->compressed) {   // tau3-hermitian compressed links (NEXT-2): one kernel, fp32, single rank
         if (halo) return fail(CD_ERR_UNSUPPORTED, "compressed links are single-rank");
-        if (l->prec != CD_FP32) return fail(CD_ERR_UNSUPPORTED, "compressed links: fp32 storage only");
         a.g = c->kg;
+        a.ysplit = c->ysplit;       // fp16: whole-site re-quantisation scratch
+        a.site_cnt = c->site_cnt;
         CUDA_TRY(launch_fgh(l->prec, a, s, c->pdl != 0), "compressed dslash launch");
         return CD_OK;
     }

@@ -496,6 +496,157 @@ __global__ void __launch_bounds__(288, NV == 24 ? 3 : 2) dslash_fgh(ApplyArgs a)
     }
 }
 
+// fp16 storage: the same decomposition with half2 payloads (FHFMA, one scale product per hop) and
+// the whole-site re-quantisation of the fp16 row-split fg variants (fp32 rows parked in an
+// L2-resident scratch, the last of the site's CTAs quantises).
+template <int NV>
+__global__ void __launch_bounds__(288, 3) dslash_fgh16(ApplyArgs a)
+{
+    using Q = Cfg<CD_FP16, NV>;
+    constexpr int ROWS = 16;
+    constexpr int NRB = Q::N / ROWS;
+    constexpr int RG = ROWS / Q::R;
+    constexpr int TJ = Q::N / 8;             // backward: input rows j per lane (8 j-groups), 16 B each
+    __shared__ __align__(16) unsigned char vs[9 * Q::VREC];
+    __shared__ float2 part[9][ROWS];
+    __shared__ float red[32];
+    __shared__ int last;
+    const int site = blockIdx.x / NRB, rb = blockIdx.x - site * NRB;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int k = kseq(warp);
+    const unsigned char *links = static_cast<const unsigned char *>(a.links);
+    const unsigned char *in = static_cast<const unsigned char *>(a.in);
+    int x[4];
+    decode(a.g, site, x);
+    const bool fwd = (k == 8) || !(k & 1);
+    const int msite = fwd ? site : neighbour(a.g, x, site, k);
+    const int crec = (k == 8) ? 0 : 1 + (k >> 1);
+    const unsigned char *m = links + ((size_t)msite * 5 + crec) * Q::MREC;
+    const int r = lane / Q::D, d = lane % Q::D;
+    const int ic = lane & 3, gj = lane >> 2;   // backward: (4 columns i, j group)
+    uint4 Lc[RG][Q::C];
+    uint4 Mc[TJ];
+    if (fwd) {
+#pragma unroll
+        for (int g = 0; g < RG; g++)
+#pragma unroll
+            for (int c = 0; c < Q::C; c++)
+                Lc[g][c] = ld_stream(m + (rb * ROWS + g * Q::R + r) * Q::ROWB + (d + Q::D * c) * 16);
+    } else {
+#pragma unroll
+        for (int t = 0; t < TJ; t++)   // rows j = gj + 8t: 8 x 64-byte column strips per instruction
+            Mc[t] = ld_stream(m + (size_t)(gj + 8 * t) * Q::ROWB + (rb * ROWS + 4 * ic) * 4);
+    }
+    const float msc = ld_nc_f32(m + Q::MSCALE);
+    pdl_trigger();
+    pdl_wait();
+    for (int t = threadIdx.x; t < 9 * Q::VCH; t += 288) {
+        const int kk = t / Q::VCH, e = t - kk * Q::VCH;
+        const int nb = neighbour(a.g, x, site, kk);
+        *reinterpret_cast<uint4 *>(vs + kk * Q::VREC + e * 16) = ld_nc(in + (size_t)nb * Q::VREC + e * 16);
+    }
+    __syncthreads();
+    const unsigned char *vrec = vs + k * Q::VREC;
+    const float sc = msc * *reinterpret_cast<const float *>(vrec + Q::VSCALE);
+    if (fwd) {
+#pragma unroll
+        for (int g = 0; g < RG; g++) {
+            float ra = 0.f, rb2 = 0.f, ia = 0.f, ib = 0.f;
+#pragma unroll
+            for (int c = 0; c < Q::C; c++) {
+                const int q = d + Q::D * c;
+                uint4 vq = lds128(vrec + q * 16);
+                if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<true>(vq);
+                hmac4(Lc[g][c], vq, ra, rb2, ia, ib);
+            }
+            float re = (ra - rb2) * sc, im = (ia + ib) * sc;
+#pragma unroll
+            for (int o = Q::D / 2; o >= 1; o >>= 1) {
+                re += shfl_xor(re, o);
+                im += shfl_xor(im, o);
+            }
+            if (d == 0) part[warp][g * Q::R + r] = make_float2(re, im);
+        }
+    } else {
+        float ra[4] = {0.f, 0.f, 0.f, 0.f}, rb2[4] = {0.f, 0.f, 0.f, 0.f};
+        float ia[4] = {0.f, 0.f, 0.f, 0.f}, ib[4] = {0.f, 0.f, 0.f, 0.f};
+        const uint32_t *u32 = reinterpret_cast<const uint32_t *>(vrec);
+#pragma unroll
+        for (int t = 0; t < TJ; t++) {
+            const int j = gj + 8 * t;
+            uint32_t u = u32[j];
+            if ((j >= NV) != (a.dagger && j >= NV)) u ^= 0x80008000u;   // s_j, times the dagger's tau3
+            const uint32_t *mw = &Mc[t].x;                           // M[j][i .. i+3]
+#pragma unroll
+            for (int q = 0; q < 4; q++) hmac1(mw[q], u, ra[q], rb2[q], ia[q], ib[q]);   // conj(M) u
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            float re = (ra[q] + rb2[q]) * sc, im = (ia[q] - ib[q]) * sc;
+#pragma unroll
+            for (int o = 4; o <= 16; o <<= 1) {
+                re += shfl_xor(re, o);
+                im += shfl_xor(im, o);
+            }
+            const int il = 4 * ic + q;
+            const float si = (rb * ROWS + il >= NV) ? -1.0f : 1.0f;
+            if (gj == 0) part[warp][il] = make_float2(si * re, si * im);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < ROWS) {
+        float yr = 0.0f, yi = 0.0f;
+#pragma unroll
+        for (int w = 0; w < 9; w++) {
+            yr += part[w][threadIdx.x].x;
+            yi += part[w][threadIdx.x].y;
+        }
+        const int row = rb * ROWS + threadIdx.x;
+        const float sg = (a.dagger && row >= NV) ? -1.0f : 1.0f;
+        a.ysplit[(size_t)site * Q::N + row] = make_float2(sg * yr, sg * yi);
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = (atomicAdd(&a.site_cnt[site], 1) == NRB - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const bool own = threadIdx.x < Q::N;
+    const float2 v = own ? __ldcg(&a.ysplit[(size_t)site * Q::N + threadIdx.x]) : make_float2(0.f, 0.f);
+    if (threadIdx.x == 0) a.site_cnt[site] = 0;
+    store_site<CD_FP16, NV>(static_cast<unsigned char *>(a.out), site, own ? threadIdx.x : 0, own, v.x, v.y, red, 288, -1);
+}
+
+// hermiticity deviation of fp16 links, on the dequantised values (payload x record scale)
+template <int NV>
+__global__ void links_herm_dev16_kernel(const unsigned char *full, KGeom g, float *dev)
+{
+    using Q = Cfg<CD_FP16, NV>;
+    const int site = blockIdx.x >> 2, mu = blockIdx.x & 3;
+    int x[4];
+    decode(g, site, x);
+    const int nb = neighbour(g, x, site, 2 * mu + 1);
+    const unsigned char *Br = full + ((size_t)site * 9 + 2 * mu + 1) * Q::MREC;
+    const unsigned char *Fr = full + ((size_t)nb * 9 + 2 * mu) * Q::MREC;
+    const __half2 *B = reinterpret_cast<const __half2 *>(Br);
+    const __half2 *F = reinterpret_cast<const __half2 *>(Fr);
+    const float sb = *reinterpret_cast<const float *>(Br + Q::MSCALE), sf = *reinterpret_cast<const float *>(Fr + Q::MSCALE);
+    float mx = 0.0f;
+    for (int e = threadIdx.x; e < Q::N * Q::N; e += blockDim.x) {
+        const int i = e / Q::N, j = e - i * Q::N;
+        const float s = ((i < NV) == (j < NV)) ? 1.0f : -1.0f;
+        const float2 f = __half22float2(F[j * Q::N + i]);
+        const float2 b = __half22float2(B[e]);
+        // rounded products (no contraction): equal scales and mirrored payloads give exactly 0
+        const float bx = __fmul_rn(b.x, sb), by = __fmul_rn(b.y, sb);
+        const float fx = __fmul_rn(s * f.x, sf), fy = __fmul_rn(s * f.y, sf);
+        mx = fmaxf(mx, fmaxf(fabsf(bx - fx), fabsf(by + fy)));
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, shfl_xor(mx, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int *>(dev), __float_as_int(mx));
+}
+
 // full links -> compressed records (X, L_0, L_2, L_4, L_6 per site), one CTA per output record
 template <cd_precision P, int NV>
 __global__ void links_compress_kernel(const unsigned char *full, unsigned char *comp, int64_t nrec)
@@ -1378,14 +1529,10 @@ cudaError_t launch_pack_t(const void *field, void *send, const KGeom &g, cudaStr
     cudaError_t launch_halo_##TAG(const ApplyArgs &a, cudaStream_t s) { return launch_halo_t<P, NV>(a, s); }      \
     cudaError_t launch_fgh_##TAG(const ApplyArgs &a, cudaStream_t s, bool pdl)                                    \
     {                                                                                                             \
-        if constexpr (P != CD_FP32) {                                                                             \
-            return cudaErrorNotSupported;                                                                         \
-        } else {                                                                                                  \
-            ApplyArgs aa = a;                                                                                     \
-            void *args[] = {&aa};                                                                                 \
-            return launch_ex((const void *)dslash_fgh<NV>, dim3((unsigned)(a.g.V * (2 * NV / 16))), dim3(288), 0, \
-                             s, pdl, args);                                                                       \
-        }                                                                                                         \
+        ApplyArgs aa = a;                                                                                         \
+        void *args[] = {&aa};                                                                                     \
+        const void *fn = P == CD_FP32 ? (const void *)dslash_fgh<NV> : (const void *)dslash_fgh16<NV>;            \
+        return launch_ex(fn, dim3((unsigned)(a.g.V * (2 * NV / 16))), dim3(288), 0, s, pdl, args);                \
     }                                                                                                             \
     cudaError_t launch_compress_##TAG(const void *full, void *comp, int64_t nsites, cudaStream_t s)               \
     {                                                                                                             \
@@ -1396,14 +1543,13 @@ cudaError_t launch_pack_t(const void *field, void *send, const KGeom &g, cudaStr
     }                                                                                                             \
     cudaError_t launch_hermdev_##TAG(const void *full, const KGeom &g, float *dev, cudaStream_t s)                \
     {                                                                                                             \
-        if constexpr (P != CD_FP32) {                                                                             \
-            return cudaErrorNotSupported;                                                                         \
-        } else {                                                                                                  \
-            count_launch();                                                                                       \
-            links_herm_dev_kernel<NV><<<(unsigned)(g.V * 4), 256, 0, s>>>(static_cast<const unsigned char *>(full), \
-                                                                         g, dev);                                 \
-            return cudaGetLastError();                                                                            \
-        }                                                                                                         \
+        count_launch();                                                                                           \
+        const unsigned char *fu = static_cast<const unsigned char *>(full);                                      \
+        if constexpr (P == CD_FP32)                                                                               \
+            links_herm_dev_kernel<NV><<<(unsigned)(g.V * 4), 256, 0, s>>>(fu, g, dev);                            \
+        else                                                                                                      \
+            links_herm_dev16_kernel<NV><<<(unsigned)(g.V * 4), 256, 0, s>>>(fu, g, dev);                          \
+        return cudaGetLastError();                                                                                \
     }                                                                                                             \
     cudaError_t launch_chain_##TAG(int id, const ApplyArgs &a, int n, unsigned base, cudaStream_t s, int sms,     \
                                    int *nrb)                                                                      \

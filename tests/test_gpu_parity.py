@@ -670,3 +670,27 @@ def test_even_odd_halo_self_exchange(mask):
     t = synth.tau3_signs(N)
     E.apply_eo(fout, fin, dagger=True)
     assert rel_l2(fout.export(), (t * oracle.schur_apply(dims, Lh, t * v))[par == 0]) <= 1e-5
+
+
+@pytest.mark.parametrize("dims,nvec", [((2, 2, 2, 2), 24), ((3, 4, 2, 5), 24), ((2, 3, 2, 2), 32), ((4, 4, 4, 4), 24)])
+def test_compressed_hermitian_links_fp16(dims, nvec):
+    """fp16 compressed links: the deviation check is exact on quantised tau3-hermitian links (paired
+    matrices share their scale, R12); apply / dagger match the oracle (fp16 gate) and the
+    uncompressed fp16 apply of the same stored links."""
+    N = 2 * nvec
+    Lh = synth.links(dims, N, kind="hermitian")
+    v = synth.vector(dims, N)
+    ctx = cd.Context(dims, nvec)
+    L = ctx.links_upload(Lh, "fp16")
+    C, dev = L.compress_hermitian()
+    assert dev == 0.0
+    fin, fout, fref = ctx.field("fp16"), ctx.field("fp16"), ctx.field("fp16")
+    fin.import_(v)
+    C.apply(fout, fin)
+    L.apply(fref, fin)
+    assert rel_l2(fout.export(), oracle.apply(dims, Lh, v)) <= 5e-3
+    assert rel_l2(fout.export(), fref.export()) <= 2e-3
+    C.apply_dagger(fout, fin)
+    assert rel_l2(fout.export(), oracle.adjoint(dims, Lh, v)) <= 5e-3
+    _, dev_g = ctx.links_upload(synth.links(dims, N, kind="general"), "fp16").compress_hermitian()
+    assert dev_g > 0.1
