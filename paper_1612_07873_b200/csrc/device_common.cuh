@@ -52,13 +52,10 @@ __device__ __forceinline__ float ld_nc_f32(const void *p)
     asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(r) : "l"(p));
     return r;
 }
-__device__ __forceinline__ uint4 lds128(const void *p)
-{
-    uint4 r;
-    uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
-    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
-    return r;
-}
+// 128-bit shared-memory load as a plain C++ access (not volatile asm): the compiler may batch and
+// hoist these loads (they only move within barrier-delimited regions), which hides their latency
+// when several chunks feed independent FMA chains.
+__device__ __forceinline__ uint4 lds128(const void *p) { return *reinterpret_cast<const uint4 *>(p); }
 
 // ------------------------------------------------------------------ PDL (griddepcontrol)
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

@@ -740,6 +740,14 @@ __global__ void __launch_bounds__(FgCfg<P, NV, KW, WR>::THREADS) dslash_chain(Ap
         for (int c = 0; c < Q::C; c++) Lc[kk][c] = ld_stream(m + row * Q::ROWB + (d + Q::D * c) * 16);
         sl[kk] = Q::F16 ? ld_nc_f32(m + Q::MSCALE) : 0.0f;
     }
+
+    if (a.dagger) {   // tau3 on the input, folded once into the register-resident links (chunks j >= Nvec)
+#pragma unroll
+        for (int j = 0; j < KW; j++)
+#pragma unroll
+            for (int c = 0; c < Q::C; c++)
+                if ((d + Q::D * c) * Q::CPC >= NV) Lc[j][c] = neg_chunk<Q::F16>(Lc[j][c]);
+    }
     const int t9 = threadIdx.x < 9 ? neighbour(a.g, x, site, threadIdx.x) : 0;
 
     for (int t = 0; t < n; t++) {
@@ -770,7 +778,6 @@ __global__ void __launch_bounds__(FgCfg<P, NV, KW, WR>::THREADS) dslash_chain(Ap
                     pi[c] = 0.0f;
                     const int q = d + Q::D * c;
                     uint4 vq = lds128(vrec + q * 16);
-                    if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<false>(vq);
                     cmac2(Lc[kk][c], vq, pr[c], pi[c]);
                 }
 #pragma unroll
@@ -781,7 +788,6 @@ __global__ void __launch_bounds__(FgCfg<P, NV, KW, WR>::THREADS) dslash_chain(Ap
                 for (int c = 0; c < Q::C; c++) {
                     const int q = d + Q::D * c;
                     uint4 vq = lds128(vrec + q * 16);
-                    if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<true>(vq);
                     hmac4(Lc[kk][c], vq, ra, rb2, ia, ib);
                 }
                 const float sc = sl[kk] * *reinterpret_cast<const float *>(vrec + Q::VSCALE);
@@ -870,6 +876,14 @@ __global__ void __launch_bounds__(FgCfg<P, NV, KW, WR>::THREADS) dslash_llchain(
         for (int c = 0; c < Q::C; c++) Lc[kk][c] = ld_stream(m + row * Q::ROWB + (d + Q::D * c) * 16);
         sl[kk] = Q::F16 ? ld_nc_f32(m + Q::MSCALE) : 0.0f;
     }
+
+    if (a.dagger) {   // tau3 on the input, folded once into the register-resident links (chunks j >= Nvec)
+#pragma unroll
+        for (int j = 0; j < KW; j++)
+#pragma unroll
+            for (int c = 0; c < Q::C; c++)
+                if ((d + Q::D * c) * Q::CPC >= NV) Lc[j][c] = neg_chunk<Q::F16>(Lc[j][c]);
+    }
     // the LL units this thread gathers: (hop k, unit w) -> source site
     int uk[U], uw[U], unb[U];
 #pragma unroll
@@ -938,7 +952,6 @@ __global__ void __launch_bounds__(FgCfg<P, NV, KW, WR>::THREADS) dslash_llchain(
                     pi[c] = 0.0f;
                     const int q = d + Q::D * c;
                     uint4 vq = lds128(vrec + q * 16);
-                    if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<false>(vq);
                     cmac2(Lc[kk][c], vq, pr[c], pi[c]);
                 }
 #pragma unroll
@@ -949,7 +962,6 @@ __global__ void __launch_bounds__(FgCfg<P, NV, KW, WR>::THREADS) dslash_llchain(
                 for (int c = 0; c < Q::C; c++) {
                     const int q = d + Q::D * c;
                     uint4 vq = lds128(vrec + q * 16);
-                    if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<true>(vq);
                     hmac4(Lc[kk][c], vq, ra, rb2, ia, ib);
                 }
                 const float sc = sl[kk] * *reinterpret_cast<const float *>(vrec + Q::VSCALE);
@@ -1082,6 +1094,14 @@ __global__ void __launch_bounds__(ClusterCfg<P, NV, NW>::THREADS, 1) dslash_clus
         for (int c = 0; c < Q::C; c++) Lc[j][c] = ld_stream(m + row * Q::ROWB + (d + Q::D * c) * 16);
         sl[j] = Q::F16 ? ld_nc_f32(m + Q::MSCALE) : 0.0f;
     }
+
+    if (a.dagger) {   // tau3 on the input, folded once into the register-resident links (chunks j >= Nvec)
+#pragma unroll
+        for (int j = 0; j < K::TPW; j++)
+#pragma unroll
+            for (int c = 0; c < Q::C; c++)
+                if ((d + Q::D * c) * Q::CPC >= NV) Lc[j][c] = neg_chunk<Q::F16>(Lc[j][c]);
+    }
     // this thread's neighbour chunk (for the staging step)
     const int sk = threadIdx.x / Q::VCH, se = threadIdx.x - sk * Q::VCH;
     const bool stager = sk < 9;
@@ -1107,7 +1127,6 @@ __global__ void __launch_bounds__(ClusterCfg<P, NV, NW>::THREADS, 1) dslash_clus
                 for (int c = 0; c < Q::C; c++) {
                     const int q = d + Q::D * c;
                     uint4 vq = lds128(vrec + q * 16);
-                    if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<false>(vq);
                     cmac2(Lc[j][c], vq, re, im);
                 }
             } else {
@@ -1116,7 +1135,6 @@ __global__ void __launch_bounds__(ClusterCfg<P, NV, NW>::THREADS, 1) dslash_clus
                 for (int c = 0; c < Q::C; c++) {
                     const int q = d + Q::D * c;
                     uint4 vq = lds128(vrec + q * 16);
-                    if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<true>(vq);
                     hmac4(Lc[j][c], vq, ra, rb2, ia, ib);
                 }
                 const float sc = sl[j] * *reinterpret_cast<const float *>(vrec + Q::VSCALE);
