@@ -235,8 +235,8 @@ int coarse_dslash_apply_chain(const cd_links *links, cd_field *x, cd_field *y, i
  * with the same nrhs (a multiple of 128), on the tcgen05 tensor cores: per site one
  * 128 x 2N x (9 * 2N) fp16 x fp16 -> fp32 GEMM accumulated in TMEM (the links are read once
  * for 128 right-hand sides); persistent warp-specialised kernel (TMA ring, tcgen05.mma, TMEM
- * double buffer).  fp16 storage only (CD_ERR_UNSUPPORTED otherwise); single-rank
- * contexts only in this version. */
+ * double buffer).  fp16 storage only (CD_ERR_UNSUPPORTED otherwise).  Collective on multi-rank
+ * contexts: face blocks are exchanged (NCCL) while the interior sites run. */
 int coarse_dslash_apply_mrhs(const cd_links *links, cd_field *out, const cd_field *in, int dagger, void *stream);
 
 /* ------------------------------------------------------------------ even-odd

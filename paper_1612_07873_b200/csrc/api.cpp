@@ -281,7 +281,7 @@ static int setup_halo(cd_context *c)
     CUDA_TRY(cudaMemset(c->recv_buf, 0, cap), "memset");
     c->halo_cap = cap;
     CUDA_TRY(cudaMalloc(&c->face_scratch, sizeof(float2) * c->V * c->N), "cudaMalloc(scratch)");
-    std::vector<int> faces;
+    std::vector<int> faces, interior;
     for (int64_t s = 0; s < c->V; s++) {
         int64_t t = s;
         int x[4];
@@ -293,8 +293,14 @@ static int setup_halo(cd_context *c)
         for (int mu = 0; mu < 4; mu++)
             if (((c->kg.split >> mu) & 1) && (x[mu] == 0 || x[mu] == c->local[mu] - 1)) face = true;
         if (face) faces.push_back((int)s);
+        else interior.push_back((int)s);
     }
     c->n_face = (int)faces.size();
+    c->n_interior = (int)interior.size();
+    CUDA_TRY(cudaMalloc(&c->interior_sites, sizeof(int) * std::max<size_t>(1, interior.size())), "cudaMalloc(interior)");
+    if (!interior.empty())
+        CUDA_TRY(cudaMemcpy(c->interior_sites, interior.data(), sizeof(int) * interior.size(), cudaMemcpyHostToDevice),
+                 "cudaMemcpy(interior)");
     CUDA_TRY(cudaMalloc(&c->face_sites, sizeof(int) * std::max<size_t>(1, faces.size())), "cudaMalloc(faces)");
     if (!faces.empty())
         CUDA_TRY(cudaMemcpy(c->face_sites, faces.data(), sizeof(int) * faces.size(), cudaMemcpyHostToDevice),
@@ -440,6 +446,9 @@ int cd_context_destroy(cd_context *c)
     if (c->recv_buf) cudaFree(c->recv_buf);
     if (c->face_scratch) cudaFree(c->face_scratch);
     if (c->face_sites) cudaFree(c->face_sites);
+    if (c->interior_sites) cudaFree(c->interior_sites);
+    if (c->mrhs_send) cudaFree(c->mrhs_send);
+    if (c->mrhs_recv) cudaFree(c->mrhs_recv);
     if (c->work) cudaFree(c->work);
     if (c->ysplit) cudaFree(c->ysplit);
     if (c->site_cnt) cudaFree(c->site_cnt);
@@ -481,9 +490,15 @@ int cd_context_set_option(cd_context *c, int option, int64_t value)
             cudaFree(c->recv_buf);
             cudaFree(c->face_scratch);
             cudaFree(c->face_sites);
+            cudaFree(c->interior_sites);
+            if (c->mrhs_send) cudaFree(c->mrhs_send);
+            if (c->mrhs_recv) cudaFree(c->mrhs_recv);
             c->send_buf = c->recv_buf = nullptr;
             c->face_scratch = nullptr;
             c->face_sites = nullptr;
+            c->interior_sites = nullptr;
+            c->mrhs_send = c->mrhs_recv = nullptr;
+            c->mrhs_cap = 0;
             c->halo_ready = false;
         }
         c->halo_self_mask = (int)value;
@@ -1177,10 +1192,63 @@ int coarse_dslash_apply_mrhs(const cd_links *l, cd_field *out, const cd_field *i
     if (in->nrhs % 128) return fail(CD_ERR_UNSUPPORTED, "nrhs must be a multiple of 128");
     if (out->base == in->base) return fail(CD_ERR_INVALID, "out must not alias in");
     cd_context *c = l->ctx;
-    if (c->kg.split != 0) return fail(CD_ERR_UNSUPPORTED, "apply_mrhs is single-rank (no halo split) for now");
     c->applied = true;
-    CUDA_TRY(launch_mrhs(c->nvec, l->base, in->base, out->base, c->kg, in->nrhs, dagger ? 1 : 0, S(stream), c->num_sms),
-             "mrhs launch");
+    cudaStream_t s = S(stream);
+    if (c->kg.split == 0) {
+        CUDA_TRY(launch_mrhs(c->nvec, l->base, in->base, out->base, c->kg, in->nrhs, dagger ? 1 : 0, s, c->num_sms),
+                 "mrhs launch");
+        return CD_OK;
+    }
+    // multi-rank: the face blocks of every split dim travel in the tensor-core layout
+    // ([f][rhs block] records of 128 rhs); the interior sites run while the exchange is in flight,
+    // the face sites after it (their remote hops read the receive buffer).
+    if (c->comm) {
+        std::string err;
+        const int r = comm_check(c->comm, err);
+        if (r != CD_OK) return fail(r, err);
+    }
+    const int nrb = in->nrhs / 128;
+    const size_t blk = (size_t)128 * 4 * c->N + 16;
+    cd_halo_plan pl = ctx_plan(c, CD_FP16);
+    MrhsHalo hl{};
+    int64_t off = 0;
+    for (int mu = 0; mu < 4; mu++) {
+        pl.block_offset[mu][0] = pl.block_offset[mu][1] = 0;
+        pl.block_bytes[mu] = 0;
+        if (!((c->kg.split >> mu) & 1)) continue;
+        const int64_t b = (int64_t)(c->V / c->local[mu]) * nrb * (int64_t)blk;
+        pl.block_offset[mu][0] = hl.off[mu][0] = off;
+        pl.block_offset[mu][1] = hl.off[mu][1] = off + b;
+        pl.block_bytes[mu] = b;
+        off += 2 * b;
+    }
+    pl.total_bytes = off;
+    if ((size_t)off > c->mrhs_cap) {
+        if (c->mrhs_send) cudaFree(c->mrhs_send);
+        if (c->mrhs_recv) cudaFree(c->mrhs_recv);
+        c->mrhs_send = c->mrhs_recv = nullptr;
+        c->mrhs_cap = 0;
+        CUDA_TRY(cudaMalloc(&c->mrhs_send, (size_t)off), "cudaMalloc(mrhs send)");
+        CUDA_TRY(cudaMalloc(&c->mrhs_recv, (size_t)off), "cudaMalloc(mrhs recv)");
+        c->mrhs_cap = (size_t)off;
+    }
+    hl.recv = c->mrhs_recv;
+    CUDA_TRY(cudaEventRecord(c->ev_in, s), "cudaEventRecord");
+    CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->ev_in, 0), "cudaStreamWaitEvent");
+    CUDA_TRY(launch_mrhs_pack(c->nvec, in->base, c->mrhs_send, c->kg, in->nrhs, hl, c->comm_stream), "mrhs pack");
+    {
+        std::string err;
+        const int r = halo_exchange_buf(c, pl, c->mrhs_send, c->mrhs_recv, c->comm_stream, err);
+        if (r != CD_OK) return fail(r, err);
+    }
+    CUDA_TRY(cudaEventRecord(c->ev_halo, c->comm_stream), "cudaEventRecord");
+    CUDA_TRY(launch_mrhs(c->nvec, l->base, in->base, out->base, c->kg, in->nrhs, dagger ? 1 : 0, s, c->num_sms,
+                         c->interior_sites, c->n_interior, &hl),
+             "mrhs interior launch");
+    CUDA_TRY(cudaStreamWaitEvent(s, c->ev_halo, 0), "cudaStreamWaitEvent");
+    CUDA_TRY(launch_mrhs(c->nvec, l->base, in->base, out->base, c->kg, in->nrhs, dagger ? 1 : 0, s, c->num_sms,
+                         c->face_sites, c->n_face, &hl),
+             "mrhs face launch");
     return CD_OK;
     API_END
 }

@@ -93,6 +93,10 @@ struct cd_context {
     size_t halo_cap = 0;
     float2 *face_scratch = nullptr;   // fp32 partial y for face sites [V][N]
     int *face_sites = nullptr;        // device list of face site indices
+    int *interior_sites = nullptr;    // device list of the other sites (multi-RHS overlap)
+    int n_interior = 0;
+    void *mrhs_send = nullptr, *mrhs_recv = nullptr;   // multi-RHS halo buffers (lazy)
+    size_t mrhs_cap = 0;
     int *work = nullptr;              // ring kernel ticket counters (4 slots x 2 ints, zero between
                                       // launches); applies on one context must be stream-ordered
     uint32_t seq = 0;                 // dslash launch sequence number
@@ -220,8 +224,17 @@ cudaError_t launch_eo_apply(int nvec, const EoApply &e);
 cudaError_t launch_fgh(cd_precision p, const ApplyArgs &a, cudaStream_t s, bool pdl);
 cudaError_t launch_compress(cd_precision p, int nv, const void *full, void *comp, int64_t nsites, cudaStream_t s);
 cudaError_t launch_hermdev(cd_precision p, int nv, const void *full, const KGeom &g, float *dev, cudaStream_t s);
+// multi-RHS halo: receive buffer in the tensor-core wire layout (per split dim: block A = the
+// x_mu = L-1 face records for the +mu neighbour, block B = the x_mu = 0 face, each [face f][rb])
+struct MrhsHalo {
+    const void *recv;        // nullptr: single rank (no remote hops)
+    int64_t off[4][2];       // byte offset of block (mu, A/B)
+};
 cudaError_t launch_mrhs(int nvec, const void *links, const void *in, void *out, const KGeom &g, int nrhs, int dagger,
-                        cudaStream_t s, int num_sms);
+                        cudaStream_t s, int num_sms, const int *sites = nullptr, int nsites = 0,
+                        const MrhsHalo *halo = nullptr);
+cudaError_t launch_mrhs_pack(int nvec, const void *field, void *send, const KGeom &g, int nrhs, const MrhsHalo &offs,
+                             cudaStream_t s);
 cudaError_t launch_flush(void *buf, size_t bytes, cudaStream_t s);
 int restrict_cluster_size(const TGeom &t, int num_sms);
 cudaError_t launch_restrict(cd_precision pc, int nvec, int cl, const void *W, const void *vf, void *vc, const TGeom &t,

@@ -116,8 +116,14 @@ int comm_check(Comm *c, std::string &err)
 // this rank itself (P_mu = 1, forced through the halo path) are copied device-to-device.
 int halo_exchange(cd_context *ctx, const cd_halo_plan &pl, cudaStream_t s, std::string &err)
 {
-    const unsigned char *send = static_cast<const unsigned char *>(ctx->send_buf);
-    unsigned char *recv = static_cast<unsigned char *>(ctx->recv_buf);
+    return halo_exchange_buf(ctx, pl, ctx->send_buf, ctx->recv_buf, s, err);
+}
+
+int halo_exchange_buf(cd_context *ctx, const cd_halo_plan &pl, const void *send_, void *recv_, cudaStream_t s,
+                      std::string &err)
+{
+    const unsigned char *send = static_cast<const unsigned char *>(send_);
+    unsigned char *recv = static_cast<unsigned char *>(recv_);
     bool group = false;
     for (int mu = 0; mu < 4; mu++) {
         if (!((pl.split_mask >> mu) & 1)) continue;

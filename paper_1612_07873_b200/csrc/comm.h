@@ -10,4 +10,7 @@ int comm_create(const uint8_t id[128], int nranks, int rank, Comm **out, std::st
 void comm_destroy(Comm *c);
 int comm_check(Comm *c, std::string &err);
 int halo_exchange(cd_context *ctx, const cd_halo_plan &plan, cudaStream_t s, std::string &err);
+// the same exchange between caller-given send / receive buffers laid out by `plan`
+int halo_exchange_buf(cd_context *ctx, const cd_halo_plan &plan, const void *send, void *recv, cudaStream_t s,
+                      std::string &err);
 }  // namespace cd

@@ -119,11 +119,39 @@ __device__ __forceinline__ void reg_fence16(uint32_t *r)
 
 // Item -> (site, rhs block), lexicographic: the ~148 items in flight are consecutive sites, which
 // share most of their neighbour lines in L2 (a 4-D Morton order was measured 7 % slower).
-__device__ __forceinline__ int item_site(int64_t it, int nrb, int &rb)
+__device__ __forceinline__ int item_site(int64_t it, int nrb, int &rb, const int *sites)
 {
     const int z = (int)(it / nrb);
     rb = (int)(it - (int64_t)z * nrb);
-    return z;
+    return sites ? __ldg(sites + z) : z;
+}
+
+// The A block of hop k: the neighbour's block in this rank's field, or -- for a hop that leaves
+// the rank (multi-rank) -- its copy in the halo receive buffer: a +mu hop reads block B (sent by
+// the +mu neighbour from its x_mu = 0 face), a -mu hop block A (R13 order, per rhs block).
+// hl.off[mu][blk] without dynamic indexing of a kernel parameter (which would force a local copy)
+__device__ __forceinline__ int64_t halo_off(const MrhsHalo &hl, int mu, int blk)
+{
+    const int64_t a0 = blk ? hl.off[0][1] : hl.off[0][0], a1 = blk ? hl.off[1][1] : hl.off[1][0];
+    const int64_t a2 = blk ? hl.off[2][1] : hl.off[2][0], a3 = blk ? hl.off[3][1] : hl.off[3][0];
+    return mu == 0 ? a0 : (mu == 1 ? a1 : (mu == 2 ? a2 : a3));
+}
+
+template <int BLK>
+__device__ __forceinline__ const unsigned char *nbr_block(const KGeom &g, const MrhsHalo &hl, const unsigned char *in,
+                                                          const int x[4], int site, int k, int nrb, int rb)
+{
+    if (hl.recv != nullptr && remote_hop(g, x, k)) {
+        const int mu = k >> 1;
+        const int blk = (k & 1) ? 0 : 1;
+        // face index: lexicographic over the other three dims (no dynamic register indexing)
+        const int f = mu == 0 ? (x[3] * g.L[2] + x[2]) * g.L[1] + x[1]
+                    : mu == 1 ? (x[3] * g.L[2] + x[2]) * g.L[0] + x[0]
+                    : mu == 2 ? (x[3] * g.L[1] + x[1]) * g.L[0] + x[0]
+                              : (x[2] * g.L[1] + x[1]) * g.L[0] + x[0];
+        return static_cast<const unsigned char *>(hl.recv) + halo_off(hl, mu, blk) + ((size_t)f * nrb + rb) * BLK;
+    }
+    return in + ((size_t)neighbour(g, x, site, k) * nrb + rb) * BLK;
 }
 
 __device__ __forceinline__ void st_evict_first(void *p, uint4 v, uint64_t pol)
@@ -136,18 +164,18 @@ __device__ __forceinline__ void st_evict_first(void *p, uint4 v, uint64_t pol)
 // hop products s_L(x,k) * s_v(nbr_k, block) and their max (identical in builders and epilogue)
 template <int NV>
 __device__ __forceinline__ float hop_scale(const unsigned char *links, const unsigned char *in, const KGeom &g,
-                                           const int x[4], int site, int k, int nrb, int rb)
+                                           const MrhsHalo &hl, const int x[4], int site, int k, int nrb, int rb)
 {
     using C = MrhsCfg<NV, 2>;
     const float sl = ld_nc_f32(links + ((size_t)site * 9 + k) * C::MREC + 4 * C::N * C::N);
-    const float sv = ld_nc_f32(in + ((size_t)neighbour(g, x, site, k) * nrb + rb) * C::BLK + C::A_BYTES);
+    const float sv = ld_nc_f32(nbr_block<C::BLK>(g, hl, in, x, site, k, nrb, rb) + C::A_BYTES);
     return sl * sv;
 }
 
 template <int NV, int NBS>
 __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
     dslash_mrhs(const unsigned char *__restrict__ links, const unsigned char *__restrict__ in, unsigned char *out,
-                KGeom g, int nrb, int dagger, long long *trace)
+                KGeom g, int nrb, int dagger, const int *sites, int nsites, MrhsHalo hl, long long *trace)
 {
     using C = MrhsCfg<NV, NBS>;
     // optional diagnostic trace of CTA 0 (CD_MRHS_TRACE): trace[ev * 512 + index] = clock64()
@@ -170,7 +198,7 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
     unsigned char *ring = bbuf + C::NBS * C::B_BYTES;            // [S][STAGE]
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t items = (int64_t)g.V * nrb;
+    const int64_t items = (int64_t)(sites ? nsites : g.V) * nrb;
 
     if (tid == 0) {
         for (int j = 0; j < C::S; j++) {
@@ -205,7 +233,7 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
             uint32_t h = 0;
             for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
                 int rb;
-                const int site = item_site(it, nrb, rb);
+                const int site = item_site(it, nrb, rb, sites);
                 int x[4];
                 decode(g, site, x);
                 for (int k = 0; k < 9; k++, h++) {
@@ -215,7 +243,7 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
                     unsigned char *dst = ring + st * C::STAGE;
                     mbar_arrive_expect_tx(&full[st], C::BLK + C::MREC);
                     // vectors are re-read by 9 sites (keep them in L2), links are read once
-                    bulk_g2s_hint(dst, in + ((size_t)neighbour(g, x, site, k) * nrb + rb) * C::BLK, C::BLK,
+                    bulk_g2s_hint(dst, nbr_block<C::BLK>(g, hl, in, x, site, k, nrb, rb), C::BLK,
                                   &full[st], pol_v);
                     bulk_g2s_hint(dst + C::BLK, links + ((size_t)site * 9 + k) * C::MREC, C::MREC, &full[st],
                                   pol_l);
@@ -275,11 +303,11 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
         float nsl = 0.0f, nsv = 0.0f;   // raw loads, multiplied only when consumed
         auto scale_of = [&](int64_t it) {
             int rb;
-                const int site = item_site(it, nrb, rb);
+                const int site = item_site(it, nrb, rb, sites);
             int x[4];
             decode(g, site, x);
             nsl = ld_nc_f32(links + ((size_t)site * 9 + bt) * C::MREC + 4 * C::N * C::N);
-            nsv = ld_nc_f32(in + ((size_t)neighbour(g, x, site, bt) * nrb + rb) * C::BLK + C::A_BYTES);
+            nsv = ld_nc_f32(nbr_block<C::BLK>(g, hl, in, x, site, bt, nrb, rb) + C::A_BYTES);
         };
         if (bt < 9 && (int64_t)blockIdx.x < items) scale_of(blockIdx.x);
         for (int64_t it = blockIdx.x; it < items; it += gridDim.x, t++) {
@@ -349,10 +377,10 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
         uint32_t t = 0;
         for (int64_t it = blockIdx.x; it < items; it += gridDim.x, t++) {
             int rb;
-                const int site = item_site(it, nrb, rb);
+                const int site = item_site(it, nrb, rb, sites);
             int x[4];
             decode(g, site, x);
-            if (et < 9) es[et] = hop_scale<NV>(links, in, g, x, site, et, nrb, rb);
+            if (et < 9) es[et] = hop_scale<NV>(links, in, g, hl, x, site, et, nrb, rb);
             const int acc = t & 1;
             if (et == 0) TR(6, t)
             mbar_wait(&accfull[acc], (t >> 1) & 1);
@@ -415,7 +443,7 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
 
 template <int NV, int NBS>
 static cudaError_t launch_mrhs_t(const void *links, const void *in, void *out, const KGeom &g, int nrhs, int dagger,
-                                 cudaStream_t s, int num_sms)
+                                 cudaStream_t s, int num_sms, const int *sites, int nsites, const MrhsHalo *halo)
 {
     using C = MrhsCfg<NV, NBS>;
     static bool attr = false;
@@ -425,7 +453,10 @@ static cudaError_t launch_mrhs_t(const void *links, const void *in, void *out, c
         attr = true;
     }
     const int nrb = nrhs / C::MR;
-    const int64_t items = (int64_t)g.V * nrb;
+    const int64_t items = (int64_t)(sites ? nsites : g.V) * nrb;
+    if (items == 0) return cudaSuccess;
+    MrhsHalo hl{};
+    if (halo) hl = *halo;
     count_launch();
     long long *trace = nullptr;
     const char *tf = getenv("CD_MRHS_TRACE");   // diagnostic only: per-event clock64 of CTA 0
@@ -435,7 +466,7 @@ static cudaError_t launch_mrhs_t(const void *links, const void *in, void *out, c
     }
     dslash_mrhs<NV, NBS><<<(unsigned)(items < num_sms ? items : num_sms), C::THREADS, C::SMEM, s>>>(
         static_cast<const unsigned char *>(links), static_cast<const unsigned char *>(in),
-        static_cast<unsigned char *>(out), g, nrb, dagger, trace);
+        static_cast<unsigned char *>(out), g, nrb, dagger, sites, nsites, hl, trace);
     cudaError_t e = cudaGetLastError();
     if (tf) {
         long long h[10 * 512];
@@ -451,12 +482,55 @@ static cudaError_t launch_mrhs_t(const void *links, const void *in, void *out, c
 }
 
 cudaError_t launch_mrhs(int nvec, const void *links, const void *in, void *out, const KGeom &g, int nrhs, int dagger,
-                        cudaStream_t s, int num_sms)
+                        cudaStream_t s, int num_sms, const int *sites, int nsites, const MrhsHalo *halo)
 {
     if (nrhs % 128) return cudaErrorInvalidValue;
     // B slots: 3 for Nvec 24 (2 and 4 measured 1-3 % slower), 2 for Nvec 32 (shared memory)
-    return nvec == 24 ? launch_mrhs_t<24, 3>(links, in, out, g, nrhs, dagger, s, num_sms)
-                      : launch_mrhs_t<32, 2>(links, in, out, g, nrhs, dagger, s, num_sms);
+    return nvec == 24 ? launch_mrhs_t<24, 3>(links, in, out, g, nrhs, dagger, s, num_sms, sites, nsites, halo)
+                      : launch_mrhs_t<32, 2>(links, in, out, g, nrhs, dagger, s, num_sms, sites, nsites, halo);
+}
+
+// face blocks of every split dim -> send buffer (one CTA row per (mu, A/B), records [f][rb])
+template <int BLK>
+__global__ void mrhs_pack_kernel(const unsigned char *field, unsigned char *send, KGeom g, int4 pairs, int nrb,
+                                 MrhsHalo offs)
+{
+    const int pi = blockIdx.y >> 1, blk = blockIdx.y & 1;
+    const int mu = pi == 0 ? pairs.x : (pi == 1 ? pairs.y : (pi == 2 ? pairs.z : pairs.w));
+    const int F = g.V / sel4(g.L, mu);
+    int o3[3], n = 0;
+    for (int nu = 0; nu < 4; nu++)
+        if (nu != mu) o3[n++] = nu;
+    for (int rec = blockIdx.x; rec < F * nrb; rec += gridDim.x) {
+        const int f = rec / nrb, rb = rec - f * nrb;
+        int x[4];
+        int t = f;
+        x[o3[0]] = t % g.L[o3[0]];
+        t /= g.L[o3[0]];
+        x[o3[1]] = t % g.L[o3[1]];
+        x[o3[2]] = t / g.L[o3[1]];
+        x[mu] = blk == 0 ? g.L[mu] - 1 : 0;
+        const uint4 *src = reinterpret_cast<const uint4 *>(field + ((size_t)encode(g, x) * nrb + rb) * BLK);
+        uint4 *dst = reinterpret_cast<uint4 *>(send + halo_off(offs, mu, blk) + (size_t)rec * BLK);
+        for (int e = threadIdx.x; e < BLK / 16; e += blockDim.x) dst[e] = src[e];
+    }
+}
+
+cudaError_t launch_mrhs_pack(int nvec, const void *field, void *send, const KGeom &g, int nrhs, const MrhsHalo &offs,
+                             cudaStream_t s)
+{
+    int4 pairs = make_int4(0, 0, 0, 0);
+    int np = 0;
+    for (int mu = 0; mu < 4; mu++)
+        if ((g.split >> mu) & 1) (&pairs.x)[np++] = mu;
+    if (np == 0) return cudaSuccess;
+    const dim3 grid(296, 2 * np);
+    const unsigned char *f = static_cast<const unsigned char *>(field);
+    unsigned char *d = static_cast<unsigned char *>(send);
+    count_launch();
+    if (nvec == 24) mrhs_pack_kernel<MrhsCfg<24>::BLK><<<grid, 256, 0, s>>>(f, d, g, pairs, nrhs / 128, offs);
+    else mrhs_pack_kernel<MrhsCfg<32>::BLK><<<grid, 256, 0, s>>>(f, d, g, pairs, nrhs / 128, offs);
+    return cudaGetLastError();
 }
 
 }  // namespace cd

@@ -39,6 +39,13 @@ for prec in ("fp32", "fp16"):
         x, y = ctx.field("fp16", nrhs=128), ctx.field("fp16", nrhs=128)
         x.generate()
         L.apply_mrhs(y, x)
+        mc = cd.Context((2, 2, 2, 4), 24)
+        mc.set_option(cd.CD_OPT_HALO_SELF_MASK, 0b1001)
+        ml = mc.links_generate("fp16", kind="hermitian", scale_log2=-4)
+        mx, my = mc.field("fp16", nrhs=128), mc.field("fp16", nrhs=128)
+        mx.generate()
+        ml.apply_mrhs(my, mx)
+        ml.apply_mrhs(mx, my, dagger=True)
     if which in ("all", "compressed") and prec == "fp32":
         C, _ = L.compress_hermitian()
         ctx.set_option(cd.CD_OPT_VARIANT, -1)
