@@ -204,10 +204,12 @@ int coarse_links_free(cd_links *l);
  * coarse operator with chirality-preserving aggregation, PAPER.md:121 fn. 1 -- the backward links
  * are L_{2mu+1}(x) = tau3 L_{2mu}(x-mu)^H tau3, so only X and the four forward links are stored
  * (5 of 9 matrices per site; the apply reads the neighbour's forward link transposed).  Creates a
- * new links object from `full`; if max_dev != NULL it first measures (host sync) the largest
- * deviation |L_{2mu+1}(x) - tau3 L_{2mu}(x-mu)^H tau3| (fp32 links only) so the caller can
- * decide whether the compression is exact.  Applies with compressed links: fp32, single rank
- * (CD_ERR_UNSUPPORTED otherwise). */
+ * new links object from `full`; if max_dev != NULL it also measures (host sync) the largest
+ * deviation |L_{2mu+1}(x) - tau3 L_{2mu}(x-mu)^H tau3| (on the dequantised values for fp16) so the
+ * caller can decide whether the compression is exact.  fp32 or fp16.  On a multi-rank context this
+ * call is collective: it performs a one-time link halo exchange (each rank sends the forward
+ * records of its x_mu = L_mu - 1 faces to the +mu neighbour) used by the backward hops of the
+ * x_mu = 0 sites; applies with the result are collective like coarse_dslash_apply. */
 int coarse_links_compress_hermitian(const cd_links *full, double *max_dev, void *stream, cd_links **out);
 
 /* ------------------------------------------------------------------ operator */

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <fstream>
 #include <sstream>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -115,10 +116,29 @@ cudaError_t launch_compress_f32_24(const void *, void *, int64_t, cudaStream_t);
 cudaError_t launch_compress_f32_32(const void *, void *, int64_t, cudaStream_t);
 cudaError_t launch_compress_f16_24(const void *, void *, int64_t, cudaStream_t);
 cudaError_t launch_compress_f16_32(const void *, void *, int64_t, cudaStream_t);
-cudaError_t launch_hermdev_f32_24(const void *, const KGeom &, float *, cudaStream_t);
-cudaError_t launch_hermdev_f32_32(const void *, const KGeom &, float *, cudaStream_t);
-cudaError_t launch_hermdev_f16_24(const void *, const KGeom &, float *, cudaStream_t);
-cudaError_t launch_hermdev_f16_32(const void *, const KGeom &, float *, cudaStream_t);
+cudaError_t launch_hermdev_f32_24(const void *, const KGeom &, float *, cudaStream_t, const void *, const int64_t *);
+cudaError_t launch_hermdev_f32_32(const void *, const KGeom &, float *, cudaStream_t, const void *, const int64_t *);
+cudaError_t launch_hermdev_f16_24(const void *, const KGeom &, float *, cudaStream_t, const void *, const int64_t *);
+cudaError_t launch_hermdev_f16_32(const void *, const KGeom &, float *, cudaStream_t, const void *, const int64_t *);
+cudaError_t launch_fgh_halo_f32_24(const ApplyArgs &, cudaStream_t);
+cudaError_t launch_fgh_halo_f32_32(const ApplyArgs &, cudaStream_t);
+cudaError_t launch_fgh_halo_f16_24(const ApplyArgs &, cudaStream_t);
+cudaError_t launch_fgh_halo_f16_32(const ApplyArgs &, cudaStream_t);
+cudaError_t launch_lhalo_pack_f32_24(const void *, void *, const KGeom &, const int64_t *, cudaStream_t);
+cudaError_t launch_lhalo_pack_f32_32(const void *, void *, const KGeom &, const int64_t *, cudaStream_t);
+cudaError_t launch_lhalo_pack_f16_24(const void *, void *, const KGeom &, const int64_t *, cudaStream_t);
+cudaError_t launch_lhalo_pack_f16_32(const void *, void *, const KGeom &, const int64_t *, cudaStream_t);
+cudaError_t launch_fgh_halo(cd_precision p, const ApplyArgs &a, cudaStream_t s)
+{
+    return PICK(p, a.nvec, launch_fgh_halo_f32_24(a, s), launch_fgh_halo_f32_32(a, s), launch_fgh_halo_f16_24(a, s),
+                launch_fgh_halo_f16_32(a, s));
+}
+cudaError_t launch_lhalo_pack(cd_precision p, int nv, const void *c, void *d, const KGeom &g, const int64_t *o,
+                              cudaStream_t s)
+{
+    return PICK(p, nv, launch_lhalo_pack_f32_24(c, d, g, o, s), launch_lhalo_pack_f32_32(c, d, g, o, s),
+                launch_lhalo_pack_f16_24(c, d, g, o, s), launch_lhalo_pack_f16_32(c, d, g, o, s));
+}
 cudaError_t launch_fgh(cd_precision p, const ApplyArgs &a, cudaStream_t s, bool pdl)
 {
     return PICK(p, a.nvec, launch_fgh_f32_24(a, s, pdl), launch_fgh_f32_32(a, s, pdl), launch_fgh_f16_24(a, s, pdl),
@@ -129,10 +149,11 @@ cudaError_t launch_compress(cd_precision p, int nv, const void *f, void *c, int6
     return PICK(p, nv, launch_compress_f32_24(f, c, n, s), launch_compress_f32_32(f, c, n, s),
                 launch_compress_f16_24(f, c, n, s), launch_compress_f16_32(f, c, n, s));
 }
-cudaError_t launch_hermdev(cd_precision p, int nv, const void *f, const KGeom &g, float *d, cudaStream_t s)
+cudaError_t launch_hermdev(cd_precision p, int nv, const void *f, const KGeom &g, float *d, cudaStream_t s,
+                           const void *lh, const int64_t *lo)
 {
-    return PICK(p, nv, launch_hermdev_f32_24(f, g, d, s), launch_hermdev_f32_32(f, g, d, s),
-                launch_hermdev_f16_24(f, g, d, s), launch_hermdev_f16_32(f, g, d, s));
+    return PICK(p, nv, launch_hermdev_f32_24(f, g, d, s, lh, lo), launch_hermdev_f32_32(f, g, d, s, lh, lo),
+                launch_hermdev_f16_24(f, g, d, s, lh, lo), launch_hermdev_f16_32(f, g, d, s, lh, lo));
 }
 cudaError_t launch_pack(cd_precision p, int nv, const void *f, void *d, const KGeom &g, cudaStream_t s)
 {
@@ -761,29 +782,53 @@ int coarse_links_compress_hermitian(const cd_links *full, double *max_dev, void 
     if (!full || !out) return fail(CD_ERR_INVALID, "links/out is NULL");
     if (full->compressed) return fail(CD_ERR_INVALID, "links are already compressed");
     cd_context *c = full->ctx;
-    if (c->kg.split != 0) return fail(CD_ERR_UNSUPPORTED, "compressed links are single-rank (no link halo yet)");
     cudaStream_t s = S(stream);
+    cd_links *l = nullptr;
+    int r = links_new(c, full->prec, &l, 1);
+    if (r != CD_OK) return r;
+    std::unique_ptr<cd_links, int (*)(cd_links *)> guard(l, coarse_links_free);
+    CUDA_TRY(launch_compress(full->prec, c->nvec, full->base, l->base, c->V, s), "links compress");
+    if (c->kg.split != 0) {
+        // multi-rank: a ONE-TIME link halo -- the backward hop of an x_mu = 0 site needs the -mu
+        // neighbour rank's forward record L_{2mu}(x - mu); every rank sends its x_mu = L-1 face
+        // records to the +mu neighbour (block A of the exchange; block B is unused).
+        const size_t mrec = mat_rec_bytes(c->N, full->prec);
+        cd_halo_plan pl = ctx_plan(c, full->prec);
+        int64_t off = 0;
+        for (int mu = 0; mu < 4; mu++) {
+            pl.block_offset[mu][0] = pl.block_offset[mu][1] = 0;
+            pl.block_bytes[mu] = 0;
+            if (!((c->kg.split >> mu) & 1)) continue;
+            const int64_t b = (int64_t)(c->V / c->local[mu]) * (int64_t)mrec;
+            pl.block_offset[mu][0] = l->lhoff[mu] = off;
+            pl.block_offset[mu][1] = off + b;
+            pl.block_bytes[mu] = b;
+            off += 2 * b;
+        }
+        pl.total_bytes = off;
+        DevBuf send;
+        CUDA_TRY(cudaMalloc(&send.p, (size_t)off), "cudaMalloc(link halo send)");
+        CUDA_TRY(cudaMalloc(&l->aux, (size_t)off), "cudaMalloc(link halo)");
+        CUDA_TRY(cudaMemsetAsync(send.p, 0, (size_t)off, s), "cudaMemsetAsync");
+        CUDA_TRY(launch_lhalo_pack(full->prec, c->nvec, l->base, send.p, c->kg, l->lhoff, s), "link halo pack");
+        std::string err;
+        r = halo_exchange_buf(c, pl, send.p, l->aux, s, err);
+        if (r != CD_OK) return fail(r, err);
+        CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    }
     if (max_dev) {
         DevBuf d;
         CUDA_TRY(cudaMalloc(&d.p, sizeof(float)), "cudaMalloc");
         float *dv = static_cast<float *>(d.p);
         CUDA_TRY(cudaMemsetAsync(dv, 0, sizeof(float), s), "cudaMemsetAsync");
-        CUDA_TRY(launch_hermdev(full->prec, c->nvec, full->base, c->kg, dv, s), "hermiticity check");
+        CUDA_TRY(launch_hermdev(full->prec, c->nvec, full->base, c->kg, dv, s, l->aux, l->aux ? l->lhoff : nullptr),
+                 "hermiticity check");
         float h = 0.0f;
         CUDA_TRY(cudaMemcpyAsync(&h, dv, sizeof(float), cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
         CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
         *max_dev = h;
     }
-    cd_links *l = nullptr;
-    int r = links_new(c, full->prec, &l, 1);
-    if (r != CD_OK) return r;
-    cudaError_t e = launch_compress(full->prec, c->nvec, full->base, l->base, c->V, s);
-    if (e != cudaSuccess) {
-        cudaFree(l->base);
-        delete l;
-        return cuda_fail(e, "links compress");
-    }
-    *out = l;
+    *out = guard.release();
     return CD_OK;
     API_END
 }
@@ -997,12 +1042,35 @@ static int do_apply(const cd_links *l, cd_field *out, const cd_field *in, void *
     a.nvec = c->nvec;
     a.dagger = dag;
     const bool halo = c->kg.split != 0;
-    if (l->compressed) {   // tau3-hermitian compressed links (NEXT-2): one kernel, fp32, single rank
-        if (halo) return fail(CD_ERR_UNSUPPORTED, "compressed links are single-rank");
-        a.g = c->kg;
+    if (l->compressed) {   // tau3-hermitian compressed links (NEXT-2)
         a.ysplit = c->ysplit;       // fp16: whole-site re-quantisation scratch
         a.site_cnt = c->site_cnt;
-        CUDA_TRY(launch_fgh(l->prec, a, s, c->pdl != 0), "compressed dslash launch");
+        if (!halo) {
+            a.g = c->kg;
+            CUDA_TRY(launch_fgh(l->prec, a, s, c->pdl != 0), "compressed dslash launch");
+            return CD_OK;
+        }
+        // multi-rank: vector halo as for the full operator; remote backward hops use the link halo
+        a.g = halo_geom(c, l->prec);
+        a.halo = 1;
+        a.scratch = c->face_scratch;
+        a.recv = c->recv_buf;
+        a.face_sites = c->face_sites;
+        a.n_face = c->n_face;
+        a.lhalo = l->aux;
+        for (int mu = 0; mu < 4; mu++) a.lhoff[mu] = l->lhoff[mu];
+        CUDA_TRY(cudaEventRecord(c->ev_in, s), "cudaEventRecord");
+        CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->ev_in, 0), "cudaStreamWaitEvent");
+        CUDA_TRY(launch_pack(l->prec, c->nvec, in->base, c->send_buf, a.g, c->comm_stream), "halo pack");
+        {
+            std::string err;
+            r = halo_exchange(c, ctx_plan(c, l->prec), c->comm_stream, err);
+            if (r != CD_OK) return fail(r, err);
+        }
+        CUDA_TRY(cudaEventRecord(c->ev_halo, c->comm_stream), "cudaEventRecord");
+        CUDA_TRY(launch_fgh(l->prec, a, s, false), "compressed dslash interior launch");
+        CUDA_TRY(cudaStreamWaitEvent(s, c->ev_halo, 0), "cudaStreamWaitEvent");
+        CUDA_TRY(launch_fgh_halo(l->prec, a, s), "compressed halo kernel");
         return CD_OK;
     }
     a.g = halo ? halo_geom(c, l->prec) : c->kg;

@@ -142,6 +142,7 @@ struct cd_links {
     int eo;           // 1: even-odd prepared: base = even sites [V/2][9], aux = odd [V/2][8] (X^-1 L_k)
     void *aux;        // eo: odd-site records
     void *tbuf;       // eo: odd half-field scratch t_o (fp32)
+    int64_t lhoff[4] = {0, 0, 0, 0};   // compressed + multi-rank: aux = link halo, dim mu's records at lhoff[mu]
 };
 
 struct cd_transfer {
@@ -175,6 +176,8 @@ struct ApplyArgs {
     int nvec;
     int dagger;
     int halo;              // 1: skip remote hops, face sites -> scratch
+    const void *lhalo;     // compressed links, multi-rank: the -mu neighbours' x_mu = L-1 forward records
+    int64_t lhoff[4];      // byte offset of dim mu's records in lhalo
 };
 
 constexpr int CLUSTER_CHAIN_ID = 1000;   // apply_chain variant: whole lattice in one cluster
@@ -223,7 +226,11 @@ struct EoApply {              // one even-odd Schur apply (coarse_dslash_apply_e
 cudaError_t launch_eo_apply(int nvec, const EoApply &e);
 cudaError_t launch_fgh(cd_precision p, const ApplyArgs &a, cudaStream_t s, bool pdl);
 cudaError_t launch_compress(cd_precision p, int nv, const void *full, void *comp, int64_t nsites, cudaStream_t s);
-cudaError_t launch_hermdev(cd_precision p, int nv, const void *full, const KGeom &g, float *dev, cudaStream_t s);
+cudaError_t launch_hermdev(cd_precision p, int nv, const void *full, const KGeom &g, float *dev, cudaStream_t s,
+                           const void *lhalo = nullptr, const int64_t *lhoff = nullptr);
+cudaError_t launch_fgh_halo(cd_precision p, const ApplyArgs &a, cudaStream_t s);
+cudaError_t launch_lhalo_pack(cd_precision p, int nv, const void *comp, void *send, const KGeom &g, const int64_t *off,
+                              cudaStream_t s);
 // multi-RHS halo: receive buffer in the tensor-core wire layout (per split dim: block A = the
 // x_mu = L-1 face records for the +mu neighbour, block B = the x_mu = 0 face, each [face f][rb])
 struct MrhsHalo {

@@ -414,6 +414,7 @@ __global__ void __launch_bounds__(288, NV == 24 ? 3 : 2) dslash_fgh(ApplyArgs a)
     int x[4];
     decode(a.g, site, x);
     const bool fwd = (k == 8) || !(k & 1);
+    const bool remote = a.halo && remote_hop(a.g, x, k);   // added by dslash_fgh_halo
     // forward / X hop: own record; backward hop: forward record of the -mu neighbour
     const int msite = fwd ? site : neighbour(a.g, x, site, k);
     const int crec = (k == 8) ? 0 : 1 + (k >> 1);
@@ -422,7 +423,8 @@ __global__ void __launch_bounds__(288, NV == 24 ? 3 : 2) dslash_fgh(ApplyArgs a)
     const int il = lane & 15, gj = lane >> 4;             // backward mapping: (row i, j group)
     uint4 Lc[RG][Q::C];
     uint2 Mc[TJ];
-    if (fwd) {
+    if (remote) {
+    } else if (fwd) {
 #pragma unroll
         for (int g = 0; g < RG; g++)
 #pragma unroll
@@ -439,12 +441,15 @@ __global__ void __launch_bounds__(288, NV == 24 ? 3 : 2) dslash_fgh(ApplyArgs a)
     pdl_wait();
     for (int t = threadIdx.x; t < 9 * Q::VCH; t += 288) {
         const int kk = t / Q::VCH, e = t - kk * Q::VCH;
+        if (a.halo && remote_hop(a.g, x, kk)) continue;
         const int nb = neighbour(a.g, x, site, kk);
         *reinterpret_cast<uint4 *>(vs + kk * Q::VREC + e * 16) = ld_nc(in + (size_t)nb * Q::VREC + e * 16);
     }
     __syncthreads();
     const float2 *vk = reinterpret_cast<const float2 *>(vs + k * Q::VREC);
-    if (fwd) {
+    if (remote) {
+        if (lane < ROWS) part[warp][lane] = make_float2(0.0f, 0.0f);
+    } else if (fwd) {
 #pragma unroll
         for (int g = 0; g < RG; g++) {
             float re = 0.0f, im = 0.0f;
@@ -490,6 +495,10 @@ __global__ void __launch_bounds__(288, NV == 24 ? 3 : 2) dslash_fgh(ApplyArgs a)
             yi += part[w][threadIdx.x].y;
         }
         const int row = rb * ROWS + threadIdx.x;
+        if (a.halo && is_face<CD_FP32, NV>(a.g, x)) {   // partial for dslash_fgh_halo (no output sign yet)
+            a.scratch[(size_t)site * Q::N + row] = make_float2(yr, yi);
+            return;
+        }
         const float sg = (a.dagger && row >= NV) ? -1.0f : 1.0f;
         reinterpret_cast<float2 *>(static_cast<unsigned char *>(a.out) + (size_t)site * Q::VREC)[row] =
             make_float2(sg * yr, sg * yi);
@@ -519,6 +528,7 @@ __global__ void __launch_bounds__(288, 3) dslash_fgh16(ApplyArgs a)
     int x[4];
     decode(a.g, site, x);
     const bool fwd = (k == 8) || !(k & 1);
+    const bool remote = a.halo && remote_hop(a.g, x, k);   // added by dslash_fgh_halo
     const int msite = fwd ? site : neighbour(a.g, x, site, k);
     const int crec = (k == 8) ? 0 : 1 + (k >> 1);
     const unsigned char *m = links + ((size_t)msite * 5 + crec) * Q::MREC;
@@ -526,7 +536,8 @@ __global__ void __launch_bounds__(288, 3) dslash_fgh16(ApplyArgs a)
     const int ic = lane & 3, gj = lane >> 2;   // backward: (4 columns i, j group)
     uint4 Lc[RG][Q::C];
     uint4 Mc[TJ];
-    if (fwd) {
+    if (remote) {
+    } else if (fwd) {
 #pragma unroll
         for (int g = 0; g < RG; g++)
 #pragma unroll
@@ -537,18 +548,21 @@ __global__ void __launch_bounds__(288, 3) dslash_fgh16(ApplyArgs a)
         for (int t = 0; t < TJ; t++)   // rows j = gj + 8t: 8 x 64-byte column strips per instruction
             Mc[t] = ld_stream(m + (size_t)(gj + 8 * t) * Q::ROWB + (rb * ROWS + 4 * ic) * 4);
     }
-    const float msc = ld_nc_f32(m + Q::MSCALE);
+    const float msc = remote ? 0.0f : ld_nc_f32(m + Q::MSCALE);
     pdl_trigger();
     pdl_wait();
     for (int t = threadIdx.x; t < 9 * Q::VCH; t += 288) {
         const int kk = t / Q::VCH, e = t - kk * Q::VCH;
+        if (a.halo && remote_hop(a.g, x, kk)) continue;
         const int nb = neighbour(a.g, x, site, kk);
         *reinterpret_cast<uint4 *>(vs + kk * Q::VREC + e * 16) = ld_nc(in + (size_t)nb * Q::VREC + e * 16);
     }
     __syncthreads();
     const unsigned char *vrec = vs + k * Q::VREC;
-    const float sc = msc * *reinterpret_cast<const float *>(vrec + Q::VSCALE);
-    if (fwd) {
+    const float sc = remote ? 0.0f : msc * *reinterpret_cast<const float *>(vrec + Q::VSCALE);
+    if (remote) {
+        if (lane < ROWS) part[warp][lane] = make_float2(0.0f, 0.0f);
+    } else if (fwd) {
 #pragma unroll
         for (int g = 0; g < RG; g++) {
             float ra = 0.f, rb2 = 0.f, ia = 0.f, ib = 0.f;
@@ -603,8 +617,10 @@ __global__ void __launch_bounds__(288, 3) dslash_fgh16(ApplyArgs a)
         }
         const int row = rb * ROWS + threadIdx.x;
         const float sg = (a.dagger && row >= NV) ? -1.0f : 1.0f;
-        a.ysplit[(size_t)site * Q::N + row] = make_float2(sg * yr, sg * yi);
+        if (a.halo && is_face<CD_FP16, NV>(a.g, x)) a.scratch[(size_t)site * Q::N + row] = make_float2(yr, yi);
+        else a.ysplit[(size_t)site * Q::N + row] = make_float2(sg * yr, sg * yi);
     }
+    if (a.halo && is_face<CD_FP16, NV>(a.g, x)) return;   // dslash_fgh_halo finishes (and quantises) it
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) last = (atomicAdd(&a.site_cnt[site], 1) == NRB - 1);
@@ -619,7 +635,8 @@ __global__ void __launch_bounds__(288, 3) dslash_fgh16(ApplyArgs a)
 
 // hermiticity deviation of fp16 links, on the dequantised values (payload x record scale)
 template <int NV>
-__global__ void links_herm_dev16_kernel(const unsigned char *full, KGeom g, float *dev)
+__global__ void links_herm_dev16_kernel(const unsigned char *full, KGeom g, float *dev, const unsigned char *lhalo,
+                                   int64_t o0, int64_t o1, int64_t o2, int64_t o3)
 {
     using Q = Cfg<CD_FP16, NV>;
     const int site = blockIdx.x >> 2, mu = blockIdx.x & 3;
@@ -627,7 +644,15 @@ __global__ void links_herm_dev16_kernel(const unsigned char *full, KGeom g, floa
     decode(g, site, x);
     const int nb = neighbour(g, x, site, 2 * mu + 1);
     const unsigned char *Br = full + ((size_t)site * 9 + 2 * mu + 1) * Q::MREC;
-    const unsigned char *Fr = full + ((size_t)nb * 9 + 2 * mu) * Q::MREC;
+    const unsigned char *frec = full + ((size_t)nb * 9 + 2 * mu) * Q::MREC;
+    if (lhalo != nullptr && ((g.split >> mu) & 1) && x[mu] == 0) {   // the -mu neighbour is remote: link halo
+        const int f = mu == 0 ? (x[3] * g.L[2] + x[2]) * g.L[1] + x[1]
+                    : mu == 1 ? (x[3] * g.L[2] + x[2]) * g.L[0] + x[0]
+                    : mu == 2 ? (x[3] * g.L[1] + x[1]) * g.L[0] + x[0]
+                              : (x[2] * g.L[1] + x[1]) * g.L[0] + x[0];
+        frec = lhalo + (mu == 0 ? o0 : mu == 1 ? o1 : mu == 2 ? o2 : o3) + (size_t)f * Q::MREC;
+    }
+    const unsigned char *Fr = frec;
     const __half2 *B = reinterpret_cast<const __half2 *>(Br);
     const __half2 *F = reinterpret_cast<const __half2 *>(Fr);
     const float sb = *reinterpret_cast<const float *>(Br + Q::MSCALE), sf = *reinterpret_cast<const float *>(Fr + Q::MSCALE);
@@ -647,6 +672,134 @@ __global__ void links_herm_dev16_kernel(const unsigned char *full, KGeom g, floa
     if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int *>(dev), __float_as_int(mx));
 }
 
+// Multi-rank compressed operator: one CTA per face site adds the remote hops to the partial of the
+// interior kernel.  Forward remote hop (x_mu = L-1): own compressed record x the vector from
+// receive block B; backward remote hop (x_mu = 0): the -mu neighbour's forward record from the
+// one-time link halo (transposed, tau3) x the vector from receive block A.  Then the final store
+// (fp16: whole-site quantisation).
+template <cd_precision P, int NV>
+__global__ void __launch_bounds__(32 * (2 * NV / Cfg<P, NV>::R)) dslash_fgh_halo(ApplyArgs a)
+{
+    using Q = Cfg<P, NV>;
+    constexpr int NWARP = Q::N / Q::R;
+    constexpr int PREC = Q::F16 ? 4 * Q::N : 8 * Q::N;   // vector wire payload record
+    __shared__ float red[32];
+    const int site = a.face_sites[blockIdx.x];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r = lane / Q::D, d = lane % Q::D;
+    const int row = warp * Q::R + r;
+    const unsigned char *links = static_cast<const unsigned char *>(a.links);
+    const unsigned char *recv = static_cast<const unsigned char *>(a.recv);
+    const unsigned char *lh = static_cast<const unsigned char *>(a.lhalo);
+    int x[4];
+    decode(a.g, site, x);
+    float re = 0.0f, im = 0.0f;
+    for (int k = 0; k < 8; k++) {
+        if (!remote_hop(a.g, x, k)) continue;
+        const int mu = k >> 1;
+        const int blk = (k & 1) ? 0 : 1;
+        const int f = mu == 0 ? (x[3] * a.g.L[2] + x[2]) * a.g.L[1] + x[1]
+                    : mu == 1 ? (x[3] * a.g.L[2] + x[2]) * a.g.L[0] + x[0]
+                    : mu == 2 ? (x[3] * a.g.L[1] + x[1]) * a.g.L[0] + x[0]
+                              : (x[2] * a.g.L[1] + x[1]) * a.g.L[0] + x[0];
+        const unsigned char *vrec = recv + a.g.blk_off[mu][blk] + (size_t)f * PREC;
+        float vsc = 1.0f;
+        if constexpr (Q::F16)
+            vsc = *reinterpret_cast<const float *>(recv + a.g.blk_off[mu][blk] + (size_t)a.g.F[mu] * PREC + (size_t)f * 4);
+        if (!(k & 1)) {   // forward: rows of the own record 1 + mu
+            const unsigned char *m = links + ((size_t)site * 5 + 1 + mu) * Q::MREC;
+            if constexpr (P == CD_FP32) {
+#pragma unroll
+                for (int c = 0; c < Q::C; c++) {
+                    const int q = d + Q::D * c;
+                    uint4 vq = ld_nc(vrec + q * 16);
+                    if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<false>(vq);
+                    cmac2(ld_nc(m + row * Q::ROWB + q * 16), vq, re, im);
+                }
+            } else {
+                float ra = 0.f, rb = 0.f, ia = 0.f, ib = 0.f;
+#pragma unroll
+                for (int c = 0; c < Q::C; c++) {
+                    const int q = d + Q::D * c;
+                    uint4 vq = ld_nc(vrec + q * 16);
+                    if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<true>(vq);
+                    hmac4(ld_nc(m + row * Q::ROWB + q * 16), vq, ra, rb, ia, ib);
+                }
+                const float sc = ld_nc_f32(m + Q::MSCALE) * vsc;
+                re = fmaf(ra - rb, sc, re);
+                im = fmaf(ia + ib, sc, im);
+            }
+        } else {          // backward: column `row` of the neighbour's forward record, tau3 on both sides
+            const unsigned char *m = lh + a.lhoff[mu] + (size_t)f * Q::MREC;
+            const float si = row >= NV ? -1.0f : 1.0f;
+            float br = 0.0f, bi = 0.0f;
+            if constexpr (P == CD_FP32) {
+                for (int j = d; j < Q::N; j += Q::D) {
+                    const float2 mm = __ldg(reinterpret_cast<const float2 *>(m + (size_t)j * Q::ROWB) + row);
+                    float2 u = __ldg(reinterpret_cast<const float2 *>(vrec) + j);
+                    if ((j >= NV) != (a.dagger && j >= NV)) u = make_float2(-u.x, -u.y);
+                    br = fmaf(mm.x, u.x, fmaf(mm.y, u.y, br));
+                    bi = fmaf(mm.x, u.y, fmaf(-mm.y, u.x, bi));
+                }
+            } else {
+                float ra = 0.f, rb = 0.f, ia = 0.f, ib = 0.f;
+                for (int j = d; j < Q::N; j += Q::D) {
+                    const uint32_t mm = __ldg(reinterpret_cast<const uint32_t *>(m + (size_t)j * Q::ROWB) + row);
+                    uint32_t u = __ldg(reinterpret_cast<const uint32_t *>(vrec) + j);
+                    if ((j >= NV) != (a.dagger && j >= NV)) u ^= 0x80008000u;
+                    hmac1(mm, u, ra, rb, ia, ib);
+                }
+                const float sc = ld_nc_f32(m + Q::MSCALE) * vsc;
+                br = (ra + rb) * sc;
+                bi = (ia - ib) * sc;
+            }
+            re += si * br;
+            im += si * bi;
+        }
+    }
+#pragma unroll
+    for (int o = Q::D / 2; o >= 1; o >>= 1) {
+        re += shfl_xor(re, o);
+        im += shfl_xor(im, o);
+    }
+    const bool owner = (d == 0);
+    if (owner) {
+        const float2 p = a.scratch[(size_t)site * Q::N + row];
+        re += p.x;
+        im += p.y;
+    }
+    const float sg = (a.dagger && row >= NV) ? -1.0f : 1.0f;
+    store_site<P, NV>(static_cast<unsigned char *>(a.out), site, row, owner, sg * re, sg * im, red, 32 * NWARP, -1);
+}
+
+// link halo send: forward record L_{2mu}(x) of every x_mu = L-1 face site (compressed record 1 + mu)
+template <cd_precision P, int NV>
+__global__ void lhalo_pack_kernel(const unsigned char *comp, unsigned char *send, KGeom g, int4 pairs, int64_t o0,
+                                  int64_t o1, int64_t o2, int64_t o3)
+{
+    using Q = Cfg<P, NV>;
+    const int pi = blockIdx.y;
+    const int mu = pi == 0 ? pairs.x : (pi == 1 ? pairs.y : (pi == 2 ? pairs.z : pairs.w));
+    const int64_t off = mu == 0 ? o0 : (mu == 1 ? o1 : (mu == 2 ? o2 : o3));
+    const int L = sel4(g.L, mu);
+    const int F = g.V / L;
+    for (int f = blockIdx.x; f < F; f += gridDim.x) {
+        int x[4];
+        // face index f: lexicographic over the other three dims (as dslash_fgh_halo)
+        if (mu == 0) { x[1] = f % g.L[1]; x[2] = (f / g.L[1]) % g.L[2]; x[3] = f / (g.L[1] * g.L[2]); }
+        else if (mu == 1) { x[0] = f % g.L[0]; x[2] = (f / g.L[0]) % g.L[2]; x[3] = f / (g.L[0] * g.L[2]); }
+        else if (mu == 2) { x[0] = f % g.L[0]; x[1] = (f / g.L[0]) % g.L[1]; x[3] = f / (g.L[0] * g.L[1]); }
+        else { x[0] = f % g.L[0]; x[1] = (f / g.L[0]) % g.L[1]; x[2] = f / (g.L[0] * g.L[1]); }
+        if (mu == 0) x[0] = L - 1;
+        else if (mu == 1) x[1] = L - 1;
+        else if (mu == 2) x[2] = L - 1;
+        else x[3] = L - 1;
+        const uint4 *src = reinterpret_cast<const uint4 *>(comp + ((size_t)encode(g, x) * 5 + 1 + mu) * Q::MREC);
+        uint4 *dst = reinterpret_cast<uint4 *>(send + off + (size_t)f * Q::MREC);
+        for (int e = threadIdx.x; e < Q::MREC / 16; e += blockDim.x) dst[e] = src[e];
+    }
+}
+
 // full links -> compressed records (X, L_0, L_2, L_4, L_6 per site), one CTA per output record
 template <cd_precision P, int NV>
 __global__ void links_compress_kernel(const unsigned char *full, unsigned char *comp, int64_t nrec)
@@ -664,7 +817,8 @@ __global__ void links_compress_kernel(const unsigned char *full, unsigned char *
 // max |L_{2mu+1}(x) - tau3 L_{2mu}(x-mu)^H tau3| over the lattice (fp32 links): the validity check
 // of the compression.  One CTA per (site, mu); result via an atomic max on the float bits (>= 0).
 template <int NV>
-__global__ void links_herm_dev_kernel(const unsigned char *full, KGeom g, float *dev)
+__global__ void links_herm_dev_kernel(const unsigned char *full, KGeom g, float *dev, const unsigned char *lhalo,
+                                   int64_t o0, int64_t o1, int64_t o2, int64_t o3)
 {
     using Q = Cfg<CD_FP32, NV>;
     const int site = blockIdx.x >> 2, mu = blockIdx.x & 3;
@@ -672,7 +826,15 @@ __global__ void links_herm_dev_kernel(const unsigned char *full, KGeom g, float 
     decode(g, site, x);
     const int nb = neighbour(g, x, site, 2 * mu + 1);
     const float2 *B = reinterpret_cast<const float2 *>(full + ((size_t)site * 9 + 2 * mu + 1) * Q::MREC);
-    const float2 *F = reinterpret_cast<const float2 *>(full + ((size_t)nb * 9 + 2 * mu) * Q::MREC);
+    const unsigned char *frec = full + ((size_t)nb * 9 + 2 * mu) * Q::MREC;
+    if (lhalo != nullptr && ((g.split >> mu) & 1) && x[mu] == 0) {   // the -mu neighbour is remote: link halo
+        const int f = mu == 0 ? (x[3] * g.L[2] + x[2]) * g.L[1] + x[1]
+                    : mu == 1 ? (x[3] * g.L[2] + x[2]) * g.L[0] + x[0]
+                    : mu == 2 ? (x[3] * g.L[1] + x[1]) * g.L[0] + x[0]
+                              : (x[2] * g.L[1] + x[1]) * g.L[0] + x[0];
+        frec = lhalo + (mu == 0 ? o0 : mu == 1 ? o1 : mu == 2 ? o2 : o3) + (size_t)f * Q::MREC;
+    }
+    const float2 *F = reinterpret_cast<const float2 *>(frec);
     float m = 0.0f;
     for (int e = threadIdx.x; e < Q::N * Q::N; e += blockDim.x) {
         const int i = e / Q::N, j = e - i * Q::N;
@@ -1559,14 +1721,39 @@ cudaError_t launch_pack_t(const void *field, void *send, const KGeom &g, cudaStr
             static_cast<const unsigned char *>(full), static_cast<unsigned char *>(comp), nsites * 5);             \
         return cudaGetLastError();                                                                                \
     }                                                                                                             \
-    cudaError_t launch_hermdev_##TAG(const void *full, const KGeom &g, float *dev, cudaStream_t s)                \
+    cudaError_t launch_hermdev_##TAG(const void *full, const KGeom &g, float *dev, cudaStream_t s,                \
+                                     const void *lhalo, const int64_t *lo)                                        \
     {                                                                                                             \
         count_launch();                                                                                           \
         const unsigned char *fu = static_cast<const unsigned char *>(full);                                      \
+        const unsigned char *lh = static_cast<const unsigned char *>(lhalo);                                     \
+        const int64_t z[4] = {0, 0, 0, 0};                                                                        \
+        const int64_t *o = lo ? lo : z;                                                                           \
         if constexpr (P == CD_FP32)                                                                               \
-            links_herm_dev_kernel<NV><<<(unsigned)(g.V * 4), 256, 0, s>>>(fu, g, dev);                            \
+            links_herm_dev_kernel<NV><<<(unsigned)(g.V * 4), 256, 0, s>>>(fu, g, dev, lh, o[0], o[1], o[2], o[3]); \
         else                                                                                                      \
-            links_herm_dev16_kernel<NV><<<(unsigned)(g.V * 4), 256, 0, s>>>(fu, g, dev);                          \
+            links_herm_dev16_kernel<NV><<<(unsigned)(g.V * 4), 256, 0, s>>>(fu, g, dev, lh, o[0], o[1], o[2], o[3]); \
+        return cudaGetLastError();                                                                                \
+    }                                                                                                             \
+    cudaError_t launch_fgh_halo_##TAG(const ApplyArgs &a, cudaStream_t s)                                         \
+    {                                                                                                             \
+        if (a.n_face == 0) return cudaSuccess;                                                                    \
+        count_launch();                                                                                           \
+        dslash_fgh_halo<P, NV><<<(unsigned)a.n_face, 32 * (2 * NV / Cfg<P, NV>::R), 0, s>>>(a);                    \
+        return cudaGetLastError();                                                                                \
+    }                                                                                                             \
+    cudaError_t launch_lhalo_pack_##TAG(const void *comp, void *send, const KGeom &g, const int64_t *o,           \
+                                        cudaStream_t s)                                                           \
+    {                                                                                                             \
+        int4 pairs = make_int4(0, 0, 0, 0);                                                                       \
+        int np = 0;                                                                                               \
+        for (int mu = 0; mu < 4; mu++)                                                                            \
+            if ((g.split >> mu) & 1) (&pairs.x)[np++] = mu;                                                       \
+        if (np == 0) return cudaSuccess;                                                                          \
+        count_launch();                                                                                           \
+        lhalo_pack_kernel<P, NV><<<dim3(296, np), 256, 0, s>>>(static_cast<const unsigned char *>(comp),          \
+                                                               static_cast<unsigned char *>(send), g, pairs, o[0], \
+                                                               o[1], o[2], o[3]);                                 \
         return cudaGetLastError();                                                                                \
     }                                                                                                             \
     cudaError_t launch_chain_##TAG(int id, const ApplyArgs &a, int n, unsigned base, cudaStream_t s, int sms,     \

@@ -18,11 +18,14 @@ ap.add_argument("--nvec", type=int, default=24)
 ap.add_argument("--reps", type=int, default=200)
 ap.add_argument("--json", default=None)
 ap.add_argument("--prec", default="fp32")
+ap.add_argument("--mask", type=int, default=0, help="CD_OPT_HALO_SELF_MASK (multi-rank path on one GPU)")
 a = ap.parse_args()
 dims = tuple(a.dims)
 V = dims[0] * dims[1] * dims[2] * dims[3]
 N = 2 * a.nvec
 ctx = cd.Context(dims, a.nvec)
+if a.mask:
+    ctx.set_option(cd.CD_OPT_HALO_SELF_MASK, a.mask)
 L = ctx.links_generate(a.prec, kind="hermitian", scale_log2=-4)
 C, dev = L.compress_hermitian()
 x, y = ctx.field(a.prec), ctx.field(a.prec)
@@ -49,7 +52,7 @@ t_full, t_comp = timed(L), timed(C)
 mb9 = perfmodel.metric_bytes_per_site(a.nvec, a.prec) * V
 mrec, vrec = (8 * N * N, 8 * N) if a.prec == "fp32" else (4 * N * N + 16, 4 * N + 16)
 mb5 = (5 * mrec + 9 * vrec) * V
-row = {"dims": dims, "nvec": a.nvec, "prec": a.prec, "max_dev": dev, "us_full": round(t_full, 2), "us_compressed": round(t_comp, 2),
+row = {"dims": dims, "nvec": a.nvec, "prec": a.prec, "halo_mask": a.mask, "max_dev": dev, "us_full": round(t_full, 2), "us_compressed": round(t_comp, 2),
        "speedup": round(t_full / t_comp, 3), "full_GBs": round(mb9 / t_full / 1e3, 1),
        "compressed_GBs_5matrix_bytes": round(mb5 / t_comp / 1e3, 1),
        "compressed_GBs_9matrix_equiv": round(mb9 / t_comp / 1e3, 1),

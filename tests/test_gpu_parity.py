@@ -716,3 +716,25 @@ def test_apply_mrhs_halo_self_exchange(mask, dims, nvec):
         got = fout.export()
         ref = np.stack([op(dims, Lh, vs[r]) for r in range(nrhs)])
         assert max(rel_l2(got[r], ref[r]) for r in range(nrhs)) <= 5e-3, dag
+
+
+@pytest.mark.parametrize("prec,tol", [("fp32", 1e-5), ("fp16", 5e-3)])
+@pytest.mark.parametrize("mask,dims,nvec", [(0b1000, (2, 2, 2, 4), 24), (0b0101, (4, 2, 3, 2), 24),
+                                            (0b1111, (2, 2, 2, 2), 24), (0b1000, (2, 3, 2, 4), 32)])
+def test_compressed_links_halo_self_exchange(mask, dims, nvec, prec, tol):
+    """Compressed links on the multi-rank path (one GPU, self exchange): the one-time link halo
+    carries the -mu neighbours' forward records, the vector halo the usual faces; the deviation
+    check sees the remote pairs through the link halo (exactly 0 on hermitian links)."""
+    N = 2 * nvec
+    Lh = synth.links(dims, N, kind="hermitian")
+    v = synth.vector(dims, N)
+    ctx = cd.Context(dims, nvec)
+    ctx.set_option(cd.CD_OPT_HALO_SELF_MASK, mask)
+    C, dev = ctx.links_upload(Lh, prec).compress_hermitian()
+    assert dev == 0.0
+    fin, fout = ctx.field(prec), ctx.field(prec)
+    fin.import_(v)
+    C.apply(fout, fin)
+    assert rel_l2(fout.export(), oracle.apply(dims, Lh, v)) <= tol
+    C.apply_dagger(fout, fin)
+    assert rel_l2(fout.export(), oracle.adjoint(dims, Lh, v)) <= tol

@@ -46,10 +46,18 @@ for prec in ("fp32", "fp16"):
         mx.generate()
         ml.apply_mrhs(my, mx)
         ml.apply_mrhs(mx, my, dagger=True)
-    if which in ("all", "compressed") and prec == "fp32":
+    if which in ("all", "compressed"):
         C, _ = L.compress_hermitian()
         ctx.set_option(cd.CD_OPT_VARIANT, -1)
         C.apply(b, a)
+        C.apply_dagger(a, b)
+        cc = cd.Context((2, 2, 2, 4), 24)
+        cc.set_option(cd.CD_OPT_HALO_SELF_MASK, 0b1001)
+        Cc, _ = cc.links_generate(prec, kind="hermitian", scale_log2=-4).compress_hermitian()
+        ca, cb = cc.field(prec), cc.field(prec)
+        ca.generate()
+        Cc.apply(cb, ca)
+        Cc.apply_dagger(ca, cb)
     if which in ("all", "eo") and prec == "fp32":
         E = L.prepare_eo()
         xe, ye = ctx.field("fp32", parity=0), ctx.field("fp32", parity=0)
