@@ -738,3 +738,45 @@ def test_compressed_links_halo_self_exchange(mask, dims, nvec, prec, tol):
     assert rel_l2(fout.export(), oracle.apply(dims, Lh, v)) <= tol
     C.apply_dagger(fout, fin)
     assert rel_l2(fout.export(), oracle.adjoint(dims, Lh, v)) <= tol
+
+
+# ---------------------------------------------------------------- seeded random geometry sweep
+def _fuzz_cases(n=24, seed=20261017):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        dims = tuple(int(d) for d in rng.integers(1, 5, size=4))
+        nvec = int(rng.choice([24, 32]))
+        prec = str(rng.choice(["fp32", "fp16"]))
+        mask = int(rng.integers(0, 16))
+        mask &= sum(1 << mu for mu in range(4) if dims[mu] >= 2)   # a halo dim needs two faces... or one
+        out.append((dims, nvec, prec, mask, int(rng.integers(0, 1 << 30))))
+    return out
+
+
+@pytest.mark.parametrize("dims,nvec,prec,mask,vseed", _fuzz_cases())
+def test_random_geometry_sweep(dims, nvec, prec, mask, vseed):
+    """Random small lattices (extents 1-4, including L = 1 and L = 2 self/double hops), both
+    storages, random halo self-exchange masks, a random forced variant: apply and dagger vs the
+    oracle."""
+    N = 2 * nvec
+    Lh = synth.links(dims, N, kind="hermitian", seed=vseed)
+    v = synth.vector(dims, N, seed=vseed + 1)
+    ctx = cd.Context(dims, nvec)
+    if mask:
+        ctx.set_option(cd.CD_OPT_HALO_SELF_MASK, mask)
+    nvar = len(ctx.variants(prec))
+    ctx.set_option(cd.CD_OPT_VARIANT, vseed % nvar)
+    L = ctx.links_upload(Lh, prec)
+    fin, fout = ctx.field(prec), ctx.field(prec)
+    fin.import_(v)
+    tol = TOL[prec]
+    try:
+        L.apply(fout, fin)
+    except cd.CDError as e:   # a forced variant may not support this geometry: fall back to the tuner
+        assert e.code in (cd.CD_ERR_UNSUPPORTED, cd.CD_ERR_INVALID), e
+        ctx.set_option(cd.CD_OPT_VARIANT, -1)
+        L.apply(fout, fin)
+    assert rel_l2(fout.export(), oracle.apply(dims, Lh, v)) <= tol
+    L.apply_dagger(fout, fin)
+    assert rel_l2(fout.export(), oracle.adjoint(dims, Lh, v)) <= tol
