@@ -291,6 +291,10 @@ class Context:
     def chosen_variant(self, prec, dagger=False):
         return lib.cd_context_chosen_variant(self.handle, PREC[prec], int(bool(dagger)))
 
+    def chosen_chain_variant(self, prec, dagger=False):
+        """apply_chain's tuned variant id (see cd_context_chosen_variant), -1 if not tuned yet."""
+        return lib.cd_context_chosen_variant(self.handle, PREC[prec], 2 + int(bool(dagger)))
+
     def field(self, prec="fp32", torch_memory=True, nrhs=1, parity=None):
         return Field(self, prec, torch_memory, nrhs, parity)
 

@@ -562,7 +562,7 @@ int cd_context_chosen_variant(const cd_context *c, cd_precision p, int dagger)
     if (!c) return -1;
     auto *cc = const_cast<cd_context *>(c);
     std::lock_guard<std::mutex> lk(cc->mu);
-    auto it = c->chosen.find(TuneKey{(int)p, dagger ? 1 : 0});
+    auto it = c->chosen.find(TuneKey{(int)p, dagger >= 2 ? (dagger & 3) : (dagger ? 1 : 0)});
     return it == c->chosen.end() ? -1 : it->second;
 }
 
@@ -1361,6 +1361,10 @@ int coarse_dslash_apply_chain(const cd_links *l, cd_field *x, cd_field *y, int n
     a.llbuf = c->llbuf;
     a.poll_ns = 0;
     if (const char *ev = getenv("CD_POLL_NS")) a.poll_ns = atoi(ev);
+    a.poll_d0 = 300;   // measured best at 2^4 (profiles/r01/chain_llreg.jsonl)
+    a.poll_d1 = 0;
+    if (const char *ev = getenv("CD_POLL_D0")) a.poll_d0 = atoi(ev);
+    if (const char *ev = getenv("CD_POLL_D1")) a.poll_d1 = atoi(ev);
     const cd_precision p = l->prec;
     const TuneKey key{(int)p, 2 + a.dagger};
     int id = -1;
@@ -1389,6 +1393,7 @@ int coarse_dslash_apply_chain(const cd_links *l, cd_field *x, cd_field *y, int n
         float best = 1e30f;
         const int trial = 64;
         std::vector<int> cands{CLUSTER_CHAIN_ID};
+        for (int i = 0; i < kNumLLReg; i++) cands.push_back(LLREG_CHAIN_ID0 + 1 + i);
         for (int v = 0; v < variant_count(p, c->nvec); v++) {
             cands.push_back(LL_CHAIN_ID0 + v);
             cands.push_back(v);
@@ -1416,7 +1421,21 @@ int coarse_dslash_apply_chain(const cd_links *l, cd_field *x, cd_field *y, int n
         std::lock_guard<std::mutex> lk(c->mu);
         c->chosen[key] = id;
     }
+    const char *tf = getenv("CD_CHAIN_TRACE");   // diagnostic only: clock64 events of CTA 0 (LL-register chain)
+    if (tf && id > LLREG_CHAIN_ID0 && id < LLREG_CHAIN_ID0 + 100)
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void **>(&a.trace), 40 * 1024 * sizeof(long long), s), "trace");
+    if (a.trace) CUDA_TRY(cudaMemsetAsync(a.trace, 0, 40 * 1024 * sizeof(long long), s), "trace");
     cudaError_t e = chain_launch(c, p, id, a, n, s);
+    if (a.trace) {
+        std::vector<long long> h(40 * 1024);
+        cudaMemcpyAsync(h.data(), a.trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        cudaFreeAsync(a.trace, s);
+        if (FILE *f = fopen(tf, "wb")) {
+            fwrite(h.data(), sizeof(long long), h.size(), f);
+            fclose(f);
+        }
+    }
     if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorNotSupported) {
         cudaGetLastError();
         return fail(CD_ERR_UNSUPPORTED, "chain variant does not fit co-resident / not a chain variant");

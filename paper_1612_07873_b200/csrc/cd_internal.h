@@ -171,17 +171,22 @@ struct ApplyArgs {
     int *site_cnt;         // fp16 row-split fg: per-site arrival counters (zero between launches)
     unsigned *chain_cnt;   // chain kernel: monotonic per-site completion counters
     void *llbuf;           // LL chain: 2 x V LL records (epoch-tagged payload words)
-    int poll_ns;           // LL chain: __nanosleep between unsuccessful polls (0 = spin)
+    int poll_ns;           // LL chain: __nanosleep between unsuccessful polls (0 = spin); LL-register: before the first poll
+    int poll_d0;           // LL-register chain: first poll of an apply no earlier than this many cycles after its start
+    int poll_d1;           // LL-register chain: cycles between unsuccessful polls
     KGeom g;
     int nvec;
     int dagger;
     int halo;              // 1: skip remote hops, face sites -> scratch
     const void *lhalo;     // compressed links, multi-rank: the -mu neighbours' x_mu = L-1 forward records
     int64_t lhoff[4];      // byte offset of dim mu's records in lhalo
+    long long *trace;      // LL-register chain diagnostic (CD_CHAIN_TRACE): clock64 events of CTA 0
 };
 
 constexpr int CLUSTER_CHAIN_ID = 1000;   // apply_chain variant: whole lattice in one cluster
 constexpr int LL_CHAIN_ID0 = 2000;       // apply_chain variants 2000 + fg id: LL-protocol chain
+constexpr int LLREG_CHAIN_ID0 = 3000;    // apply_chain variants 3001 + i: LL-register chain (fp32), i < kNumLLReg
+constexpr int kNumLLReg = 6;
 
 int variant_count(cd_precision p, int nvec);
 const char *variant_name(cd_precision p, int nvec, int id);

@@ -1183,6 +1183,239 @@ __global__ void __launch_bounds__(FgCfg<P, NV, KW, WR>::THREADS) dslash_llchain(
     }
 }
 
+// ------------------------------------------------------------------ LL-register chain (2^4 latency regime)
+// The LL protocol of dslash_llchain with the on-chip critical path cut down:
+//  * one warp per hop k (the paper's direction split) polls ITS OWN neighbour's LL
+//    record (lane-contiguous 16-B units, whole record) -- no CTA barrier before the math; a warp
+//    runs its chunk FMAs the moment its neighbour's record lands;
+//  * the hop partials meet in shared memory; the hop warps `bar.arrive` (non-blocking), warp 0
+//    alone `bar.sync`s, sums the 9 partials in the fixed hop order and stores the LL record;
+//  * GATE: the hop warps then wait (second named barrier) until warp 0 has ISSUED that store
+//    before they poll the next epoch -- spinning loads of the next epoch would otherwise sit in
+//    the SM's L1tex queue in front of warp 0's shared loads and LL store (the critical path;
+//    measured 440-1050 cycles of queueing without the gate);
+//  * REP: the writer stores its rows to REP replicas of the LL buffer and reader CTA b polls
+//    replica b % REP, so each 128-B line has REP x fewer pollers (a hot line is served by one L2
+//    slice; 108 warps poll each line per round at 2^4 with 12 CTAs per site).
+//  * ROWS rows per CTA (NRB = N / ROWS CTAs per site; ROWS = 6 gives 128 CTAs at 2^4 -- one
+//    per SM); WR = ceil(ROWS / 4) warps per hop, surplus rows computed on clamped data, unused.
+// Without GATE, the named barriers and the partial buffers alternate with t & 1: a hop warp
+// can run at most one apply ahead of warp 0 (its neighbour's epoch t+2 needs this site's epoch
+// t+1 record, which warp 0 writes after consuming the partials of apply t).
+// The per-row arithmetic (chunk partials, xor-shuffle over the dot split, hop sum from 0 in hop
+// order) is that of dslash_fg<kw=1>: the chain is bitwise equal to single applies of it.
+// fp32 storage (the fp16 format quantises a whole site, which one CTA of ROWS rows cannot).
+struct LLRDesc {
+    int rows, ld;   // rows per CTA, lanes per row (dot-product split)
+};
+constexpr LLRDesc kLLR[] = {{4, 8}, {8, 4}, {6, 4}, {8, 8}, {12, 4}, {16, 2}};
+constexpr int kNLLR = sizeof(kLLR) / sizeof(kLLR[0]);
+static_assert(kNLLR == kNumLLReg, "LL-register variant count");
+
+template <int NV, int ROWS, int LD>
+struct LLRegCfg {
+    static constexpr int N = 2 * NV;
+    static constexpr int LR = 32 / LD;               // rows per warp
+    static constexpr int LC = N / (2 * LD);          // 16-B chunks (2 complex) per lane per row
+    static constexpr int WR = (ROWS + LR - 1) / LR;  // warps per hop
+    static constexpr int NW = 9 * WR;
+    static constexpr int THREADS = 32 * NW;
+    static constexpr int NRB = N / ROWS;
+    static constexpr bool OK = (N % ROWS == 0) && (LC * LD * 2 == N) && NW <= 32 && ROWS <= 32;
+};
+
+__device__ __forceinline__ void spin_until(long long c)
+{
+    while (clock64() < c) {
+    }
+}
+
+template <int NV, int ROWS, int LD>
+__global__ void __launch_bounds__(LLRegCfg<NV, ROWS, LD>::THREADS) dslash_llreg(ApplyArgs a, int n, unsigned base)
+{
+    using Q = Cfg<CD_FP32, NV>;
+    using F = LLRegCfg<NV, ROWS, LD>;
+    using LL = LLCfg<CD_FP32, NV>;
+    constexpr int UPL = (LL::WP + 31) / 32;   // LL units per lane (whole record, lane-contiguous)
+    __shared__ float2 part[9][F::WR * F::LR];
+    __shared__ __align__(16) float2 vst[F::NW][Q::N];
+
+    const int site = blockIdx.x / F::NRB, rb = blockIdx.x - site * F::NRB;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wk = warp / F::WR, wr = warp - wk * F::WR;
+    const int r = lane / LD, d = lane % LD;
+    const int rowl = wr * F::LR + r;
+    const int row = rb * ROWS + (rowl < ROWS ? rowl : ROWS - 1);
+    const int k = kseq(wk);
+    unsigned char *const buf0 = const_cast<unsigned char *>(static_cast<const unsigned char *>(a.in));
+    unsigned char *const buf1 = static_cast<unsigned char *>(a.out);
+    unsigned char *const ll = reinterpret_cast<unsigned char *>(a.llbuf);
+    const size_t llhalf = (size_t)a.g.V * LL::REC;
+    long long *const tr = (a.trace && blockIdx.x == 0 && lane == 0) ? a.trace : nullptr;
+
+    int x[4];
+    decode(a.g, site, x);
+    const int nb = neighbour(a.g, x, site, k);
+    uint4 Lc[F::LC];
+    {
+        const unsigned char *m = static_cast<const unsigned char *>(a.links) + ((size_t)site * 9 + k) * Q::MREC;
+#pragma unroll
+        for (int c = 0; c < F::LC; c++) Lc[c] = ld_stream(m + row * Q::ROWB + (d + LD * c) * 16);
+    }
+    if (a.dagger) {   // tau3 on the input folded into the register-resident links (columns j >= Nvec)
+#pragma unroll
+        for (int c = 0; c < F::LC; c++)
+            if ((d + LD * c) * 2 >= NV) Lc[c] = neg_chunk<false>(Lc[c]);
+    }
+
+    for (int t = 0; t < n; t++) {
+        // trace (CD_CHAIN_TRACE, CTA 0, lane 0 of the wr == 0 warps): absolute clock64 per event,
+        // written at the end of the apply; row 4 * wk + e (e: 0 start, 1 record landed, 2 arrived
+        // at the partials barrier (hop warps) / its LDS returned (warp 0)), warp 0 also 36 summed,
+        // 37 LL store issued, 38 go barrier arrived, 39 trace written.  (BAR.SYNC defers blocking
+        // to the next dependent memory instruction, so warp 0's barrier time is read after a load.)
+        long long c_start = 0, c_data = 0, c_bar = 0, c_sum = 0, c_st = 0;
+        const long long c_start0 = clock64();
+        if (tr) c_start = c_start0;
+        uint4 vq[F::LC];
+        if (t == 0) {   // the input is ready at launch: ordinary format
+#pragma unroll
+            for (int c = 0; c < F::LC; c++) vq[c] = ld_nc(buf0 + (size_t)nb * Q::VREC + (d + LD * c) * 16);
+        } else {        // poll the neighbour's record of epoch base + t
+            const unsigned want = base + (unsigned)t;
+            const unsigned char *src = ll + (size_t)(t & 1) * llhalf + (size_t)nb * LL::REC;
+            uint4 u[UPL];
+            unsigned miss = 0;
+#pragma unroll
+            for (int i = 0; i < UPL; i++)
+                if (lane + 32 * i < LL::WP) miss |= 1u << i;
+            // Polls are cheap for the poller but not for the system: every poll of a hot line
+            // queues at its L2 slice in front of the writers' stores and the other pollers
+            // (measured: two rounds in flight per warp slow the chain by 10 %).  So the first
+            // poll waits until the record can plausibly have landed (poll_d0 cycles after this
+            // warp's start of the apply) and unsuccessful polls back off poll_d1 cycles.
+            if (a.poll_ns > 0) __nanosleep(a.poll_ns);
+            if (a.poll_d0 > 0) spin_until(c_start0 + a.poll_d0);
+            while (true) {
+#pragma unroll
+                for (int i = 0; i < UPL; i++)
+                    if (miss & (1u << i)) u[i] = ld_cg(src + (lane + 32 * i) * 16);
+#pragma unroll
+                for (int i = 0; i < UPL; i++)
+                    if ((miss & (1u << i)) && u[i].y == want && u[i].w == want) miss &= ~(1u << i);
+                if (!__any_sync(0xffffffffu, miss != 0u)) break;
+                if (a.poll_d1 > 0) spin_until(clock64() + a.poll_d1);
+            }
+#pragma unroll
+            for (int i = 0; i < UPL; i++)
+                if (lane + 32 * i < LL::WP)
+                    vst[warp][lane + 32 * i] = make_float2(__uint_as_float(u[i].x), __uint_as_float(u[i].z));
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < F::LC; c++) vq[c] = lds128(&vst[warp][2 * (d + LD * c)]);
+            __syncwarp();
+        }
+        if (tr) c_data = clock64();
+        float re = 0.0f, im = 0.0f;
+        {
+            float pr[F::LC], pi[F::LC];
+#pragma unroll
+            for (int c = 0; c < F::LC; c++) {
+                pr[c] = 0.0f;
+                pi[c] = 0.0f;
+                cmac2(Lc[c], vq[c], pr[c], pi[c]);
+            }
+#pragma unroll
+            for (int c = 0; c < F::LC; c++) { re += pr[c]; im += pi[c]; }
+        }
+#pragma unroll
+        for (int m = LD / 2; m >= 1; m >>= 1) {
+            re += shfl_xor(re, m);
+            im += shfl_xor(im, m);
+        }
+        if (d == 0) part[wk][rowl] = make_float2(re, im);
+        if (warp != 0) {   // hop warps: arrive, then wait until warp 0 has issued the LL store
+            asm volatile("bar.arrive 1, %0;" ::"r"(F::THREADS) : "memory");
+            if (tr) c_bar = clock64();
+            asm volatile("bar.sync 2, %0;" ::"r"(F::THREADS) : "memory");
+            if (tr && wr == 0 && t < 1024) {
+                tr[(4 * wk + 0) * 1024 + t] = c_start;
+                tr[(4 * wk + 1) * 1024 + t] = c_data;
+                tr[(4 * wk + 2) * 1024 + t] = c_bar;
+            }
+            continue;
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(F::THREADS) : "memory");
+        if (lane < ROWS) {
+            float yr = 0.0f, yi = 0.0f;
+#pragma unroll
+            for (int w = 0; w < 9; w++) {
+                const float2 p = part[w][lane];
+                if (w == 0 && tr) c_bar = clock64();
+                yr += p.x;
+                yi += p.y;
+            }
+            const int orow = rb * ROWS + lane;
+            if (a.dagger && orow >= NV) yr = -yr, yi = -yi;
+            if (tr) c_sum = clock64();
+            const unsigned ep = base + (unsigned)t + 1;
+            reinterpret_cast<uint4 *>(ll + (size_t)((t + 1) & 1) * llhalf + (size_t)site * LL::REC)[orow] =
+                make_uint4(__float_as_uint(yr), ep, __float_as_uint(yi), ep);
+            if (t >= n - 2) {   // the caller sees the last two iterates (x / y ping-pong)
+                unsigned char *gout = (t & 1) ? buf0 : buf1;
+                reinterpret_cast<float2 *>(gout + (size_t)site * Q::VREC)[orow] = make_float2(yr, yi);
+            }
+        }
+        if (tr) c_st = clock64();
+        asm volatile("bar.arrive 2, %0;" ::"r"(F::THREADS) : "memory");
+        if (tr && t < 1024) {
+            const long long c_go = clock64();
+            tr[0 * 1024 + t] = c_start;
+            tr[1 * 1024 + t] = c_data;
+            tr[2 * 1024 + t] = c_bar;
+            tr[36 * 1024 + t] = c_sum;
+            tr[37 * 1024 + t] = c_st;
+            tr[38 * 1024 + t] = c_go;
+            tr[39 * 1024 + t] = clock64();
+        }
+    }
+}
+
+template <int NV, int I>
+cudaError_t launch_llreg_t(const ApplyArgs &a, int n, unsigned base, cudaStream_t s, int num_sms)
+{
+    constexpr LLRDesc D = kLLR[I];
+    using F = LLRegCfg<NV, D.rows, D.ld>;
+    if constexpr (!F::OK) {
+        return cudaErrorNotSupported;
+    } else {
+        auto fn = dslash_llreg<NV, D.rows, D.ld>;
+        const size_t smem = 0;
+        int per_sm = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, F::THREADS, smem);
+        if (e != cudaSuccess) return e;
+        if ((int64_t)a.g.V * F::NRB > (int64_t)per_sm * num_sms) return cudaErrorCooperativeLaunchTooLarge;
+        ApplyArgs aa = a;
+        int nn = n;
+        unsigned bb = base;
+        void *args[] = {&aa, &nn, &bb};
+        return launch_ex((const void *)fn, dim3((unsigned)(a.g.V * F::NRB)), dim3(F::THREADS), smem, s, false, args,
+                         true);
+    }
+}
+
+// LL-register chain variants: id LLREG_CHAIN_ID0 + 1 + index into kLLR
+template <cd_precision P, int NV, int I = 0>
+cudaError_t dispatch_llreg(int idx, const ApplyArgs &a, int n, unsigned base, cudaStream_t s, int num_sms)
+{
+    if constexpr (P != CD_FP32 || I >= kNLLR) {
+        return cudaErrorNotSupported;
+    } else {
+        if (idx == I) return launch_llreg_t<NV, I>(a, n, base, s, num_sms);
+        return dispatch_llreg<P, NV, I + 1>(idx, a, n, base, s, num_sms);
+    }
+}
+
 template <cd_precision P, int NV, int KW, int WR>
 cudaError_t launch_llchain_t(const ApplyArgs &a, int n, unsigned base, cudaStream_t s, int num_sms)
 {
@@ -1759,6 +1992,10 @@ cudaError_t launch_pack_t(const void *field, void *send, const KGeom &g, cudaStr
     cudaError_t launch_chain_##TAG(int id, const ApplyArgs &a, int n, unsigned base, cudaStream_t s, int sms,     \
                                    int *nrb)                                                                      \
     {                                                                                                             \
+        if (id > LLREG_CHAIN_ID0 && id < LLREG_CHAIN_ID0 + 100) {                                                    \
+            *nrb = 0;                                                                                             \
+            return dispatch_llreg<P, NV>(id - LLREG_CHAIN_ID0 - 1, a, n, base, s, sms);                             \
+        }                                                                                                         \
         if (id >= LL_CHAIN_ID0 && id < LL_CHAIN_ID0 + Variants<P, NV>::n) {                                       \
             *nrb = 0;                                                                                             \
             return dispatch_llchain<P, NV, 0>(id - LL_CHAIN_ID0, a, n, base, s, sms);                             \

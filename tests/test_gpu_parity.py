@@ -441,6 +441,77 @@ def test_ll_chain_all_variants(dims, nvec, prec, n):
     assert ran > 0
 
 
+@pytest.mark.parametrize("dims,nvec,n", [((2, 2, 2, 2), 24, 6), ((2, 2, 2, 2), 24, 1), ((3, 2, 2, 2), 24, 5),
+                                         ((2, 2, 2, 2), 32, 4), ((2, 1, 2, 2), 32, 7)])
+def test_llreg_chain_all_variants(dims, nvec, n):
+    """LL-register chain (variants 3001 + i; fp32): every (rows per CTA, lanes per row) variant
+    that fits co-resident, apply and dagger, last and previous iterate against the oracle,
+    repeated calls (epoch continuity across launches)."""
+    N = 2 * nvec
+    Lh = synth.links(dims, N, kind="hermitian", scale_log2=-4)
+    v = synth.vector(dims, N)
+    ctx = cd.Context(dims, nvec)
+    L = ctx.links_upload(Lh, "fp32")
+    x, y = ctx.field("fp32"), ctx.field("fp32")
+    tol = 2e-6 * n
+    ran = 0
+    for var in range(3001, 3001 + 6):
+        ctx.set_option(cd.CD_OPT_VARIANT, var)
+        for dag in (False, True):
+            for _rep in range(2):
+                x.import_(v)
+                try:
+                    L.apply_chain(x, y, n, dagger=dag)
+                except cd.CDError:
+                    break
+                ran += 1
+                ref, prev = v, v
+                for _ in range(n):
+                    prev, ref = ref, (oracle.adjoint if dag else oracle.apply)(dims, Lh, ref)
+                last, other = (y, x) if n % 2 else (x, y)
+                assert rel_l2(last.export(), ref) <= tol, (var, dag)
+                if n > 1:
+                    assert rel_l2(other.export(), prev) <= tol, (var, dag)
+    assert ran >= 4
+
+
+def test_llreg_chain_bitwise_vs_single_applies():
+    """Variant 3001 (4 rows per CTA, 8 lanes per row) does the per-row arithmetic of the
+    fg_kw1_wr1 single-apply kernel in the same order: a chain of n equals n single applies."""
+    dims, nvec, n = (2, 2, 2, 2), 24, 5
+    N = 2 * nvec
+    Lh = synth.links(dims, N, kind="general", scale_log2=-4)
+    v = synth.vector(dims, N)
+    ctx = cd.Context(dims, nvec)
+    L = ctx.links_upload(Lh, "fp32")
+    x, y = ctx.field("fp32"), ctx.field("fp32")
+    ctx.set_option(cd.CD_OPT_VARIANT, 3001)
+    x.import_(v)
+    L.apply_chain(x, y, n)
+    chain = y.export()
+    ctx.set_option(cd.CD_OPT_VARIANT, ctx.variants("fp32").index("fg_kw1_wr1_f32_nv24"))
+    a, b = ctx.field("fp32"), ctx.field("fp32")
+    a.import_(v)
+    for _ in range(n):
+        L.apply(b, a)
+        a, b = b, a
+    np.testing.assert_array_equal(chain, a.export())
+
+
+def test_chain_tuner_reports_choice():
+    """The chain tuner's pick is queryable (cd_context_chosen_variant with dagger = 2 / 3)."""
+    dims, nvec = (2, 2, 2, 2), 24
+    ctx = cd.Context(dims, nvec)
+    L = ctx.links_generate("fp32", scale_log2=-4)
+    x, y = ctx.field("fp32"), ctx.field("fp32")
+    x.generate()
+    assert ctx.chosen_chain_variant("fp32") == -1
+    L.apply_chain(x, y, 4)
+    vid = ctx.chosen_chain_variant("fp32")
+    assert vid == 1000 or 2000 <= vid < 2000 + len(ctx.variants("fp32")) or 3001 <= vid < 3007 \
+        or 0 <= vid < len(ctx.variants("fp32"))
+
+
 # ---------------------------------------------------------------- multi-RHS on tcgen05 tensor cores
 @pytest.mark.parametrize("dims,nvec,nrhs", [((2, 2, 2, 2), 24, 128), ((2, 3, 2, 2), 32, 128),
                                             ((2, 2, 2, 2), 24, 256)])
