@@ -20,7 +20,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcoarse_dslash.so")
+LIB_PATH = os.environ.get("CD_LIB_PATH") or os.path.join(_HERE, "libcoarse_dslash.so")   # override: A/B experiments
 
 CD_OK, CD_ERR_INVALID, CD_ERR_UNSUPPORTED, CD_ERR_OOM, CD_ERR_CUDA, CD_ERR_NCCL, CD_ERR_MISMATCH = 0, -1, -2, -3, -4, -5, -6
 CD_FP32, CD_FP16 = 0, 1
