@@ -51,6 +51,10 @@ class ClockSampler:
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    # nvidia-smi needs ~0.1-0.3 s to start: it is started before the settle phase, every row is
+    # stamped with the host clock when it arrives, and the summary keeps the rows that arrived
+    # inside the timed window (mark(), unmark()); if fewer than 3 did, the settle-phase rows
+    # (the same workload, already under load) are added and the summary says so.
 
     def __init__(self, device: int):
         self.device = device
@@ -73,7 +77,13 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 9:
-                self.rows.append(parts)
+                self.rows.append([time.perf_counter()] + parts)
+
+    def mark(self):
+        self.t0 = time.perf_counter()
+
+    def unmark(self):
+        self.t1 = time.perf_counter()
 
     def stop(self):
         if self.proc:
@@ -86,14 +96,20 @@ class ClockSampler:
             self.thread.join(timeout=5)
 
     def summary(self):
-        if not self.rows:
+        t0, t1 = getattr(self, "t0", None), getattr(self, "t1", None)
+        rows = [r[1:] for r in self.rows if t0 is None or t1 is None or t0 <= r[0] <= t1 + 0.02]
+        window = "timed region"
+        if len(rows) < 3 and t1 is not None:
+            rows = [r[1:] for r in self.rows if r[0] <= t1 + 0.02]
+            window = "settle phase + timed region (same workload)"
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i].lower() == "active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows), "window": window}
 
 
 # ------------------------------------------------------------------ oracle timing (CPU baseline)
@@ -343,6 +359,8 @@ def run_ours(args):
     # warm-up (the first call autotunes; excluded, as the paper excludes its tuning solve)
     steps(max(args.warmup, 3))
     torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
     t_end = time.perf_counter() + 0.5       # settle clocks under load before the timed region
     while time.perf_counter() < t_end:
         steps(50)
@@ -350,15 +368,14 @@ def run_ours(args):
     a.generate(seed=0x7873, tag=2)
     barrier(world)
     torch.cuda.synchronize()
-    sampler = ClockSampler(local)
-    sampler.start()
-    time.sleep(0.05)
+    sampler.mark()
     n0 = cd.cd_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     steps(args.steps)
     e1.record(stream)
     torch.cuda.synchronize()
+    sampler.unmark()
     sampler.stop()
     launches = cd.cd_launch_count() - n0
     ms_local = e0.elapsed_time(e1) / args.steps
@@ -380,33 +397,44 @@ def run_ours(args):
     # region (first H2D after the start event, last D2H before the end event).
     N = 2 * nvec
     cdt = torch.complex64
-    hv = [torch.empty((V_local, N), dtype=cdt).pin_memory() for _ in range(2)]
-    hy = [torch.empty((V_local, N), dtype=cdt).pin_memory() for _ in range(2)]
+    # NS buffer slots, steps issued in groups of G: the H2D copies of a group land while the
+    # previous group computes, so the compute stream waits on the copy stream once per group and
+    # the applies inside a group stay back to back (programmatic dependent launch between them;
+    # an event wait between two kernels would drain the first before the second starts).
+    NS, G = 8, 4
+    hv = [torch.empty((V_local, N), dtype=cdt).pin_memory() for _ in range(NS)]
+    hy = [torch.empty((V_local, N), dtype=cdt).pin_memory() for _ in range(NS)]
     a.export(hv[0], stream=stream)
-    hv[1].copy_(hv[0])
-    fa = [a, ctx.field(prec)]
-    fb = [b, ctx.field(prec)]
+    for h in hv[1:]:
+        h.copy_(hv[0])
+    fa = [a] + [ctx.field(prec) for _ in range(NS - 1)]
+    fb = [b] + [ctx.field(prec) for _ in range(NS - 1)]
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-    ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("in", "done", "out")}
+    ngrp = NS // G
+    ev = {k: [torch.cuda.Event() for _ in range(ngrp)] for k in ("in", "done", "out")}
     k_e2e = max(10, min(args.steps, 500))
 
     def e2e_steps(n, f0=None):
         if f0 is not None:
             s_in.wait_event(f0)
-        for i in range(n):
-            j = i & 1
-            if i >= 2:
-                s_in.wait_event(ev["done"][j])          # apply i-2 finished reading fa[j]
-            fa[j].import_(hv[j], s_in)
-            ev["in"][j].record(s_in)
-            stream.wait_event(ev["in"][j])
-            if i >= 2:
-                stream.wait_event(ev["out"][j])         # D2H of step i-2 finished with fb[j]
-            links.apply(fb[j], fa[j], stream)
-            ev["done"][j].record(stream)
-            s_out.wait_event(ev["done"][j])
-            fb[j].export(hy[j], stream=s_out, sync=False)
-            ev["out"][j].record(s_out)
+        for g0 in range(0, n, G):
+            grp = range(g0, min(n, g0 + G))
+            q = (g0 // G) % ngrp                     # event set of this group (slots q*G .. q*G+G-1)
+            if g0 >= NS:
+                s_in.wait_event(ev["done"][q])       # the applies of group g-ngrp finished reading fa[]
+            for i in grp:
+                fa[i % NS].import_(hv[i % NS], s_in)
+            ev["in"][q].record(s_in)
+            stream.wait_event(ev["in"][q])
+            if g0 >= NS:
+                stream.wait_event(ev["out"][q])      # the D2H of group g-ngrp finished with fb[]
+            for i in grp:
+                links.apply(fb[i % NS], fa[i % NS], stream)
+            ev["done"][q].record(stream)
+            s_out.wait_event(ev["done"][q])
+            for i in grp:
+                fb[i % NS].export(hy[i % NS], stream=s_out, sync=False)
+            ev["out"][q].record(s_out)
         stream.wait_stream(s_in)
         stream.wait_stream(s_out)
 
@@ -430,7 +458,7 @@ def run_ours(args):
     g1.record(stream)
     torch.cuda.synchronize()
     ms_serial = dist_max(g0.elapsed_time(g1) / k_e2e, world, device=f"cuda:{local}")
-    del fa[1], fb[1]
+    del fa[1:], fb[1:]
 
     # ---- informational extras on one GPU (not the headline): fp16 storage, the 2^4 coarsest
     # grid as chained applies in one kernel, 128 right-hand sides on the tcgen05 tensor cores
@@ -475,7 +503,7 @@ def run_ours(args):
                          "algorithmic_bytes_per_launch": perfmodel.metric_bytes_per_site(nvec, prec) * V_local},
             "e2e": {"value": round(e2e_val, 2), "unit": "GFLOPS", "ms_per_step": round(ms_e2e, 5),
                     "h2d_bytes_per_step": V_local * N * 8, "d2h_bytes_per_step": V_local * N * 8,
-                    "pipeline": "H2D / apply / D2H on three streams, two buffer slots",
+                    "pipeline": "H2D / apply / D2H on three streams, 8 buffer slots, groups of 4 steps",
                     "ms_per_step_serialised": round(ms_serial, 5)},
             "gpu_launches": int(launches),
             "clocks": clocks,
