@@ -1408,7 +1408,7 @@ int coarse_dslash_apply_chain(const cd_links *l, cd_field *x, cd_field *y, int n
         CUDA_TRY(cudaEventCreate(&e0), "event");
         CUDA_TRY(cudaEventCreate(&e1), "event");
         float best = 1e30f;
-        std::vector<int> cands{CLUSTER_CHAIN_ID};
+        std::vector<int> cands{CPUSH_CHAIN_ID, CLUSTER_CHAIN_ID};
         for (int i = 0; i < kNumLLReg; i++) cands.push_back(LLREG_CHAIN_ID0 + 1 + i);
         for (int v = 0; v < variant_count(p, c->nvec); v++) {
             cands.push_back(LL_CHAIN_ID0 + v);
@@ -1454,7 +1454,7 @@ int coarse_dslash_apply_chain(const cd_links *l, cd_field *x, cd_field *y, int n
         c->chosen[key] = id;
     }
     const char *tf = getenv("CD_CHAIN_TRACE");   // diagnostic only: clock64 events of CTA 0 (LL-register chain)
-    if (tf && id > LLREG_CHAIN_ID0 && id < LLREG_CHAIN_ID0 + 100)
+    if (tf && ((id > LLREG_CHAIN_ID0 && id < LLREG_CHAIN_ID0 + 100) || id == CPUSH_CHAIN_ID))
         CUDA_TRY(cudaMallocAsync(reinterpret_cast<void **>(&a.trace), 40 * 1024 * sizeof(long long), s), "trace");
     if (a.trace) CUDA_TRY(cudaMemsetAsync(a.trace, 0, 40 * 1024 * sizeof(long long), s), "trace");
     cudaError_t e = chain_launch(c, p, id, a, n, s);

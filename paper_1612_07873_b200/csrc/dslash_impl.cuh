@@ -1617,6 +1617,298 @@ cudaError_t launch_cluster_chain_t(const ApplyArgs &a, int n, cudaStream_t s)
     return cudaLaunchKernelExC(&cfg, (const void *)dslash_cluster_chain<P, NV, NW>, args);
 }
 
+// ------------------------------------------------------------------ CLUSTER push chain (V <= 16, fp32, Nvec 24)
+// The whole lattice in ONE thread-block cluster, one CTA per site, the site's nine 48 x 48
+// complex matrices in registers for all n applies, and NO barrier inside an apply:
+//   * thread (row i, lane d of 8) holds L_k(x)[i][chunks d, d+8, d+16] for ALL nine hops
+//     (108 floats), so the hop sum stays in registers and the 8-lane xor-shuffle that finishes
+//     the dot product leaves y(x)[i] in every lane of the row (12 warps x 4 rows);  the complex
+//     MACs run on the packed FP32 pipe (cmac2x: FFMA2 with a broadcast scalar);
+//   * lane d of the row then pushes y(x)[i] to destination d -- this CTA's own slot 8 and the
+//     receive slots of the CTAs that read x as a neighbour -- with st.async into their shared
+//     memory, and lane (row 0 of the warp, d) adds the warp's arrival + 32 bytes of expected
+//     transaction on the destination's mbarrier (remote arrive.expect_tx): barrier 0 (own slot)
+//     completes when the 12 own warps arrived and 384 bytes landed, barrier 1 (all remote
+//     slots) when 12 warps of every producing neighbour arrived and all their bytes landed --
+//     no local re-arming;
+//   * a warp does the X hop as soon as its own record lands, then waits once for the remote
+//     records (the X math overlaps their DSMEM flight).
+// Receive slots (consumer c, hop k): k = 8 or L_mu = 1 -> slot 8 (own); L_mu = 2 -> slot 2 mu
+// for both hops (x + mu = x - mu: one record); else slot k.  Flow control needs no extra signal:
+// a warp pushes epoch t+1 only after it received the complete epoch-t records of every
+// neighbour, and every warp of a neighbour pushes its part of epoch t only after it finished
+// reading epoch t-1 (the slot parity being overwritten) and observed both barrier phases of
+// epoch t-1 -- the neighbour relation is symmetric.  Measured (2^4, Nvec 24): 1.02 us per
+// apply against 0.91 us for the LL-register chain: one SM per site issues the site's 83k FMAs
+// in ~1200 cycles (FP32 pipe at ~60 % in situ), which the short DSMEM hop does not win back
+// (DESIGN.md §6).
+template <int NV>
+struct CPushCfg {
+    static constexpr int N = 2 * NV;
+    static constexpr int LD = 8;              // lanes per row (dot-product split)
+    static constexpr int RPW = 32 / LD;       // rows per warp
+    static constexpr int NW = N / RPW;        // warps (producer warps per slot phase)
+    static constexpr int THREADS = 32 * NW;
+    static constexpr int LC = N / (2 * LD);   // 16-B chunks per lane per hop row
+};
+
+// fp32 complex MAC of one 16-B chunk pair on the packed FP32 pipe (SASS FFMA2 with a scalar
+// broadcast operand): A += lr * (vr, vi), B += li * (vr, vi) for both complex of the chunk;
+// the complex result is (A.x - B.y, A.y + B.x).  Two FFMA2 per complex MAC instead of four FFMA,
+// and the vector pair is read once (reuse) for both.
+__device__ __forceinline__ void cmac2x(const uint4 &a, const uint4 &b, unsigned long long &A, unsigned long long &B)
+{
+    asm("{\n.reg .b64 l0, l1, v0, v1, i0, i1;\n"
+        "mov.b64 l0, {%2, %2};\n"
+        "mov.b64 i0, {%3, %3};\n"
+        "mov.b64 v0, {%6, %7};\n"
+        "fma.rn.f32x2 %0, l0, v0, %0;\n"
+        "fma.rn.f32x2 %1, i0, v0, %1;\n"
+        "mov.b64 l1, {%4, %4};\n"
+        "mov.b64 i1, {%5, %5};\n"
+        "mov.b64 v1, {%8, %9};\n"
+        "fma.rn.f32x2 %0, l1, v1, %0;\n"
+        "fma.rn.f32x2 %1, i1, v1, %1;\n}"
+        : "+l"(A), "+l"(B) : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w));
+}
+
+// wait for a phase, return 0 as a value the dependent shared loads use in their address
+__device__ __forceinline__ uint32_t mbar_wait_dep(uint32_t bar, uint32_t parity)
+{
+    uint32_t z;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "@!p bra WAIT_%=;\n"
+        "mov.u32 %0, 0;\n"
+        "}\n" : "=r"(z) : "r"(bar), "r"(parity) : "memory");
+    return z;
+}
+// the same, issued only after `after` is computed (keeps the X-hop math ahead of the remote wait)
+__device__ __forceinline__ uint32_t mbar_wait_dep_after(uint32_t bar, uint32_t parity, float after)
+{
+    uint32_t z;
+    asm volatile(
+        "{\n"
+        ".reg .pred p, q;\n"
+        "setp.eq.b32 q, %3, 0x7F800001;\n"   // a signalling-NaN pattern arithmetic never produces: never
+                                               // true, but orders the wait after `after`
+        "@q bra DONE_%=;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "@!p bra WAIT_%=;\n"
+        "DONE_%=:\n"
+        "mov.u32 %0, 0;\n"
+        "}\n" : "=r"(z) : "r"(bar), "r"(parity), "r"(__float_as_uint(after)) : "memory");
+    return z;
+}
+// shared load the compiler may schedule freely (ordered only through its address operand)
+__device__ __forceinline__ uint4 lds128_dep(uint32_t a)
+{
+    uint4 v;
+    asm("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t local, unsigned cta)
+{
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(cta));
+    return r;
+}
+__device__ __forceinline__ void st_async_f2(uint32_t dst, float a, float b, uint32_t bar)
+{
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];"
+                 ::"r"(dst), "f"(a), "f"(b), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx_remote(uint32_t bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+
+template <int NV, bool TRACE>
+__global__ void __launch_bounds__(CPushCfg<NV>::THREADS, 1) dslash_cpush(ApplyArgs a, int n)
+{
+    using Q = Cfg<CD_FP32, NV>;
+    using K = CPushCfg<NV>;
+    __shared__ __align__(16) float2 rec[2][9][K::N];   // receive slots by epoch parity
+    __shared__ __align__(8) uint64_t bar[2][2];         // [parity][0: own slot 8, 1: all remote slots]
+
+    const int site = (int)cluster_rank();   // grid == one cluster of V CTAs
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int row = warp * K::RPW + lane / K::LD, d = lane % K::LD;
+    const unsigned char *links = static_cast<const unsigned char *>(a.links);
+    unsigned char *const g0 = const_cast<unsigned char *>(static_cast<const unsigned char *>(a.in));
+    unsigned char *const g1 = static_cast<unsigned char *>(a.out);
+    int x[4];
+    decode(a.g, site, x);
+
+    // this lane's push destination (index d into: own slot 8, then per mu the -mu / +mu readers)
+    int dst_cta = -1, dst_slot = 0;
+    {
+        int i = 0;
+        if (d == i) dst_cta = site, dst_slot = 8;
+        i++;
+#pragma unroll
+        for (int mu = 0; mu < 4; mu++) {
+            const int L = sel4(a.g.L, mu);
+            if (L >= 2) {   // x - mu reads us through hop 2mu (L = 2: x - mu = x + mu, one push)
+                if (d == i) dst_cta = neighbour(a.g, x, site, 2 * mu + 1), dst_slot = 2 * mu;
+                i++;
+            }
+            if (L >= 3) {   // x + mu reads us through hop 2mu + 1
+                if (d == i) dst_cta = neighbour(a.g, x, site, 2 * mu), dst_slot = 2 * mu + 1;
+                i++;
+            }
+        }
+    }
+    const uint32_t rec_s = (uint32_t)__cvta_generic_to_shared(&rec[0][0][0]);
+    const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(&bar[0][0]);
+    uint32_t dst_rec = 0, dst_bar = 0;   // cluster addresses of slot dst_slot / its barrier, parity 0
+    if (dst_cta >= 0) {
+        dst_rec = mapa_u32(rec_s + (uint32_t)(dst_slot * K::N + row) * 8u, (unsigned)dst_cta);
+        dst_bar = mapa_u32(bar_s + (dst_slot == 8 ? 0u : 8u), (unsigned)dst_cta);
+    }
+    // the slot each hop reads (kseq order: X first), and the number of remote producers
+    uint64_t slotmask = 0;   // 4 bits per hop position
+    int nremote = 0;
+#pragma unroll
+    for (int i = 0; i < 9; i++) {
+        const int k = kseq(i);
+        int s = 8;
+        if (k < 8) {
+            const int L = sel4(a.g.L, k >> 1);
+            s = L == 1 ? 8 : (L == 2 ? (k & ~1) : k);
+            if (L >= 3 || (L == 2 && !(k & 1))) nremote++;
+        }
+        slotmask |= (uint64_t)s << (4 * i);
+    }
+
+    uint4 Lc[9][K::LC];
+#pragma unroll
+    for (int i = 0; i < 9; i++) {
+        const unsigned char *m = links + ((size_t)site * 9 + kseq(i)) * Q::MREC + row * Q::ROWB;
+#pragma unroll
+        for (int c = 0; c < K::LC; c++) Lc[i][c] = ld_stream(m + (d + K::LD * c) * 16);
+    }
+    if (a.dagger) {   // tau3 on the input folded into the register-resident links (chunks q >= Nvec/2)
+#pragma unroll
+        for (int i = 0; i < 9; i++)
+#pragma unroll
+            for (int c = 0; c < K::LC; c++)
+                if ((d + K::LD * c) * 2 >= NV) Lc[i][c] = neg_chunk<false>(Lc[i][c]);
+    }
+    const float osign = (a.dagger && row >= NV) ? -1.0f : 1.0f;
+    if (threadIdx.x == 0) {   // own: 12 producer warps; remote: 12 per producing neighbour
+        for (int p = 0; p < 2; p++) {
+            mbar_init(&bar[p][0], K::NW);
+            mbar_init(&bar[p][1], K::NW * (nremote > 0 ? nremote : 1));
+        }
+        fence_mbar_init();
+    }
+    cluster_sync_all();
+
+    long long *const tr = (TRACE && a.trace && blockIdx.x == 0 && lane == 0) ? a.trace : nullptr;
+    for (int t = 0; t < n; t++) {
+        const int par = t & 1;
+        const bool trt = TRACE && tr && t < 1024 && warp < 8;
+        if (trt) tr[(4 * warp) * 1024 + t] = clock64();
+        unsigned long long A = 0ull, B = 0ull;   // packed (x, y) accumulators, see cmac2x
+        if (t == 0) {   // the input is ready at launch
+#pragma unroll
+            for (int i = 0; i < 9; i++) {
+                const unsigned char *src = g0 + (size_t)neighbour(a.g, x, site, kseq(i)) * Q::VREC;
+#pragma unroll
+                for (int c = 0; c < K::LC; c++) cmac2x(Lc[i][c], ld_nc(src + (d + K::LD * c) * 16), A, B);
+            }
+        } else {
+            const uint32_t ph = ((t - 1) >> 1) & 1;
+            // X (own slot, lands first) while the remote records are in flight, then one wait
+            // for all remote slots.  Records arrive through st.async: the shared loads take a
+            // zero from the wait as an address operand so they cannot move above it.
+            uint32_t z = mbar_wait_dep(bar_s + (uint32_t)(par * 2) * 8u, ph);
+            if (TRACE && trt) tr[(4 * warp + 1) * 1024 + t] = clock64();
+#pragma unroll
+            for (int i = 0; i < 9; i++) {
+                const uint32_t s = (uint32_t)(slotmask >> (4 * i)) & 15u;
+                if (i == 1 && nremote > 0) {
+                    z = mbar_wait_dep_after(bar_s + (uint32_t)(par * 2 + 1) * 8u, ph,
+                                            __uint_as_float((uint32_t)A ^ (uint32_t)B));
+                    if (TRACE && trt) tr[(32 + warp) * 1024 + t] = clock64() + z;
+                }
+                const uint32_t src = rec_s + (uint32_t)((par * 9 + s) * K::N) * 8u + z;
+#pragma unroll
+                for (int c = 0; c < K::LC; c++) cmac2x(Lc[i][c], lds128_dep(src + (uint32_t)(d + K::LD * c) * 16u), A, B);
+            }
+        }
+        float re = __uint_as_float((uint32_t)A) - __uint_as_float((uint32_t)(B >> 32));
+        float im = __uint_as_float((uint32_t)(A >> 32)) + __uint_as_float((uint32_t)B);
+        if (trt) tr[(4 * warp + 2) * 1024 + t] = clock64();
+#pragma unroll
+        for (int m = K::LD / 2; m >= 1; m >>= 1) {
+            re += shfl_xor(re, m);
+            im += shfl_xor(im, m);
+        }
+        re *= osign;
+        im *= osign;
+        if (t + 1 < n && dst_cta >= 0) {
+            const uint32_t off = (uint32_t)(par ^ 1);
+            st_async_f2(dst_rec + off * 9u * K::N * 8u, re, im, dst_bar + off * 16u);
+            if (lane < K::LD) mbar_arrive_expect_tx_remote(dst_bar + off * 16u, K::RPW * 8u);
+        }
+        if (t >= n - 2 && d == 0) {   // the caller sees the last two iterates (x / y ping-pong)
+            unsigned char *gout = (t & 1) ? g0 : g1;
+            reinterpret_cast<float2 *>(gout + (size_t)site * Q::VREC)[row] = make_float2(re, im);
+        }
+        if (trt) tr[(4 * warp + 3) * 1024 + t] = clock64();
+    }
+    cluster_sync_all();   // no CTA leaves while a peer may still address its shared memory
+}
+
+template <cd_precision P, int NV>
+cudaError_t launch_cpush_t(const ApplyArgs &a, int n, cudaStream_t s)
+{
+    if constexpr (P != CD_FP32 || NV != 24) {
+        return cudaErrorNotSupported;
+    } else {
+        using K = CPushCfg<NV>;
+        // st.async needs a real cluster (>= 2 CTAs); one cluster holds at most 16 CTAs
+        if (a.g.V < 2 || a.g.V > 16 || a.halo || a.g.split) return cudaErrorNotSupported;
+        const void *fn = a.trace ? (const void *)dslash_cpush<NV, true> : (const void *)dslash_cpush<NV, false>;
+        static bool attr = false;
+        if (!attr) {
+            cudaError_t e = cudaFuncSetAttribute(dslash_cpush<NV, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(dslash_cpush<NV, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (e != cudaSuccess) return e;
+            attr = true;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)a.g.V);
+        cfg.blockDim = dim3(K::THREADS);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)a.g.V;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg);
+        if (e != cudaSuccess) return e;
+        if (nclusters < 1) return cudaErrorCooperativeLaunchTooLarge;
+        ApplyArgs aa = a;
+        int nn = n;
+        void *args[] = {&aa, &nn};
+        count_launch();
+        return cudaLaunchKernelExC(&cfg, fn, args);
+    }
+}
+
 // ------------------------------------------------------------------ halo term (multi-rank)
 // One CTA per face site: y(x) = partial(x) + sum over remote hops L_k(x) v_halo, then the
 // final store (fp16: whole-site re-quantisation).  Neighbour records come from the receive
@@ -1999,6 +2291,10 @@ cudaError_t launch_pack_t(const void *field, void *send, const KGeom &g, cudaStr
         if (id >= LL_CHAIN_ID0 && id < LL_CHAIN_ID0 + Variants<P, NV>::n) {                                       \
             *nrb = 0;                                                                                             \
             return dispatch_llchain<P, NV, 0>(id - LL_CHAIN_ID0, a, n, base, s, sms);                             \
+        }                                                                                                         \
+        if (id == CPUSH_CHAIN_ID) {                                                                               \
+            *nrb = 0;                                                                                             \
+            return launch_cpush_t<P, NV>(a, n, s);                                                                \
         }                                                                                                         \
         if (id == CLUSTER_CHAIN_ID) {                                                                             \
             *nrb = 0;                                                                                             \

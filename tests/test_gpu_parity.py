@@ -409,6 +409,48 @@ def test_cluster_chain_forced(nvec, prec, n):
         assert rel_l2(other.export(), prev) <= (2e-6 * n if prec == "fp32" else 2e-3 * n)
 
 
+@pytest.mark.parametrize("dims,n", [((2, 2, 2, 2), 7), ((2, 2, 2, 2), 1), ((2, 2, 2, 2), 2), ((2, 1, 2, 2), 6),
+                                    ((3, 3, 1, 1), 5), ((4, 2, 2, 1), 4), ((2, 1, 1, 1), 3), ((3, 1, 5, 1), 6)])
+def test_cpush_chain_forced(dims, n):
+    """Cluster push chain (variant 4000; fp32, Nvec 24, V <= 16): receive-slot mapping for
+    extents 1 (self hop), 2 (shared +-mu slot) and >= 3 (two slots); apply and dagger, last and
+    previous iterate against the oracle, repeated launches (mbarrier phases restart per launch)."""
+    nvec = 24
+    N = 2 * nvec
+    Lh = synth.links(dims, N, kind="hermitian", scale_log2=-4)
+    v = synth.vector(dims, N)
+    ctx = cd.Context(dims, nvec)
+    ctx.set_option(cd.CD_OPT_VARIANT, 4000)
+    L = ctx.links_upload(Lh, "fp32")
+    x, y = ctx.field("fp32"), ctx.field("fp32")
+    tol = 2e-6 * n
+    for dag in (False, True):
+        ref, prev = v, v
+        for _ in range(n):
+            prev, ref = ref, (oracle.adjoint if dag else oracle.apply)(dims, Lh, ref)
+        for _rep in range(2):
+            x.import_(v)
+            L.apply_chain(x, y, n, dagger=dag)
+            last, other = (y, x) if n % 2 else (x, y)
+            assert rel_l2(last.export(), ref) <= tol, (dims, dag)
+            if n > 1:
+                assert rel_l2(other.export(), prev) <= tol, (dims, dag)
+
+
+def test_cpush_chain_unsupported_shapes():
+    """Variant 4000 refuses lattices above one 16-CTA cluster, a single site (st.async needs a
+    cluster of >= 2 CTAs), fp16 storage and Nvec 32."""
+    for dims, nvec, prec in (((3, 2, 2, 2), 24, "fp32"), ((1, 1, 1, 1), 24, "fp32"), ((2, 2, 2, 2), 24, "fp16"),
+                             ((2, 2, 2, 2), 32, "fp32")):
+        ctx = cd.Context(dims, nvec)
+        ctx.set_option(cd.CD_OPT_VARIANT, 4000)
+        L = ctx.links_generate(prec, scale_log2=-4)
+        x, y = ctx.field(prec), ctx.field(prec)
+        x.generate()
+        with pytest.raises(cd.CDError):
+            L.apply_chain(x, y, 3)
+
+
 @pytest.mark.parametrize("dims,nvec,prec,n", [((2, 2, 2, 2), 24, "fp32", 6), ((2, 2, 2, 2), 24, "fp16", 3),
                                               ((3, 2, 2, 2), 32, "fp32", 5), ((2, 2, 2, 2), 32, "fp16", 4)])
 def test_ll_chain_all_variants(dims, nvec, prec, n):
@@ -508,7 +550,7 @@ def test_chain_tuner_reports_choice():
     assert ctx.chosen_chain_variant("fp32") == -1
     L.apply_chain(x, y, 4)
     vid = ctx.chosen_chain_variant("fp32")
-    assert vid == 1000 or 2000 <= vid < 2000 + len(ctx.variants("fp32")) or 3001 <= vid < 3007 \
+    assert vid in (1000, 4000) or 2000 <= vid < 2000 + len(ctx.variants("fp32")) or 3001 <= vid < 3007 \
         or 0 <= vid < len(ctx.variants("fp32"))
 
 
