@@ -131,7 +131,8 @@ const char *cd_variant_name(const cd_context *ctx, cd_precision prec, int id);
 /* Variant chosen for (prec, dagger) by the tuner / heuristic for this context's geometry
  * (-1 if that key has not been resolved yet).  dagger = 2 / 3 query coarse_dslash_apply_chain's
  * choice for D / D^dagger (ids: fg variant = counter chain, 1000 = cluster chain, 2000 + fg
- * variant = LL chain, 3001 + i = LL-register chain, 4000 = cluster push chain). */
+ * variant = LL chain, 3001 + i = LL-register chain, 4000 = cluster push chain, 5000 = LL-warp
+ * chain). */
 int cd_context_chosen_variant(const cd_context *ctx, cd_precision prec, int dagger);
 
 /* Total kernels launched by this process through this library (for launch accounting). */

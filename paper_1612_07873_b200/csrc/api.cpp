@@ -1408,7 +1408,7 @@ int coarse_dslash_apply_chain(const cd_links *l, cd_field *x, cd_field *y, int n
         CUDA_TRY(cudaEventCreate(&e0), "event");
         CUDA_TRY(cudaEventCreate(&e1), "event");
         float best = 1e30f;
-        std::vector<int> cands{CPUSH_CHAIN_ID, CLUSTER_CHAIN_ID};
+        std::vector<int> cands{LLWARP_CHAIN_ID, CPUSH_CHAIN_ID, CLUSTER_CHAIN_ID};
         for (int i = 0; i < kNumLLReg; i++) cands.push_back(LLREG_CHAIN_ID0 + 1 + i);
         for (int v = 0; v < variant_count(p, c->nvec); v++) {
             cands.push_back(LL_CHAIN_ID0 + v);

@@ -185,6 +185,7 @@ struct ApplyArgs {
 
 constexpr int CLUSTER_CHAIN_ID = 1000;   // apply_chain variant: whole lattice in one cluster
 constexpr int CPUSH_CHAIN_ID = 4000;     // apply_chain variant: one cluster, DSMEM push (fp32, Nvec 24)
+constexpr int LLWARP_CHAIN_ID = 5000;    // apply_chain variant: LL protocol, one warp per 4 rows (fp32)
 constexpr int LL_CHAIN_ID0 = 2000;       // apply_chain variants 2000 + fg id: LL-protocol chain
 constexpr int LLREG_CHAIN_ID0 = 3000;    // apply_chain variants 3001 + i: LL-register chain (fp32), i < kNumLLReg
 constexpr int kNumLLReg = 6;

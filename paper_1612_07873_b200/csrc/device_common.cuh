@@ -159,6 +159,26 @@ __device__ __forceinline__ void cmac2(const uint4 &a, const uint4 &b, float &re,
     im = fmaf(ai1, br1, im);
 }
 
+// fp32 complex MAC of one 16-B chunk pair on the packed FP32 pipe (SASS FFMA2 with a scalar
+// broadcast operand): A += lr * (vr, vi), B += li * (vr, vi) for both complex of the chunk;
+// the complex result is (A.x - B.y, A.y + B.x).  Two FFMA2 per complex MAC instead of four FFMA,
+// and the vector pair is read once (reuse) for both.
+__device__ __forceinline__ void cmac2x(const uint4 &a, const uint4 &b, unsigned long long &A, unsigned long long &B)
+{
+    asm("{\n.reg .b64 l0, l1, v0, v1, i0, i1;\n"
+        "mov.b64 l0, {%2, %2};\n"
+        "mov.b64 i0, {%3, %3};\n"
+        "mov.b64 v0, {%6, %7};\n"
+        "fma.rn.f32x2 %0, l0, v0, %0;\n"
+        "fma.rn.f32x2 %1, i0, v0, %1;\n"
+        "mov.b64 l1, {%4, %4};\n"
+        "mov.b64 i1, {%5, %5};\n"
+        "mov.b64 v1, {%8, %9};\n"
+        "fma.rn.f32x2 %0, l1, v1, %0;\n"
+        "fma.rn.f32x2 %1, i1, v1, %1;\n}"
+        : "+l"(A), "+l"(B) : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w));
+}
+
 // fp16 complex MAC of one complex pair held as half2 {re, im} words, fp32 accumulate:
 // one FHFMA (fma.rn.f32.f16) per real product; no conversions (SURVEY §0 probe).
 //   ra += lr*vr, rb += li*vi, ia += lr*vi, ib += li*vr   ->  re = ra - rb, im = ia + ib

@@ -1436,6 +1436,165 @@ cudaError_t launch_llchain_t(const ApplyArgs &a, int n, unsigned base, cudaStrea
     }
 }
 
+// ------------------------------------------------------------------ LL-warp chain (fp32; latency regime)
+// The LL protocol of dslash_llchain / dslash_llreg with the work of a row kept in ONE warp:
+//   * CTA = one warp = 4 rows of one site (N/4 CTAs per site); lane (row r, d of 8) holds
+//     L_k(x)[row][chunks d, d+8, ...] for ALL nine hops in registers (cmac2x / FFMA2 math), so
+//     the hop sum never leaves registers and the 8-lane xor-shuffle leaves y(x)[row] in every
+//     lane of the row -- no shared-memory reduction, no CTA barrier, no warp hand-off;
+//   * the warp polls the distinct neighbour records of the epoch it needs (at L_mu = 2 the
+//     +-mu hops share one record, at L_mu = 1 a hop reads the site's own record) with one
+//     round of lane-contiguous 16-B LL loads per poll, stages the payload in shared memory and
+//     runs the nine mat-vecs; lane d = 0 of each row then stores the row's LL word.
+// Critical path per apply: L2 round trip of the LL words + the warp's math + 3 shuffles + one
+// store (the LL-register chain adds a cross-warp reduction and a barrier hand-off).  fp32 only.
+template <int NV>
+struct LLWarpCfg {
+    static constexpr int N = 2 * NV;
+    static constexpr int LD = 8;              // lanes per row (dot-product split)
+    static constexpr int RPW = 32 / LD;       // rows per warp (= per CTA)
+    static constexpr int NWS = N / RPW;       // CTAs per site
+    static constexpr int LC = N / (2 * LD);   // 16-B link chunks per lane per hop
+};
+
+template <int NV>
+__global__ void __launch_bounds__(32, 1) dslash_llwarp(ApplyArgs a, int n, unsigned base)
+{
+    using Q = Cfg<CD_FP32, NV>;
+    using K = LLWarpCfg<NV>;
+    using LL = LLCfg<CD_FP32, NV>;
+    constexpr int UPL = (LL::WP + 31) / 32;   // LL units per lane per record
+    __shared__ __align__(16) float2 vst[9][K::N];
+
+    const int site = blockIdx.x / K::NWS, wb = blockIdx.x - site * K::NWS;
+    const int lane = threadIdx.x, d = lane % K::LD;
+    const int row = wb * K::RPW + lane / K::LD;
+    unsigned char *const buf0 = const_cast<unsigned char *>(static_cast<const unsigned char *>(a.in));
+    unsigned char *const buf1 = static_cast<unsigned char *>(a.out);
+    unsigned char *const ll = reinterpret_cast<unsigned char *>(a.llbuf);
+    const size_t llhalf = (size_t)a.g.V * LL::REC;
+
+    int x[4];
+    decode(a.g, site, x);
+    int nb[9];          // neighbour of hop position i (kseq order: X first)
+    uint32_t dup = 0;   // bit i: hop i reads the record staged for hop src(i) (L_mu = 2: i - 1; L_mu = 1: 0)
+    uint32_t dsrc1 = 0; // bit i: ... and that source is X (L_mu = 1)
+#pragma unroll
+    for (int i = 0; i < 9; i++) {
+        const int k = kseq(i);
+        nb[i] = neighbour(a.g, x, site, k);
+        if (k < 8) {
+            const int L = sel4(a.g.L, k >> 1);
+            if (L == 1) dup |= 1u << i, dsrc1 |= 1u << i;
+            else if (L == 2 && (k & 1)) dup |= 1u << i;
+        }
+    }
+    uint4 Lc[9][K::LC];
+#pragma unroll
+    for (int i = 0; i < 9; i++) {
+        const unsigned char *m = static_cast<const unsigned char *>(a.links) + ((size_t)site * 9 + kseq(i)) * Q::MREC +
+                                 row * Q::ROWB;
+#pragma unroll
+        for (int c = 0; c < K::LC; c++) Lc[i][c] = ld_stream(m + (d + K::LD * c) * 16);
+    }
+    if (a.dagger) {   // tau3 on the input folded into the register-resident links (chunks q >= Nvec/2)
+#pragma unroll
+        for (int i = 0; i < 9; i++)
+#pragma unroll
+            for (int c = 0; c < K::LC; c++)
+                if ((d + K::LD * c) * 2 >= NV) Lc[i][c] = neg_chunk<false>(Lc[i][c]);
+    }
+    const float osign = (a.dagger && row >= NV) ? -1.0f : 1.0f;
+
+    for (int t = 0; t < n; t++) {
+        const long long c_start = clock64();
+        unsigned long long A = 0ull, B = 0ull;
+        if (t == 0) {   // the input is ready at launch: ordinary format
+#pragma unroll
+            for (int i = 0; i < 9; i++) {
+                const unsigned char *src = buf0 + (size_t)nb[i] * Q::VREC;
+#pragma unroll
+                for (int c = 0; c < K::LC; c++) cmac2x(Lc[i][c], ld_nc(src + (d + K::LD * c) * 16), A, B);
+            }
+        } else {
+            const unsigned want = base + (unsigned)t;
+            const unsigned char *src = ll + (size_t)(t & 1) * llhalf;
+            uint32_t miss = 0;   // bit UPL * i + u: unit lane + 32 u of hop i's record not landed yet
+#pragma unroll
+            for (int i = 0; i < 9; i++)
+#pragma unroll
+                for (int u = 0; u < UPL; u++)
+                    if (!((dup >> i) & 1u) && lane + 32 * u < LL::WP) miss |= 1u << (UPL * i + u);
+            __syncwarp();   // every lane finished reading vst (previous apply)
+            if (a.poll_d0 > 0) spin_until(c_start + a.poll_d0);
+            while (true) {
+                uint4 w[9][UPL];
+#pragma unroll
+                for (int i = 0; i < 9; i++)
+#pragma unroll
+                    for (int u = 0; u < UPL; u++)
+                        if ((miss >> (UPL * i + u)) & 1u) w[i][u] = ld_cg(src + (size_t)nb[i] * LL::REC + (lane + 32 * u) * 16);
+#pragma unroll
+                for (int i = 0; i < 9; i++)
+#pragma unroll
+                    for (int u = 0; u < UPL; u++)
+                        if (((miss >> (UPL * i + u)) & 1u) && w[i][u].y == want && w[i][u].w == want) {
+                            miss &= ~(1u << (UPL * i + u));
+                            vst[i][lane + 32 * u] = make_float2(__uint_as_float(w[i][u].x), __uint_as_float(w[i][u].z));
+                        }
+                if (!__any_sync(0xffffffffu, miss != 0u)) break;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 9; i++) {
+                const int s = (i > 0 && ((dup >> i) & 1u)) ? (((dsrc1 >> i) & 1u) ? 0 : i - 1) : i;
+                const float2 *v = vst[s];
+#pragma unroll
+                for (int c = 0; c < K::LC; c++) cmac2x(Lc[i][c], lds128(v + 2 * (d + K::LD * c)), A, B);
+            }
+        }
+        float re = __uint_as_float((uint32_t)A) - __uint_as_float((uint32_t)(B >> 32));
+        float im = __uint_as_float((uint32_t)(A >> 32)) + __uint_as_float((uint32_t)B);
+#pragma unroll
+        for (int m = K::LD / 2; m >= 1; m >>= 1) {
+            re += shfl_xor(re, m);
+            im += shfl_xor(im, m);
+        }
+        re *= osign;
+        im *= osign;
+        if (d == 0) {
+            const unsigned ep = base + (unsigned)t + 1;
+            if (t + 1 < n)
+                reinterpret_cast<uint4 *>(ll + (size_t)((t + 1) & 1) * llhalf + (size_t)site * LL::REC)[row] =
+                    make_uint4(__float_as_uint(re), ep, __float_as_uint(im), ep);
+            if (t >= n - 2) {   // the caller sees the last two iterates (x / y ping-pong)
+                unsigned char *gout = (t & 1) ? buf0 : buf1;
+                reinterpret_cast<float2 *>(gout + (size_t)site * Q::VREC)[row] = make_float2(re, im);
+            }
+        }
+    }
+}
+
+template <cd_precision P, int NV>
+cudaError_t launch_llwarp_t(const ApplyArgs &a, int n, unsigned base, cudaStream_t s, int num_sms)
+{
+    if constexpr (P != CD_FP32) {
+        return cudaErrorNotSupported;
+    } else {
+        using K = LLWarpCfg<NV>;
+        int per_sm = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dslash_llwarp<NV>, 32, 0);
+        if (e != cudaSuccess) return e;
+        if ((int64_t)a.g.V * K::NWS > (int64_t)per_sm * num_sms) return cudaErrorCooperativeLaunchTooLarge;
+        ApplyArgs aa = a;
+        int nn = n;
+        unsigned bb = base;
+        void *args[] = {&aa, &nn, &bb};
+        return launch_ex((const void *)dslash_llwarp<NV>, dim3((unsigned)(a.g.V * K::NWS)), dim3(32), 0, s, false, args,
+                         true);
+    }
+}
+
 // ------------------------------------------------------------------ CLUSTER chain (V <= 16 sites)
 // The whole lattice in ONE thread-block cluster (non-portable size up to 16, one CTA per site):
 // every CTA keeps its site's nine matrices in registers for all n applies and its current
@@ -1651,26 +1810,6 @@ struct CPushCfg {
     static constexpr int THREADS = 32 * NW;
     static constexpr int LC = N / (2 * LD);   // 16-B chunks per lane per hop row
 };
-
-// fp32 complex MAC of one 16-B chunk pair on the packed FP32 pipe (SASS FFMA2 with a scalar
-// broadcast operand): A += lr * (vr, vi), B += li * (vr, vi) for both complex of the chunk;
-// the complex result is (A.x - B.y, A.y + B.x).  Two FFMA2 per complex MAC instead of four FFMA,
-// and the vector pair is read once (reuse) for both.
-__device__ __forceinline__ void cmac2x(const uint4 &a, const uint4 &b, unsigned long long &A, unsigned long long &B)
-{
-    asm("{\n.reg .b64 l0, l1, v0, v1, i0, i1;\n"
-        "mov.b64 l0, {%2, %2};\n"
-        "mov.b64 i0, {%3, %3};\n"
-        "mov.b64 v0, {%6, %7};\n"
-        "fma.rn.f32x2 %0, l0, v0, %0;\n"
-        "fma.rn.f32x2 %1, i0, v0, %1;\n"
-        "mov.b64 l1, {%4, %4};\n"
-        "mov.b64 i1, {%5, %5};\n"
-        "mov.b64 v1, {%8, %9};\n"
-        "fma.rn.f32x2 %0, l1, v1, %0;\n"
-        "fma.rn.f32x2 %1, i1, v1, %1;\n}"
-        : "+l"(A), "+l"(B) : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w));
-}
 
 // wait for a phase, return 0 as a value the dependent shared loads use in their address
 __device__ __forceinline__ uint32_t mbar_wait_dep(uint32_t bar, uint32_t parity)
@@ -2291,6 +2430,10 @@ cudaError_t launch_pack_t(const void *field, void *send, const KGeom &g, cudaStr
         if (id >= LL_CHAIN_ID0 && id < LL_CHAIN_ID0 + Variants<P, NV>::n) {                                       \
             *nrb = 0;                                                                                             \
             return dispatch_llchain<P, NV, 0>(id - LL_CHAIN_ID0, a, n, base, s, sms);                             \
+        }                                                                                                         \
+        if (id == LLWARP_CHAIN_ID) {                                                                              \
+            *nrb = 0;                                                                                             \
+            return launch_llwarp_t<P, NV>(a, n, base, s, sms);                                                    \
         }                                                                                                         \
         if (id == CPUSH_CHAIN_ID) {                                                                               \
             *nrb = 0;                                                                                             \

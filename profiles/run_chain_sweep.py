@@ -44,7 +44,7 @@ for _ in range(5):
     r0, r1 = r1, r0
 ref = r0.export()
 names = ctx.variants(a.prec)
-cands = a.variants if a.variants else [4000, 1000, 1001] + [2000 + i for i in range(1, len(names))] + list(range(3001, 3007))
+cands = a.variants if a.variants else [5000, 4000, 1000, 1001] + [2000 + i for i in range(1, len(names))] + list(range(3001, 3007))
 V = int(np.prod(a.dims))
 rows = []
 for vid in cands:

@@ -437,6 +437,34 @@ def test_cpush_chain_forced(dims, n):
                 assert rel_l2(other.export(), prev) <= tol, (dims, dag)
 
 
+@pytest.mark.parametrize("dims,nvec,n", [((2, 2, 2, 2), 24, 7), ((2, 2, 2, 2), 24, 1), ((2, 2, 2, 2), 24, 2),
+                                         ((2, 1, 2, 2), 24, 6), ((3, 3, 1, 1), 24, 5), ((3, 2, 2, 2), 24, 4),
+                                         ((1, 1, 1, 1), 24, 3), ((2, 2, 2, 2), 32, 4), ((2, 1, 2, 3), 32, 5)])
+def test_llwarp_chain_forced(dims, nvec, n):
+    """LL-warp chain (variant 5000; fp32): one warp per 4 rows with all nine hops in registers;
+    record sharing for extents 1 and 2, apply and dagger, last and previous iterate against the
+    oracle, repeated launches (epoch continuity)."""
+    N = 2 * nvec
+    Lh = synth.links(dims, N, kind="hermitian", scale_log2=-4)
+    v = synth.vector(dims, N)
+    ctx = cd.Context(dims, nvec)
+    ctx.set_option(cd.CD_OPT_VARIANT, 5000)
+    L = ctx.links_upload(Lh, "fp32")
+    x, y = ctx.field("fp32"), ctx.field("fp32")
+    tol = 2e-6 * n
+    for dag in (False, True):
+        ref, prev = v, v
+        for _ in range(n):
+            prev, ref = ref, (oracle.adjoint if dag else oracle.apply)(dims, Lh, ref)
+        for _rep in range(2):
+            x.import_(v)
+            L.apply_chain(x, y, n, dagger=dag)
+            last, other = (y, x) if n % 2 else (x, y)
+            assert rel_l2(last.export(), ref) <= tol, (dims, dag)
+            if n > 1:
+                assert rel_l2(other.export(), prev) <= tol, (dims, dag)
+
+
 def test_cpush_chain_unsupported_shapes():
     """Variant 4000 refuses lattices above one 16-CTA cluster, a single site (st.async needs a
     cluster of >= 2 CTAs), fp16 storage and Nvec 32."""
@@ -550,7 +578,7 @@ def test_chain_tuner_reports_choice():
     assert ctx.chosen_chain_variant("fp32") == -1
     L.apply_chain(x, y, 4)
     vid = ctx.chosen_chain_variant("fp32")
-    assert vid in (1000, 4000) or 2000 <= vid < 2000 + len(ctx.variants("fp32")) or 3001 <= vid < 3007 \
+    assert vid in (1000, 4000, 5000) or 2000 <= vid < 2000 + len(ctx.variants("fp32")) or 3001 <= vid < 3007 \
         or 0 <= vid < len(ctx.variants("fp32"))
 
 

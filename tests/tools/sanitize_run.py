@@ -20,7 +20,7 @@ for prec in ("fp32", "fp16"):
             L.apply(b, a)
             L.apply_dagger(a, b)
     if which in ("all", "chain"):
-        for v in [4000, 1000, 2001, 2002, 1, 3001, 3002, 3003]:
+        for v in [5000, 4000, 1000, 2001, 2002, 1, 3001, 3002, 3003]:
             ctx.set_option(cd.CD_OPT_VARIANT, v)
             try:
                 L.apply_chain(a, b, 3)
