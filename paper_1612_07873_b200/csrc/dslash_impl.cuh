@@ -128,11 +128,50 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
         // `slot` (launch % 4) was reset by the last CTA of the launch 4 before this one, which
         // completed before this launch's predecessor did (stream order / griddepcontrol.wait).
         if (lane == 0) {
-            pdl_wait();   // `in` is written by the previous kernel in the stream
             int stage = 0;
             uint32_t phase = 0;
+            // The first site of CTA b is site b (static); its link matrices do not depend on the
+            // previous kernel, so their bulk copies go out BEFORE griddepcontrol.wait and overlap
+            // that kernel's tail (PDL).  Its vector records (`in`, written by the previous
+            // kernel) follow the wait.  Later sites come from the ticket counter (site =
+            // gridDim.x + ticket).
+            const bool pre = (G <= S) && (int)blockIdx.x < V;
+            if (pre) {
+                const int site = (int)blockIdx.x;
+                int x[4];
+                decode(a.g, site, x);
+                const unsigned char *lsite = links + (size_t)site * 9 * Q::MREC;
+                for (int gi = 0; gi < G; gi++) {
+                    int nvc = 0;
+#pragma unroll
+                    for (int j = 0; j < MPS; j++) nvc += !(a.halo && remote_hop(a.g, x, gi * MPS + j));
+                    unsigned char *st = stages + (size_t)gi * RC::STAGE;
+                    mbar_arrive_expect_tx(&full[gi], MPS * Q::MREC + nvc * Q::VREC + (gi == 0 ? 4 : 0));
+                    if (gi == 0) st_async_u32(&siteq[gi], (uint32_t)site, &full[gi]);
+                    bulk_g2s(st, lsite + (size_t)gi * MPS * Q::MREC, MPS * Q::MREC, &full[gi]);
+                }
+                pdl_wait();   // `in` is written by the previous kernel in the stream
+                for (int gi = 0; gi < G; gi++) {
+                    unsigned char *st = stages + (size_t)gi * RC::STAGE;
+#pragma unroll
+                    for (int j = 0; j < MPS; j++) {
+                        const int k = gi * MPS + j;
+                        if (a.halo && remote_hop(a.g, x, k)) continue;
+                        bulk_g2s(st + RC::VOFF + j * Q::VREC, in + (size_t)neighbour(a.g, x, site, k) * Q::VREC,
+                                 Q::VREC, &full[gi]);
+                    }
+                }
+                stage = G % S;
+                phase = (G == S) ? 1u : 0u;
+            } else {
+                pdl_wait();   // `in` is written by the previous kernel in the stream
+            }
+            // without the prefetch (a site needs more stages than the ring holds) the static
+            // first site goes through the loop like any other
+            bool first = !pre && (int)blockIdx.x < V;
             for (;;) {
-                const int site = atomicAdd(tickets, 1);
+                const int site = first ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(tickets, 1);
+                first = false;
                 if (site >= V) {   // sentinel stage: tells the consumers to stop
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&full[stage], 4);
