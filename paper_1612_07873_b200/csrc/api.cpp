@@ -991,16 +991,19 @@ static int resolve_variant(cd_context *c, cd_precision p, int dag, const ApplyAr
             CUDA_TRY(cudaEventCreate(&e1), "event");
             float best = 1e30f;
             const int reps = c->V >= 2048 ? 3 : 20;
-            // time `r` launches of variant id2; < 0 if it cannot run here
+            // time `r` back-to-back launches of variant id2 with the production PDL setting (a
+            // variant that overlaps its ramp with the previous launch's tail is timed as it will
+            // run in a chain of applies); < 0 if it cannot run here
+            const bool tpdl = c->pdl != 0;
             auto timeit = [&](int id2, int r) -> float {
                 cudaError_t e = cudaSuccess;
-                for (int w = 0; w < 2 && e == cudaSuccess; w++) e = launch_next(c, p, id2, a, s, false);
+                for (int w = 0; w < 2 && e == cudaSuccess; w++) e = launch_next(c, p, id2, a, s, tpdl);
                 if (e != cudaSuccess) {
                     cudaGetLastError();
                     return -1.f;
                 }
                 cudaEventRecord(e0, s);
-                for (int rr = 0; rr < r && e == cudaSuccess; rr++) e = launch_next(c, p, id2, a, s, false);
+                for (int rr = 0; rr < r && e == cudaSuccess; rr++) e = launch_next(c, p, id2, a, s, tpdl);
                 cudaEventRecord(e1, s);
                 if (e != cudaSuccess || cudaEventSynchronize(e1) != cudaSuccess) {
                     cudaGetLastError();
