@@ -1843,11 +1843,10 @@ cudaError_t launch_cluster_chain_t(const ApplyArgs &a, int n, cudaStream_t s)
 template <int NV>
 struct CPushCfg {
     static constexpr int N = 2 * NV;
-    static constexpr int LD = 8;              // lanes per row (dot-product split)
-    static constexpr int RPW = 32 / LD;       // rows per warp
-    static constexpr int NW = N / RPW;        // warps (producer warps per slot phase)
-    static constexpr int THREADS = 32 * NW;
-    static constexpr int LC = N / (2 * LD);   // 16-B chunks per lane per hop row
+    static constexpr int NT = 4;              // warp triples (12 warps)
+    static constexpr int RPT = N / NT;        // rows per triple (12): 4 row groups of 3 rows
+    static constexpr int THREADS = 32 * 3 * NT;
+    static_assert(NV == 24, "layout: 24 chunks per row = 3 warps x 8 lanes, 16 row groups of 3 rows");
 };
 
 // wait for a phase, return 0 as a value the dependent shared loads use in their address
@@ -1906,38 +1905,44 @@ __device__ __forceinline__ void mbar_arrive_expect_tx_remote(uint32_t bar, uint3
                  : "memory");
 }
 
-template <int NV, bool TRACE>
+template <int NV, bool TRACE, bool ALL2>
 __global__ void __launch_bounds__(CPushCfg<NV>::THREADS, 1) dslash_cpush(ApplyArgs a, int n)
 {
     using Q = Cfg<CD_FP32, NV>;
     using K = CPushCfg<NV>;
-    __shared__ __align__(16) float2 rec[2][9][K::N];   // receive slots by epoch parity
-    __shared__ __align__(8) uint64_t bar[2][2];         // [parity][0: own slot 8, 1: all remote slots]
+    __shared__ __align__(16) float2 rec[2][9][K::N];          // receive slots by epoch parity
+    __shared__ __align__(8) uint64_t bar[2][2];                // [parity][0: own slot 8, 1: all remote slots]
+    __shared__ float part[2][K::NT][3][K::RPT * 2];            // [parity][triple][member][row of triple, re/im]
 
     const int site = (int)cluster_rank();   // grid == one cluster of V CTAs
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int row = warp * K::RPW + lane / K::LD, d = lane % K::LD;
+    const int tw = warp / 3, m = warp - 3 * tw;                // triple, member (chunk block)
+    const int rq = lane >> 3, d = lane & 7;
+    const int rg = tw * 4 + rq;                                // row group: rows 3 rg .. 3 rg + 2
+    const int q = m * 8 + d;                                   // the 16-B chunk (complex 2q, 2q+1) of this lane
     const unsigned char *links = static_cast<const unsigned char *>(a.links);
     unsigned char *const g0 = const_cast<unsigned char *>(static_cast<const unsigned char *>(a.in));
     unsigned char *const g1 = static_cast<unsigned char *>(a.out);
     int x[4];
     decode(a.g, site, x);
 
-    // this lane's push destination (index d into: own slot 8, then per mu the -mu / +mu readers)
-    int dst_cta = -1, dst_slot = 0;
+    // push role after the triple reduction: row (of the triple's 12) r12, destination dd
+    const int tid3 = m * 32 + lane, r12 = tid3 >> 3, dd = tid3 & 7;
+    const int prow = tw * K::RPT + r12;
+    int dst_cta = -1, dst_slot = 0;   // destination dd: own slot 8, then per mu the -mu / +mu readers
     {
         int i = 0;
-        if (d == i) dst_cta = site, dst_slot = 8;
+        if (dd == i) dst_cta = site, dst_slot = 8;
         i++;
 #pragma unroll
         for (int mu = 0; mu < 4; mu++) {
             const int L = sel4(a.g.L, mu);
             if (L >= 2) {   // x - mu reads us through hop 2mu (L = 2: x - mu = x + mu, one push)
-                if (d == i) dst_cta = neighbour(a.g, x, site, 2 * mu + 1), dst_slot = 2 * mu;
+                if (dd == i) dst_cta = neighbour(a.g, x, site, 2 * mu + 1), dst_slot = 2 * mu;
                 i++;
             }
             if (L >= 3) {   // x + mu reads us through hop 2mu + 1
-                if (d == i) dst_cta = neighbour(a.g, x, site, 2 * mu), dst_slot = 2 * mu + 1;
+                if (dd == i) dst_cta = neighbour(a.g, x, site, 2 * mu), dst_slot = 2 * mu + 1;
                 i++;
             }
         }
@@ -1946,7 +1951,7 @@ __global__ void __launch_bounds__(CPushCfg<NV>::THREADS, 1) dslash_cpush(ApplyAr
     const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(&bar[0][0]);
     uint32_t dst_rec = 0, dst_bar = 0;   // cluster addresses of slot dst_slot / its barrier, parity 0
     if (dst_cta >= 0) {
-        dst_rec = mapa_u32(rec_s + (uint32_t)(dst_slot * K::N + row) * 8u, (unsigned)dst_cta);
+        dst_rec = mapa_u32(rec_s + (uint32_t)(dst_slot * K::N + prow) * 8u, (unsigned)dst_cta);
         dst_bar = mapa_u32(bar_s + (dst_slot == 8 ? 0u : 8u), (unsigned)dst_cta);
     }
     // the slot each hop reads (kseq order: X first), and the number of remote producers
@@ -1964,25 +1969,25 @@ __global__ void __launch_bounds__(CPushCfg<NV>::THREADS, 1) dslash_cpush(ApplyAr
         slotmask |= (uint64_t)s << (4 * i);
     }
 
-    uint4 Lc[9][K::LC];
+    uint32_t hoff[8];   // byte offset of the receive slot of hop position i = 1..8 (k = i - 1)
 #pragma unroll
-    for (int i = 0; i < 9; i++) {
-        const unsigned char *m = links + ((size_t)site * 9 + kseq(i)) * Q::MREC + row * Q::ROWB;
+    for (int i = 1; i < 9; i++)   // ALL2 (every extent 2, the 2^4 coarsest grid): compile-time slots 2 mu
+        hoff[i - 1] = (ALL2 ? (uint32_t)((i - 1) & ~1) : ((uint32_t)(slotmask >> (4 * i)) & 15u)) * (uint32_t)(K::N * 8);
+    // links: chunk q of rows 3 rg + j, all nine hops (108 floats per thread)
+    uint4 Lc[9][3];
+    const bool negq = a.dagger && q * 2 >= NV;   // tau3 on the input folded into the links
 #pragma unroll
-        for (int c = 0; c < K::LC; c++) Lc[i][c] = ld_stream(m + (d + K::LD * c) * 16);
-    }
-    if (a.dagger) {   // tau3 on the input folded into the register-resident links (chunks q >= Nvec/2)
+    for (int i = 0; i < 9; i++)
 #pragma unroll
-        for (int i = 0; i < 9; i++)
-#pragma unroll
-            for (int c = 0; c < K::LC; c++)
-                if ((d + K::LD * c) * 2 >= NV) Lc[i][c] = neg_chunk<false>(Lc[i][c]);
-    }
-    const float osign = (a.dagger && row >= NV) ? -1.0f : 1.0f;
-    if (threadIdx.x == 0) {   // own: 12 producer warps; remote: 12 per producing neighbour
+        for (int j = 0; j < 3; j++) {
+            uint4 l = ld_stream(links + ((size_t)site * 9 + kseq(i)) * Q::MREC + (3 * rg + j) * Q::ROWB + q * 16);
+            Lc[i][j] = negq ? neg_chunk<false>(l) : l;
+        }
+    const float osign = (a.dagger && prow >= NV) ? -1.0f : 1.0f;
+    if (threadIdx.x == 0) {   // own: 4 producer triples; remote: 4 per producing neighbour
         for (int p = 0; p < 2; p++) {
-            mbar_init(&bar[p][0], K::NW);
-            mbar_init(&bar[p][1], K::NW * (nremote > 0 ? nremote : 1));
+            mbar_init(&bar[p][0], K::NT);
+            mbar_init(&bar[p][1], K::NT * (nremote > 0 ? nremote : 1));
         }
         fence_mbar_init();
     }
@@ -1993,52 +1998,88 @@ __global__ void __launch_bounds__(CPushCfg<NV>::THREADS, 1) dslash_cpush(ApplyAr
         const int par = t & 1;
         const bool trt = TRACE && tr && t < 1024 && warp < 8;
         if (trt) tr[(4 * warp) * 1024 + t] = clock64();
-        unsigned long long A = 0ull, B = 0ull;   // packed (x, y) accumulators, see cmac2x
+        unsigned long long A[3] = {0ull, 0ull, 0ull}, B[3] = {0ull, 0ull, 0ull};   // packed, see cmac2x
         if (t == 0) {   // the input is ready at launch
 #pragma unroll
             for (int i = 0; i < 9; i++) {
-                const unsigned char *src = g0 + (size_t)neighbour(a.g, x, site, kseq(i)) * Q::VREC;
+                const uint4 v = ld_nc(g0 + (size_t)neighbour(a.g, x, site, kseq(i)) * Q::VREC + q * 16);
 #pragma unroll
-                for (int c = 0; c < K::LC; c++) cmac2x(Lc[i][c], ld_nc(src + (d + K::LD * c) * 16), A, B);
+                for (int j = 0; j < 3; j++) cmac2x(Lc[i][j], v, A[j], B[j]);
             }
         } else {
             const uint32_t ph = ((t - 1) >> 1) & 1;
-            // X (own slot, lands first) while the remote records are in flight, then one wait
-            // for all remote slots.  Records arrive through st.async: the shared loads take a
-            // zero from the wait as an address operand so they cannot move above it.
             uint32_t z = mbar_wait_dep(bar_s + (uint32_t)(par * 2) * 8u, ph);
             if (TRACE && trt) tr[(4 * warp + 1) * 1024 + t] = clock64();
+            {   // X: own slot 8, while the remote records are in flight
+                const uint4 v = lds128_dep(rec_s + (uint32_t)((par * 9 + 8) * K::N) * 8u + z + (uint32_t)q * 16u);
 #pragma unroll
-            for (int i = 0; i < 9; i++) {
-                const uint32_t s = (uint32_t)(slotmask >> (4 * i)) & 15u;
-                if (i == 1 && nremote > 0) {
-                    z = mbar_wait_dep_after(bar_s + (uint32_t)(par * 2 + 1) * 8u, ph,
-                                            __uint_as_float((uint32_t)A ^ (uint32_t)B));
-                    if (TRACE && trt) tr[(32 + warp) * 1024 + t] = clock64() + z;
-                }
-                const uint32_t src = rec_s + (uint32_t)((par * 9 + s) * K::N) * 8u + z;
-#pragma unroll
-                for (int c = 0; c < K::LC; c++) cmac2x(Lc[i][c], lds128_dep(src + (uint32_t)(d + K::LD * c) * 16u), A, B);
+                for (int j = 0; j < 3; j++) cmac2x(Lc[0][j], v, A[j], B[j]);
             }
-        }
-        float re = __uint_as_float((uint32_t)A) - __uint_as_float((uint32_t)(B >> 32));
-        float im = __uint_as_float((uint32_t)(A >> 32)) + __uint_as_float((uint32_t)B);
-        if (trt) tr[(4 * warp + 2) * 1024 + t] = clock64();
+            if (nremote > 0) {
+                z = mbar_wait_dep_after(bar_s + (uint32_t)(par * 2 + 1) * 8u, ph, __uint_as_float((uint32_t)A[0] ^ (uint32_t)B[2]));
+                if (TRACE && trt) tr[(32 + warp) * 1024 + t] = clock64() + z;
+            }
+            // per-thread part of the address in one register, per-hop part uniform (slot offsets
+            // precomputed): one LDS [R + UR] per hop
+            const uint32_t tb = rec_s + (uint32_t)q * 16u + z + (uint32_t)(par * 9 * K::N * 8);
+            uint4 v[8];
 #pragma unroll
-        for (int m = K::LD / 2; m >= 1; m >>= 1) {
-            re += shfl_xor(re, m);
-            im += shfl_xor(im, m);
+            for (int i = 1; i < 9; i++) v[i - 1] = lds128_dep(tb + hoff[i - 1]);
+#pragma unroll
+            for (int i = 1; i < 9; i++)
+#pragma unroll
+                for (int j = 0; j < 3; j++) cmac2x(Lc[i][j], v[i - 1], A[j], B[j]);
         }
-        re *= osign;
-        im *= osign;
-        if (t + 1 < n && dst_cta >= 0) {
-            const uint32_t off = (uint32_t)(par ^ 1);
-            st_async_f2(dst_rec + off * 9u * K::N * 8u, re, im, dst_bar + off * 16u);
-            if (lane < K::LD) mbar_arrive_expect_tx_remote(dst_bar + off * 16u, K::RPW * 8u);
+        if (trt) tr[(4 * warp + 2) * 1024 + t] = clock64();
+        // 6 values (re, im of rows 3 rg + j) summed over the 8 lanes d by a reduce-scatter:
+        // lane d ends with value d (values 6, 7 are padding)
+        float w[8];
+#pragma unroll
+        for (int j = 0; j < 3; j++) {
+            w[2 * j] = __uint_as_float((uint32_t)A[j]) - __uint_as_float((uint32_t)(B[j] >> 32));
+            w[2 * j + 1] = __uint_as_float((uint32_t)(A[j] >> 32)) + __uint_as_float((uint32_t)B[j]);
         }
-        if (t >= n - 2 && d == 0) {   // the caller sees the last two iterates (x / y ping-pong)
-            unsigned char *gout = (t & 1) ? g0 : g1;
-            reinterpret_cast<float2 *>(gout + (size_t)site * Q::VREC)[row] = make_float2(re, im);
+        w[6] = 0.0f;
+        w[7] = 0.0f;
+        {
+            const bool hi = d & 4;   // keep values 4..7 (hi) or 0..3
+            float u[4];
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                const float send = hi ? w[e] : w[e + 4];
+                const float keep = hi ? w[e + 4] : w[e];
+                u[e] = keep + shfl_xor(send, 4);
+            }
+            const bool h2 = d & 2;   // keep u[2..3] or u[0..1]
+            float u2[2];
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+                const float send = h2 ? u[e] : u[e + 2];
+                const float keep = h2 ? u[e + 2] : u[e];
+                u2[e] = keep + shfl_xor(send, 2);
+            }
+            const bool h1 = d & 1;
+            const float send = h1 ? u2[0] : u2[1];
+            const float keep = h1 ? u2[1] : u2[0];
+            const float r = keep + shfl_xor(send, 1);   // value index d
+            if (d < 6) part[par][tw][m][rq * 6 + d] = r;   // row 3 rq + d / 2 of the triple, re/im = d & 1
+        }
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + tw), "r"(96) : "memory");   // the triple's three members
+        {
+            const float *pp = &part[par][tw][0][2 * r12];
+            float yr = pp[0] + pp[K::RPT * 2] + pp[2 * K::RPT * 2];
+            float yi = pp[1] + pp[K::RPT * 2 + 1] + pp[2 * K::RPT * 2 + 1];
+            yr *= osign;
+            yi *= osign;
+            if (t + 1 < n && dst_cta >= 0) {
+                const uint32_t off = (uint32_t)(par ^ 1);
+                st_async_f2(dst_rec + off * 9u * K::N * 8u, yr, yi, dst_bar + off * 16u);
+                if (r12 == 0) mbar_arrive_expect_tx_remote(dst_bar + off * 16u, K::RPT * 8u);
+            }
+            if (t >= n - 2 && dd == 0) {   // the caller sees the last two iterates (x / y ping-pong)
+                unsigned char *gout = (t & 1) ? g0 : g1;
+                reinterpret_cast<float2 *>(gout + (size_t)site * Q::VREC)[prow] = make_float2(yr, yi);
+            }
         }
         if (trt) tr[(4 * warp + 3) * 1024 + t] = clock64();
     }
@@ -2054,13 +2095,16 @@ cudaError_t launch_cpush_t(const ApplyArgs &a, int n, cudaStream_t s)
         using K = CPushCfg<NV>;
         // st.async needs a real cluster (>= 2 CTAs); one cluster holds at most 16 CTAs
         if (a.g.V < 2 || a.g.V > 16 || a.halo || a.g.split) return cudaErrorNotSupported;
-        const void *fn = a.trace ? (const void *)dslash_cpush<NV, true> : (const void *)dslash_cpush<NV, false>;
+        const bool all2 = a.g.L[0] == 2 && a.g.L[1] == 2 && a.g.L[2] == 2 && a.g.L[3] == 2;
+        const void *fns[2][2] = {{(const void *)dslash_cpush<NV, false, false>, (const void *)dslash_cpush<NV, false, true>},
+                                 {(const void *)dslash_cpush<NV, true, false>, (const void *)dslash_cpush<NV, true, true>}};
+        const void *fn = fns[a.trace ? 1 : 0][all2 ? 1 : 0];
         static bool attr = false;
         if (!attr) {
-            cudaError_t e = cudaFuncSetAttribute(dslash_cpush<NV, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-            if (e == cudaSuccess)
-                e = cudaFuncSetAttribute(dslash_cpush<NV, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-            if (e != cudaSuccess) return e;
+            for (int i = 0; i < 4; i++) {
+                cudaError_t e = cudaFuncSetAttribute(fns[i >> 1][i & 1], cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                if (e != cudaSuccess) return e;
+            }
             attr = true;
         }
         cudaLaunchConfig_t cfg = {};
