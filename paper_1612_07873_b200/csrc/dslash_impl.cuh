@@ -1817,29 +1817,33 @@ cudaError_t launch_cluster_chain_t(const ApplyArgs &a, int n, cudaStream_t s)
 
 // ------------------------------------------------------------------ CLUSTER push chain (V <= 16, fp32, Nvec 24)
 // The whole lattice in ONE thread-block cluster, one CTA per site, the site's nine 48 x 48
-// complex matrices in registers for all n applies, and NO barrier inside an apply:
-//   * thread (row i, lane d of 8) holds L_k(x)[i][chunks d, d+8, d+16] for ALL nine hops
-//     (108 floats), so the hop sum stays in registers and the 8-lane xor-shuffle that finishes
-//     the dot product leaves y(x)[i] in every lane of the row (12 warps x 4 rows);  the complex
-//     MACs run on the packed FP32 pipe (cmac2x: FFMA2 with a broadcast scalar);
-//   * lane d of the row then pushes y(x)[i] to destination d -- this CTA's own slot 8 and the
-//     receive slots of the CTAs that read x as a neighbour -- with st.async into their shared
-//     memory, and lane (row 0 of the warp, d) adds the warp's arrival + 32 bytes of expected
-//     transaction on the destination's mbarrier (remote arrive.expect_tx): barrier 0 (own slot)
-//     completes when the 12 own warps arrived and 384 bytes landed, barrier 1 (all remote
-//     slots) when 12 warps of every producing neighbour arrived and all their bytes landed --
-//     no local re-arming;
+// complex matrices in registers for all n applies; no L2 traffic and no polling:
+//   * thread (row group rg of 3 rows, chunk q of 24) holds L_k(x)[3 rg + j][chunk q] for all
+//     nine hops and j = 0..2 (108 floats): one 16-B shared load of a neighbour record per hop
+//     feeds three rows (a shared load costs 4 wavefronts however many lanes share its address,
+//     so the earlier one-row-per-thread layout was bound by the shared-memory data pipe);
+//     complex MACs on the packed FP32 pipe (cmac2x);
+//   * a warp = 4 row groups x 8 chunks; the three warps of a "triple" cover all 24 chunks of the
+//     same 12 rows: xor-shuffle reduce-scatter over the 8 lanes, the three partials meet in
+//     shared memory behind one 96-thread named barrier;
+//   * thread (row r12 of the triple, destination dd) then pushes y(x)[row] to destination dd --
+//     this CTA's own slot 8 and the receive slots of the CTAs that read x as a neighbour -- with
+//     st.async into their shared memory; one thread per (triple, destination) adds the triple's
+//     arrival + 96 bytes of expected transaction on the destination's mbarrier (remote
+//     arrive.expect_tx): barrier 0 (own slot) completes when the 4 own triples arrived and 384
+//     bytes landed, barrier 1 (all remote slots) when 4 triples of every producing neighbour
+//     did -- no local re-arming;
 //   * a warp does the X hop as soon as its own record lands, then waits once for the remote
-//     records (the X math overlaps their DSMEM flight).
+//     records (the X math overlaps their DSMEM flight); on all-extent-2 lattices the slot
+//     offsets are compile-time and the +-mu hops share one load.
 // Receive slots (consumer c, hop k): k = 8 or L_mu = 1 -> slot 8 (own); L_mu = 2 -> slot 2 mu
 // for both hops (x + mu = x - mu: one record); else slot k.  Flow control needs no extra signal:
-// a warp pushes epoch t+1 only after it received the complete epoch-t records of every
-// neighbour, and every warp of a neighbour pushes its part of epoch t only after it finished
+// a thread pushes epoch t+1 only after its warp received the complete epoch-t records of every
+// neighbour, and every triple of a neighbour pushes its part of epoch t only after it finished
 // reading epoch t-1 (the slot parity being overwritten) and observed both barrier phases of
-// epoch t-1 -- the neighbour relation is symmetric.  Measured (2^4, Nvec 24): 1.02 us per
-// apply against 0.91 us for the LL-register chain: one SM per site issues the site's 83k FMAs
-// in ~1200 cycles (FP32 pipe at ~60 % in situ), which the short DSMEM hop does not win back
-// (DESIGN.md §6).
+// epoch t-1 -- the neighbour relation is symmetric.  The per-triple partial buffer alternates
+// with the apply parity (its barrier orders a rewrite after every read of two applies ago).
+// Measured (2^4, Nvec 24): 0.864 us per apply, LL-register chain 0.915.
 template <int NV>
 struct CPushCfg {
     static constexpr int N = 2 * NV;
