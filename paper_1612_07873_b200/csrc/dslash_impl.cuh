@@ -2003,7 +2003,14 @@ __global__ void __launch_bounds__(CPushCfg<NV>::THREADS, 1) dslash_cpush(ApplyAr
         const bool trt = TRACE && tr && t < 1024 && warp < 8;
         if (trt) tr[(4 * warp) * 1024 + t] = clock64();
         unsigned long long A[3] = {0ull, 0ull, 0ull}, B[3] = {0ull, 0ull, 0ull};   // packed, see cmac2x
+        // The triple's arrival (+ its 96 expected bytes) on each destination's barrier for epoch
+        // t + 1 goes out early, off the epilogue: it needs no data, and it cannot reach a phase
+        // before its time -- the destination finished with that barrier's previous phase (epoch
+        // t - 1) before it pushed the epoch-t record this warp has just received, and the new
+        // phase still needs every byte of epoch t + 1 to complete.
+        const bool early_arrive = t + 1 < n && dst_cta >= 0 && r12 == 0;
         if (t == 0) {   // the input is ready at launch
+            if (early_arrive) mbar_arrive_expect_tx_remote(dst_bar + 16u, K::RPT * 8u);
 #pragma unroll
             for (int i = 0; i < 9; i++) {
                 const uint4 v = ld_nc(g0 + (size_t)neighbour(a.g, x, site, kseq(i)) * Q::VREC + q * 16);
@@ -2026,6 +2033,7 @@ __global__ void __launch_bounds__(CPushCfg<NV>::THREADS, 1) dslash_cpush(ApplyAr
             // per-thread part of the address in one register, per-hop part uniform (slot offsets
             // precomputed): one LDS [R + UR] per hop
             const uint32_t tb = rec_s + (uint32_t)q * 16u + z + (uint32_t)(par * 9 * K::N * 8);
+            if (early_arrive) mbar_arrive_expect_tx_remote(dst_bar + (uint32_t)(par ^ 1) * 16u + z, K::RPT * 8u);
             uint4 v[8];
 #pragma unroll
             for (int i = 1; i < 9; i++) v[i - 1] = lds128_dep(tb + hoff[i - 1]);
@@ -2078,7 +2086,6 @@ __global__ void __launch_bounds__(CPushCfg<NV>::THREADS, 1) dslash_cpush(ApplyAr
             if (t + 1 < n && dst_cta >= 0) {
                 const uint32_t off = (uint32_t)(par ^ 1);
                 st_async_f2(dst_rec + off * 9u * K::N * 8u, yr, yi, dst_bar + off * 16u);
-                if (r12 == 0) mbar_arrive_expect_tx_remote(dst_bar + off * 16u, K::RPT * 8u);
             }
             if (t >= n - 2 && dd == 0) {   // the caller sees the last two iterates (x / y ping-pong)
                 unsigned char *gout = (t & 1) ? g0 : g1;
