@@ -1843,7 +1843,7 @@ cudaError_t launch_cluster_chain_t(const ApplyArgs &a, int n, cudaStream_t s)
 // reading epoch t-1 (the slot parity being overwritten) and observed both barrier phases of
 // epoch t-1 -- the neighbour relation is symmetric.  The per-triple partial buffer alternates
 // with the apply parity (its barrier orders a rewrite after every read of two applies ago).
-// Measured (2^4, Nvec 24): 0.864 us per apply, LL-register chain 0.915.
+// Measured (2^4, Nvec 24): 0.841 us per apply = 40.3 % of 8 TB/s, LL-register chain 0.915-0.934.
 template <int NV>
 struct CPushCfg {
     static constexpr int N = 2 * NV;
@@ -1916,7 +1916,7 @@ __global__ void __launch_bounds__(CPushCfg<NV>::THREADS, 1) dslash_cpush(ApplyAr
     using K = CPushCfg<NV>;
     __shared__ __align__(16) float2 rec[2][9][K::N];          // receive slots by epoch parity
     __shared__ __align__(8) uint64_t bar[2][2];                // [parity][0: own slot 8, 1: all remote slots]
-    __shared__ float part[2][K::NT][3][K::RPT * 2];            // [parity][triple][member][row of triple, re/im]
+    __shared__ __align__(16) float part[2][K::NT][3][K::RPT * 2];   // [parity][triple][member][row of triple, re/im]
 
     const int site = (int)cluster_rank();   // grid == one cluster of V CTAs
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1979,15 +1979,16 @@ __global__ void __launch_bounds__(CPushCfg<NV>::THREADS, 1) dslash_cpush(ApplyAr
         hoff[i - 1] = (ALL2 ? (uint32_t)((i - 1) & ~1) : ((uint32_t)(slotmask >> (4 * i)) & 15u)) * (uint32_t)(K::N * 8);
     // links: chunk q of rows 3 rg + j, all nine hops (108 floats per thread)
     uint4 Lc[9][3];
-    const bool negq = a.dagger && q * 2 >= NV;   // tau3 on the input folded into the links
+    // dagger: tau3 on the input (columns of chunks q >= Nvec/2) and on the output (rows >= Nvec)
+    // folded into the register-resident links -- no sign work per apply
 #pragma unroll
     for (int i = 0; i < 9; i++)
 #pragma unroll
         for (int j = 0; j < 3; j++) {
             uint4 l = ld_stream(links + ((size_t)site * 9 + kseq(i)) * Q::MREC + (3 * rg + j) * Q::ROWB + q * 16);
-            Lc[i][j] = negq ? neg_chunk<false>(l) : l;
+            const bool neg = a.dagger && ((q * 2 >= NV) != (3 * rg + j >= NV));
+            Lc[i][j] = neg ? neg_chunk<false>(l) : l;
         }
-    const float osign = (a.dagger && prow >= NV) ? -1.0f : 1.0f;
     if (threadIdx.x == 0) {   // own: 4 producer triples; remote: 4 per producing neighbour
         for (int p = 0; p < 2; p++) {
             mbar_init(&bar[p][0], K::NT);
@@ -2081,8 +2082,6 @@ __global__ void __launch_bounds__(CPushCfg<NV>::THREADS, 1) dslash_cpush(ApplyAr
             const float *pp = &part[par][tw][0][2 * r12];
             float yr = pp[0] + pp[K::RPT * 2] + pp[2 * K::RPT * 2];
             float yi = pp[1] + pp[K::RPT * 2 + 1] + pp[2 * K::RPT * 2 + 1];
-            yr *= osign;
-            yi *= osign;
             if (t + 1 < n && dst_cta >= 0) {
                 const uint32_t off = (uint32_t)(par ^ 1);
                 st_async_f2(dst_rec + off * 9u * K::N * 8u, yr, yi, dst_bar + off * 16u);
