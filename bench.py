@@ -240,8 +240,8 @@ def extras(cd, perfmodel, torch, other_prec="fp16"):
     vid = ctx.chosen_chain_variant("fp32")
     out["2^4_fp32_chain"] = {"us_per_apply": round(us, 3), "GBs_effective": round(gbs, 1),
                              "pct_of_8tbs": round(100 * gbs / 8000, 1), "variant": vid,
-                             "note": "coarse_dslash_apply_chain (one persistent kernel, L2/on-chip resident; "
-                                     "variant 3001+: LL-register chain)"}
+                             "note": "coarse_dslash_apply_chain (one persistent kernel, on-chip resident; "
+                                     "variant 4000: cluster push chain, 3001+: LL-register chain)"}
     del L, a, b, ctx
     # the 8^4 workload with the other storage precision
     ctx = cd.Context(WORKLOAD["dims"], nvec)
