@@ -410,7 +410,8 @@ def test_cluster_chain_forced(nvec, prec, n):
 
 
 @pytest.mark.parametrize("dims,n", [((2, 2, 2, 2), 7), ((2, 2, 2, 2), 1), ((2, 2, 2, 2), 2), ((2, 1, 2, 2), 6),
-                                    ((3, 3, 1, 1), 5), ((4, 2, 2, 1), 4), ((2, 1, 1, 1), 3), ((3, 1, 5, 1), 6)])
+                                    ((3, 3, 1, 1), 5), ((4, 2, 2, 1), 4), ((2, 1, 1, 1), 3), ((3, 1, 5, 1), 6),
+                                    ((4, 4, 1, 1), 5), ((16, 1, 1, 1), 3), ((1, 2, 2, 4), 4)])
 def test_cpush_chain_forced(dims, n):
     """Cluster push chain (variant 4000; fp32, Nvec 24, V <= 16): receive-slot mapping for
     extents 1 (self hop), 2 (shared +-mu slot) and >= 3 (two slots); apply and dagger, last and
