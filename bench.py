@@ -209,6 +209,9 @@ def ncu_traffic(prec, variant):
 def _events_us(torch, fn, reps):
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # a ~100 us spin kernel ahead of the start event keeps the stream busy while the host
+    # submits fn, so host launch latency does not show up as device idle time in the window
+    torch.cuda._sleep(200000)
     e0.record(s)
     fn(reps)
     e1.record(s)
@@ -235,11 +238,29 @@ def extras(cd, perfmodel, torch, other_prec="fp16"):
     a.generate()
     L.apply_chain(a, b, 8)
     torch.cuda.synchronize()
-    us = statistics.median(_events_us(torch, lambda n: L.apply_chain(a, b, n), 2000) for _ in range(3))
+    # 800 applies per launch: with links x 2^-4 the iterate grows ~1.09x per apply (1e30 after
+    # 800, finite in fp32); v is regenerated (untimed) before every timed launch
+    def chain_us(n):
+        ts = []
+        for _ in range(3):
+            a.generate()
+            torch.cuda.synchronize()
+            ts.append(_events_us(torch, lambda k: L.apply_chain(a, b, k), n))
+        return statistics.median(ts)
+
+    us = chain_us(800)
+    us200 = chain_us(200)
+    # marginal cost of one more apply inside a chain (the per-launch cost -- kernel launch, the
+    # links' one-time load, the first apply from global memory -- drops out of the slope)
+    us_marg = (us * 800 - us200 * 200) / 600
     gbs = perfmodel.metric_bytes_per_site(nvec, "fp32") * 16 / us / 1e3
     vid = ctx.chosen_chain_variant("fp32")
+    gbs_marg = perfmodel.metric_bytes_per_site(nvec, "fp32") * 16 / us_marg / 1e3
     out["2^4_fp32_chain"] = {"us_per_apply": round(us, 3), "GBs_effective": round(gbs, 1),
                              "pct_of_8tbs": round(100 * gbs / 8000, 1), "variant": vid,
+                             "applies_per_launch": 800,
+                             "us_per_apply_marginal": round(us_marg, 3),
+                             "pct_of_8tbs_marginal": round(100 * gbs_marg / 8000, 1),
                              "note": "coarse_dslash_apply_chain (one persistent kernel, on-chip resident; "
                                      "variant 4000: cluster push chain, 3001+: LL-register chain)"}
     del L, a, b, ctx

@@ -17,3 +17,5 @@ print(f"period (w0 start -> next start): {np.median(tr[0, ts + 1] - base):.0f} c
 for r, nm in sorted(names.items(), key=lambda kv: (kv[0] % 32 // 4 if kv[0] < 32 else kv[0] - 32, kv[0] >= 32 and 1.5 or kv[0] % 4)):
     d = tr[r, ts] - base
     print(f"{nm:22s} {np.median(d):8.0f}  (p10 {np.percentile(d, 10):.0f}, p90 {np.percentile(d, 90):.0f})")
+print(f"prologue: entry -> after cluster barrier {tr[38, 0] - tr[39, 0]} cycles, -> apply 0 start {tr[0, 0] - tr[39, 0]}, "
+      f"apply 1 start {tr[0, 1] - tr[39, 0]}, apply 2 start {tr[0, 2] - tr[39, 0]}")

@@ -466,6 +466,28 @@ def test_llwarp_chain_forced(dims, nvec, n):
                 assert rel_l2(other.export(), prev) <= tol, (dims, dag)
 
 
+@pytest.mark.parametrize("variant", [4000, 3002])
+def test_long_chain_matches_oracle(variant):
+    """256 chained applies in one launch: epoch / mbarrier-phase wrap-around over many applies,
+    both iterates against 256 float64 oracle applies (links x 2^-4: the norm grows ~1.09x per
+    apply, 1e9 after 256, well inside fp32); measured 6-7e-7 after 256, gate 1e-5."""
+    dims, nvec, n = (2, 2, 2, 2), 24, 256
+    N = 2 * nvec
+    Lh = synth.links(dims, N, kind="general", scale_log2=-4)
+    v = synth.vector(dims, N)
+    ref, prev = v, v
+    for _ in range(n):
+        prev, ref = ref, oracle.apply(dims, Lh, ref)
+    ctx = cd.Context(dims, nvec)
+    ctx.set_option(cd.CD_OPT_VARIANT, variant)
+    L = ctx.links_upload(Lh, "fp32")
+    x, y = ctx.field("fp32"), ctx.field("fp32")
+    x.import_(v)
+    L.apply_chain(x, y, n)
+    assert rel_l2(x.export(), ref) <= 1e-5   # n even: the last iterate is in x
+    assert rel_l2(y.export(), prev) <= 1e-5
+
+
 def test_cpush_chain_unsupported_shapes():
     """Variant 4000 refuses lattices above one 16-CTA cluster, a single site (st.async needs a
     cluster of >= 2 CTAs), fp16 storage and Nvec 32."""
