@@ -1030,12 +1030,14 @@ static int resolve_variant(cd_context *c, cd_precision p, int dag, const ApplyAr
                 }
             for (size_t i = 0; i < t1.size(); i++)
                 if (t2[i] < best) best = t2[i], v = t1[i].second;
-            // Near-ties go to the TMA ring: it moves the links without a register round trip and
+            // Near-ties on lattices whose links stream from HBM go to the TMA ring: it moves the links
+            // without a register round trip and
             // draws less power per byte, so under the sustained power cap of a long run it keeps
             // a higher SM clock (8^4 fp32, 2000 steps: 96.2 vs 98.2 us per apply for fg_kw3_wr4,
             // profiles/r01/bench_sustained_variants.txt) -- a difference the short tuning bursts
             // at full clock cannot see.
-            if (std::strncmp(variant_name(p, c->nvec, v), "ring", 4) != 0)
+            const double link_bytes = (double)c->V * 9.0 * (p == CD_FP32 ? 8.0 : 4.0) * c->N * c->N;
+            if (link_bytes > 128e6 && std::strncmp(variant_name(p, c->nvec, v), "ring", 4) != 0)   // HBM-streaming sizes
                 for (size_t i = 0; i < t1.size(); i++)
                     if (std::strncmp(variant_name(p, c->nvec, t1[i].second), "ring", 4) == 0 && t2[i] <= 1.015f * best) {
                         v = t1[i].second;
