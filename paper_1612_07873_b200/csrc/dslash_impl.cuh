@@ -1837,9 +1837,9 @@ cudaError_t launch_cluster_chain_t(const ApplyArgs &a, int n, cudaStream_t s)
 //     arrive.expect_tx): barrier 0 (own slot) completes when the 4 own triples arrived and 384
 //     bytes landed, barrier 1 (all remote slots) when 4 triples of every producing neighbour
 //     did -- no local re-arming;
-//   * a warp does the X hop as soon as its own record lands, then waits once for the remote
-//     records (the X math overlaps their DSMEM flight); on all-extent-2 lattices the slot
-//     offsets are compile-time and the +-mu hops share one load.
+//   * a warp waits for its own record (X hop), then once for the remote records; the X math
+//     overlaps the remote wait; on all-extent-2 lattices the slot offsets are compile-time and
+//     the +-mu hops share one load.
 // Receive slots (consumer c, hop k): k = 8 or L_mu = 1 -> slot 8 (own); L_mu = 2 -> slot 2 mu
 // for both hops (x + mu = x - mu: one record); else slot k.  Flow control needs no extra signal:
 // a thread pushes epoch t+1 only after its warp received the complete epoch-t records of every
@@ -1869,24 +1869,6 @@ __device__ __forceinline__ uint32_t mbar_wait_dep(uint32_t bar, uint32_t parity)
         "@!p bra WAIT_%=;\n"
         "mov.u32 %0, 0;\n"
         "}\n" : "=r"(z) : "r"(bar), "r"(parity) : "memory");
-    return z;
-}
-// the same, issued only after `after` is computed (keeps the X-hop math ahead of the remote wait)
-__device__ __forceinline__ uint32_t mbar_wait_dep_after(uint32_t bar, uint32_t parity, float after)
-{
-    uint32_t z;
-    asm volatile(
-        "{\n"
-        ".reg .pred p, q;\n"
-        "setp.eq.b32 q, %3, 0x7F800001;\n"   // a signalling-NaN pattern arithmetic never produces: never
-                                               // true, but orders the wait after `after`
-        "@q bra DONE_%=;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        "@!p bra WAIT_%=;\n"
-        "DONE_%=:\n"
-        "mov.u32 %0, 0;\n"
-        "}\n" : "=r"(z) : "r"(bar), "r"(parity), "r"(__float_as_uint(after)) : "memory");
     return z;
 }
 // shared load the compiler may schedule freely (ordered only through its address operand)
@@ -2037,7 +2019,9 @@ __global__ void __launch_bounds__(CPushCfg<NV>::THREADS, 1) dslash_cpush(ApplyAr
                 for (int j = 0; j < 3; j++) cmac2x(Lc[0][j], v, A[j], B[j]);
             }
             if (nremote > 0) {
-                z = mbar_wait_dep_after(bar_s + (uint32_t)(par * 2 + 1) * 8u, ph, __uint_as_float((uint32_t)A[0] ^ (uint32_t)B[2]));
+                // (not ordered after the X math: forcing that order cost 3 %, the scheduler overlaps
+                // the X FFMA2s with the wait on its own)
+                z = mbar_wait_dep(bar_s + (uint32_t)(par * 2 + 1) * 8u, ph);
                 if (TRACE && trt) tr[(32 + warp) * 1024 + t] = clock64() + z;
             }
             // per-thread part of the address in one register, per-hop part uniform (slot offsets
