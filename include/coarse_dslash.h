@@ -41,6 +41,16 @@
  *   - apply / apply_dagger are COLLECTIVE when nranks > 1: every rank calls them in
  *     the same order.  They are CUDA-graph capturable once the (volume, Nvec,
  *     precision, op, partition) key has been tuned (first call; or CD_TUNE=0).
+ *   - SINGLE STREAM PER CONTEXT: all operator calls (apply, apply_dagger, apply_chain,
+ *     apply_mrhs, apply_eo) on one context must be ordered on one stream (or on streams
+ *     the caller orders with events).  The persistent kernels' work tickets and the halo
+ *     transport's epochs are per-context sequence numbers; two concurrently running
+ *     applies on one context would share them.  Use one context per stream instead.
+ *   - Every entry point makes the context's device current for its duration and restores
+ *     the caller's current device before returning.
+ *   - Link objects have a kind: full (upload / generate), compressed
+ *     (coarse_links_compress_hermitian) or even-odd (coarse_links_prepare_eo).  A call
+ *     given a kind it does not support returns CD_ERR_INVALID without enqueuing work.
  */
 #ifndef COARSE_DSLASH_H
 #define COARSE_DSLASH_H

@@ -143,20 +143,21 @@ def _check(rc):
     return rc
 
 
-def default_stream():
-    """The current torch CUDA stream handle (0 = legacy default stream if torch is unusable)."""
+def default_stream(device=None):
+    """The current torch CUDA stream handle of `device` (default: torch's current device);
+    0 = legacy default stream if torch is unusable."""
     try:
         import torch
         if torch.cuda.is_available():
-            return torch.cuda.current_stream().cuda_stream
+            return torch.cuda.current_stream(device).cuda_stream
     except Exception:
         pass
     return 0
 
 
-def _stream(s):
+def _stream(s, device=None):
     if s is None:
-        return ctypes.c_void_p(default_stream())
+        return ctypes.c_void_p(default_stream(device))
     if hasattr(s, "cuda_stream"):
         return ctypes.c_void_p(s.cuda_stream)
     return ctypes.c_void_p(int(s))
@@ -249,17 +250,17 @@ def coarse_links_generate(ctx, prec, kind="general", seed=0x1612, scale_log2=0, 
     return out
 
 
-def coarse_dslash_apply(links, out, in_, stream=None):
-    _check(lib.coarse_dslash_apply(links, out, in_, _stream(stream)))
+def coarse_dslash_apply(links, out, in_, stream=None, device=None):
+    _check(lib.coarse_dslash_apply(links, out, in_, _stream(stream, device)))
 
 
-def coarse_dslash_apply_dagger(links, out, in_, stream=None):
-    _check(lib.coarse_dslash_apply_dagger(links, out, in_, _stream(stream)))
+def coarse_dslash_apply_dagger(links, out, in_, stream=None, device=None):
+    _check(lib.coarse_dslash_apply_dagger(links, out, in_, _stream(stream, device)))
 
 
-def coarse_dslash_apply_chain(links, x, y, n, dagger=False, stream=None):
+def coarse_dslash_apply_chain(links, x, y, n, dagger=False, stream=None, device=None):
     """n chained applies in one persistent kernel: t even y = D x, t odd x = D y."""
-    _check(lib.coarse_dslash_apply_chain(links, x, y, int(n), int(bool(dagger)), _stream(stream)))
+    _check(lib.coarse_dslash_apply_chain(links, x, y, int(n), int(bool(dagger)), _stream(stream, device)))
 
 
 # ------------------------------------------------------------------ classes
@@ -271,6 +272,7 @@ class Context:
         self.nvec = int(nvec)
         self.N = 2 * self.nvec
         self.proc_grid = tuple(int(x) for x in proc_grid)
+        self.device = int(device)
         self.handle = cd_context_create(self.global_dims, self.nvec, self.proc_grid, device, nranks, rank, nccl_id)
         ld = (ctypes.c_int32 * 4)()
         gc = (ctypes.c_int32 * 4)()
@@ -307,11 +309,11 @@ class Context:
 
     def halo_pack(self, field, stream=None) -> bytes:
         n = ctypes.c_size_t()
-        _check(lib.coarse_halo_pack(self.handle, field.handle, None, 0, ctypes.byref(n), _stream(stream)))
+        _check(lib.coarse_halo_pack(self.handle, field.handle, None, 0, ctypes.byref(n), _stream(stream, self.device)))
         buf = np.zeros(max(n.value, 1), np.uint8)
         if n.value:
             _check(lib.coarse_halo_pack(self.handle, field.handle, buf.ctypes.data, 0, ctypes.byref(n),
-                                        _stream(stream)))
+                                        _stream(stream, self.device)))
         return buf[:n.value].tobytes()
 
     def transfer(self, block, nspin, ncolor, basis, stream=None):
@@ -320,7 +322,7 @@ class Context:
         return Transfer(self, block, nspin, ncolor, basis, stream)
 
     def flush_l2(self, nbytes=512 << 20, stream=None):
-        _check(lib.cd_flush_l2(self.handle, nbytes, _stream(stream)))
+        _check(lib.cd_flush_l2(self.handle, nbytes, _stream(stream, self.device)))
 
     def close(self):
         if self.handle:
@@ -349,7 +351,7 @@ class Field:
         ptr = None
         if torch_memory:
             import torch
-            self._mem = torch.empty(self.nbytes, dtype=torch.uint8, device="cuda")
+            self._mem = torch.empty(self.nbytes, dtype=torch.uint8, device=f"cuda:{ctx.device}")
             ptr = self._mem.data_ptr()
         if parity is not None:
             out = ctypes.c_void_p()
@@ -367,7 +369,7 @@ class Field:
     def import_(self, v, stream=None):
         """v: canonical LOCAL [V, N] complex64/complex128 (numpy host or torch host/device)."""
         p, dev, keep = _ptr(v)
-        _check(lib.coarse_field_import(self.handle, p, dev, CD_C128 if _is_c128(v) else CD_C64, _stream(stream)))
+        _check(lib.coarse_field_import(self.handle, p, dev, CD_C128 if _is_c128(v) else CD_C64, _stream(stream, self.ctx.device)))
         return keep
 
     def export(self, dst=None, dtype=np.complex128, stream=None, sync=True):
@@ -375,18 +377,18 @@ class Field:
             shape = (self.sites, self.ctx.N) if self.nrhs == 1 else (self.nrhs, self.sites, self.ctx.N)
             dst = np.empty(shape, dtype)
         p, dev, _ = _ptr(dst)
-        _check(lib.coarse_field_export(self.handle, p, dev, CD_C128 if _is_c128(dst) else CD_C64, _stream(stream)))
+        _check(lib.coarse_field_export(self.handle, p, dev, CD_C128 if _is_c128(dst) else CD_C64, _stream(stream, self.ctx.device)))
         if sync:
             _sync(stream)
         return dst
 
     def generate(self, seed=0x7873, tag=2, scale_log2=0, stream=None):
-        _check(lib.coarse_field_generate(self.handle, seed, tag, scale_log2, _stream(stream)))
+        _check(lib.coarse_field_generate(self.handle, seed, tag, scale_log2, _stream(stream, self.ctx.device)))
 
     def read_stored(self, stream=None) -> bytes:
         n = int(lib.coarse_field_stored_bytes(self.handle))
         buf = np.empty(n, np.uint8)
-        _check(lib.coarse_field_read_stored(self.handle, buf.ctypes.data, 0, _stream(stream)))
+        _check(lib.coarse_field_read_stored(self.handle, buf.ctypes.data, 0, _stream(stream, self.ctx.device)))
         return buf.tobytes()
 
     def close(self):
@@ -410,13 +412,13 @@ class Links:
         self.handle = handle
 
     def apply(self, out: Field, in_: Field, stream=None):
-        coarse_dslash_apply(self.handle, out.handle, in_.handle, stream)
+        coarse_dslash_apply(self.handle, out.handle, in_.handle, stream, self.ctx.device)
 
     def apply_dagger(self, out: Field, in_: Field, stream=None):
-        coarse_dslash_apply_dagger(self.handle, out.handle, in_.handle, stream)
+        coarse_dslash_apply_dagger(self.handle, out.handle, in_.handle, stream, self.ctx.device)
 
     def apply_chain(self, x: Field, y: Field, n: int, dagger=False, stream=None):
-        coarse_dslash_apply_chain(self.handle, x.handle, y.handle, n, dagger, stream)
+        coarse_dslash_apply_chain(self.handle, x.handle, y.handle, n, dagger, stream, self.ctx.device)
 
     def prepare_eo(self, stream=None):
         """Even-odd preconditioned operator (X_o^-1 L_k(o) precomputed); returns new Links."""
@@ -426,7 +428,7 @@ class Links:
 
     def apply_eo(self, out: Field, in_: Field, dagger=False, stream=None):
         """out_e = M_ee in_e (Schur complement on even sites; parity-0 fields)."""
-        _check(lib.coarse_dslash_apply_eo(self.handle, out.handle, in_.handle, int(bool(dagger)), _stream(stream)))
+        _check(lib.coarse_dslash_apply_eo(self.handle, out.handle, in_.handle, int(bool(dagger)), _stream(stream, self.ctx.device)))
 
     def compress_hermitian(self, check=True, stream=None):
         """tau3-hermitian compressed copy (X + 4 forward links per site); returns (Links, max_dev)."""
@@ -438,12 +440,12 @@ class Links:
 
     def apply_mrhs(self, out: Field, in_: Field, dagger=False, stream=None):
         """out_r = D in_r for all right-hand sides (tcgen05 tensor cores, fp16 storage)."""
-        _check(lib.coarse_dslash_apply_mrhs(self.handle, out.handle, in_.handle, int(bool(dagger)), _stream(stream)))
+        _check(lib.coarse_dslash_apply_mrhs(self.handle, out.handle, in_.handle, int(bool(dagger)), _stream(stream, self.ctx.device)))
 
     def read_stored(self, stream=None) -> bytes:
         n = int(lib.coarse_links_stored_bytes(self.handle))
         buf = np.empty(n, np.uint8)
-        _check(lib.coarse_links_read_stored(self.handle, buf.ctypes.data, 0, _stream(stream)))
+        _check(lib.coarse_links_read_stored(self.handle, buf.ctypes.data, 0, _stream(stream, self.ctx.device)))
         return buf.tobytes()
 
     def close(self):
@@ -481,14 +483,14 @@ class Transfer:
     def fine_field(self):
         """A device complex64 fine field [Vf, nspin, ncolor] (torch)."""
         import torch
-        return torch.zeros((self.Vf, self.nspin, self.ncolor), dtype=torch.complex64, device="cuda")
+        return torch.zeros((self.Vf, self.nspin, self.ncolor), dtype=torch.complex64, device=f"cuda:{self.ctx.device}")
 
     def orthonormalise(self, stream=None):
-        _check(lib.coarse_transfer_orthonormalise(self.handle, _stream(stream)))
+        _check(lib.coarse_transfer_orthonormalise(self.handle, _stream(stream, self.ctx.device)))
 
     def read_basis(self, stream=None):
         out = np.empty((self.Vf, self.nspin, self.ncolor, self.ctx.nvec), np.complex64)
-        _check(lib.coarse_transfer_read_basis(self.handle, out.ctypes.data, 0, _stream(stream)))
+        _check(lib.coarse_transfer_read_basis(self.handle, out.ctypes.data, 0, _stream(stream, self.ctx.device)))
         return out
 
     def restrict(self, coarse_out: Field, fine_in, stream=None):
@@ -496,14 +498,14 @@ class Transfer:
         p, dev, _ = _ptr(fine_in)
         if not dev:
             raise ValueError("fine_in must be device memory")
-        _check(lib.coarse_restrict(self.handle, coarse_out.handle, p, _stream(stream)))
+        _check(lib.coarse_restrict(self.handle, coarse_out.handle, p, _stream(stream, self.ctx.device)))
 
     def prolong(self, fine_out, coarse_in: Field, stream=None):
         """fine_out = P coarse_in (fine_out: device complex64 [Vf, nspin, ncolor])."""
         p, dev, _ = _ptr(fine_out)
         if not dev:
             raise ValueError("fine_out must be device memory")
-        _check(lib.coarse_prolong(self.handle, p, coarse_in.handle, _stream(stream)))
+        _check(lib.coarse_prolong(self.handle, p, coarse_in.handle, _stream(stream, self.ctx.device)))
 
     def close(self):
         if self.handle:

@@ -211,6 +211,24 @@ struct DevBuf {
     }
 };
 
+// Makes the context's device current for the duration of an entry point and restores the
+// caller's device afterwards (a process may hold contexts on several GPUs).
+struct DevGuard {
+    int prev = -1;
+    bool changed = false;
+    explicit DevGuard(int dev)
+    {
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) changed = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DevGuard()
+    {
+        if (changed) cudaSetDevice(prev);
+    }
+    DevGuard(const DevGuard &) = delete;
+    DevGuard &operator=(const DevGuard &) = delete;
+};
+#define CTX_GUARD(ctx) DevGuard dev_guard_((ctx)->device)
+
 // ------------------------------------------------------------------ decomposition + halo plan
 // Geometry checks shared by cd_context_create and cd_halo_plan_create.
 static int check_geometry(const cd_geometry *geom, int nranks, int rank)
@@ -366,6 +384,22 @@ static void tune_file_store(const std::string &key, int id, const char *name, fl
 }
 
 // ------------------------------------------------------------------ context
+// Frees everything a (possibly half-built) context holds, then the context itself.
+static void ctx_release(cd_context *c)
+{
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    void *bufs[] = {c->send_buf, c->recv_buf, c->face_scratch, c->face_sites, c->interior_sites, c->mrhs_send,
+                    c->mrhs_recv, c->work, c->ysplit, c->site_cnt, c->chain_cnt, c->llbuf};
+    for (void *b : bufs)
+        if (b) cudaFree(b);
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    if (c->ev_in) cudaEventDestroy(c->ev_in);
+    if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+    comm_destroy(c->comm);
+    delete c;
+}
+
 extern "C" {
 
 const char *cd_version(void) { return "coarse_dslash 0.1 (sm_100a)"; }
@@ -395,7 +429,7 @@ int cd_context_create(const cd_geometry *geom, int device, int nranks, int rank,
     int ndev = 0;
     CUDA_TRY(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
     if (device < 0 || device >= ndev) return fail(CD_ERR_INVALID, "bad device");
-    CUDA_TRY(cudaSetDevice(device), "cudaSetDevice");
+    DevGuard dev_guard_(device);
 
     cd_context *c = new cd_context();
     c->geom = *geom;
@@ -421,7 +455,7 @@ int cd_context_create(const cd_geometry *geom, int device, int nranks, int rank,
     cudaDeviceProp prop;
     cudaError_t e = cudaGetDeviceProperties(&prop, device);
     if (e != cudaSuccess) {
-        delete c;
+        ctx_release(c);
         return cuda_fail(e, "cudaGetDeviceProperties");
     }
     c->num_sms = prop.multiProcessorCount;
@@ -433,7 +467,7 @@ int cd_context_create(const cd_geometry *geom, int device, int nranks, int rank,
     if (e == cudaSuccess) e = cudaMalloc(&c->chain_cnt, sizeof(unsigned) * c->V);
     if (e == cudaSuccess) e = cudaMemset(c->chain_cnt, 0, sizeof(unsigned) * c->V);
     if (e != cudaSuccess) {
-        delete c;
+        ctx_release(c);
         return cuda_fail(e, "cudaMalloc(work)");
     }
     if (const char *ev = getenv("CD_TUNE")) c->tune = atoi(ev) ? 1 : 0;
@@ -443,13 +477,13 @@ int cd_context_create(const cd_geometry *geom, int device, int nranks, int rank,
         std::string err;
         int r = comm_create(nccl_id, nranks, rank, &c->comm, err);
         if (r != CD_OK) {
-            delete c;
+            ctx_release(c);
             return fail(r, err);
         }
     }
     int r = setup_halo(c);
     if (r != CD_OK) {
-        delete c;
+        ctx_release(c);
         return r;
     }
     *out = c;
@@ -461,25 +495,8 @@ int cd_context_destroy(cd_context *c)
 {
     API_BEGIN
     if (!c) return fail(CD_ERR_INVALID, "ctx is NULL");
-    cudaSetDevice(c->device);
-    cudaDeviceSynchronize();
-    if (c->send_buf) cudaFree(c->send_buf);
-    if (c->recv_buf) cudaFree(c->recv_buf);
-    if (c->face_scratch) cudaFree(c->face_scratch);
-    if (c->face_sites) cudaFree(c->face_sites);
-    if (c->interior_sites) cudaFree(c->interior_sites);
-    if (c->mrhs_send) cudaFree(c->mrhs_send);
-    if (c->mrhs_recv) cudaFree(c->mrhs_recv);
-    if (c->work) cudaFree(c->work);
-    if (c->ysplit) cudaFree(c->ysplit);
-    if (c->site_cnt) cudaFree(c->site_cnt);
-    if (c->chain_cnt) cudaFree(c->chain_cnt);
-    if (c->llbuf) cudaFree(c->llbuf);
-    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
-    if (c->ev_in) cudaEventDestroy(c->ev_in);
-    if (c->ev_halo) cudaEventDestroy(c->ev_halo);
-    comm_destroy(c->comm);
-    delete c;
+    DevGuard dev_guard_(c->device);
+    ctx_release(c);
     return CD_OK;
     API_END
 }
@@ -488,6 +505,7 @@ int cd_context_set_option(cd_context *c, int option, int64_t value)
 {
     API_BEGIN
     if (!c) return fail(CD_ERR_INVALID, "ctx is NULL");
+    CTX_GUARD(c);
     std::lock_guard<std::mutex> lk(c->mu);
     switch (option) {
     case CD_OPT_VARIANT:
@@ -578,6 +596,7 @@ int coarse_field_alloc(cd_context *c, cd_precision p, void *mem, size_t bytes, c
     API_BEGIN
     if (!c || !out) return fail(CD_ERR_INVALID, "ctx/out is NULL");
     if (p != CD_FP32 && p != CD_FP16) return fail(CD_ERR_INVALID, "bad precision");
+    CTX_GUARD(c);
     const size_t need = coarse_field_bytes(c, p);
     bool owned = false;
     if (!mem) {
@@ -611,6 +630,7 @@ int coarse_field_alloc_mrhs(cd_context *c, cd_precision p, int nrhs, void *mem, 
     if (!c || !out) return fail(CD_ERR_INVALID, "ctx/out is NULL");
     if (p != CD_FP32 && p != CD_FP16) return fail(CD_ERR_INVALID, "bad precision");
     if (nrhs < 1) return fail(CD_ERR_INVALID, "nrhs must be >= 1");
+    CTX_GUARD(c);
     if (p == CD_FP16 && nrhs > 1 && nrhs % 128)
         return fail(CD_ERR_UNSUPPORTED, "fp16 multi-RHS fields hold blocks of 128 right-hand sides (nrhs % 128 == 0)");
     const size_t need = coarse_field_bytes_mrhs(c, p, nrhs);
@@ -634,6 +654,7 @@ int coarse_field_free(cd_field *f)
 {
     API_BEGIN
     if (!f) return fail(CD_ERR_INVALID, "field is NULL");
+    CTX_GUARD(f->ctx);
     if (f->owned) cudaFree(f->base);
     delete f;
     return CD_OK;
@@ -652,6 +673,7 @@ int coarse_field_import(cd_field *f, const void *src, int src_on_device, cd_host
     API_BEGIN
     if (!f || !src) return fail(CD_ERR_INVALID, "field/src is NULL");
     if (dt != CD_C64 && dt != CD_C128) return fail(CD_ERR_INVALID, "bad dtype");
+    CTX_GUARD(f->ctx);
     cd_context *c = f->ctx;
     const size_t elem = dt == CD_C128 ? 16 : 8;
     const size_t bytes = elem * c->N * (size_t)field_sites(f) * f->nrhs;
@@ -680,6 +702,7 @@ int coarse_field_export(const cd_field *f, void *dst, int dst_on_device, cd_host
     API_BEGIN
     if (!f || !dst) return fail(CD_ERR_INVALID, "field/dst is NULL");
     if (dt != CD_C64 && dt != CD_C128) return fail(CD_ERR_INVALID, "bad dtype");
+    CTX_GUARD(f->ctx);
     cd_context *c = f->ctx;
     const size_t elem = dt == CD_C128 ? 16 : 8;
     const size_t bytes = elem * c->N * (size_t)field_sites(f) * f->nrhs;
@@ -708,6 +731,7 @@ int coarse_field_generate(cd_field *f, uint64_t seed, uint32_t tag, int32_t scal
 {
     API_BEGIN
     if (!f) return fail(CD_ERR_INVALID, "field is NULL");
+    CTX_GUARD(f->ctx);
     if (scale_log2 < -60 || scale_log2 > 60) return fail(CD_ERR_INVALID, "scale_log2 out of range");
     if (f->parity >= 0) return fail(CD_ERR_UNSUPPORTED, "generate: full-lattice fields only");
     CUDA_TRY(launch_field_generate(f->prec, f->ctx->nvec, f->ctx, seed, tag, scale_log2, f->base, S(stream), f->nrhs),
@@ -749,6 +773,7 @@ int coarse_field_read_stored(const cd_field *f, void *dst, int dst_on_device, vo
 {
     API_BEGIN
     if (!f || !dst) return fail(CD_ERR_INVALID, "field/dst is NULL");
+    CTX_GUARD(f->ctx);
     const int N = f->ctx->N;
     const bool f16 = f->prec == CD_FP16;
     if (f16 && f->nrhs > 1) {   // tensor-core blocks are returned as stored (R22)
@@ -780,13 +805,16 @@ int coarse_links_compress_hermitian(const cd_links *full, double *max_dev, void 
 {
     API_BEGIN
     if (!full || !out) return fail(CD_ERR_INVALID, "links/out is NULL");
+    CTX_GUARD(full->ctx);
     if (full->compressed) return fail(CD_ERR_INVALID, "links are already compressed");
+    if (full->eo) return fail(CD_ERR_INVALID, "even-odd prepared links cannot be compressed");
     cd_context *c = full->ctx;
     cudaStream_t s = S(stream);
     cd_links *l = nullptr;
     int r = links_new(c, full->prec, &l, 1);
     if (r != CD_OK) return r;
     std::unique_ptr<cd_links, int (*)(cd_links *)> guard(l, coarse_links_free);
+    l->split = c->kg.split;
     CUDA_TRY(launch_compress(full->prec, c->nvec, full->base, l->base, c->V, s), "links compress");
     if (c->kg.split != 0) {
         // multi-rank: a ONE-TIME link halo -- the backward hop of an x_mu = 0 site needs the -mu
@@ -838,6 +866,7 @@ int coarse_links_upload(cd_context *c, cd_precision p, const void *src, int src_
 {
     API_BEGIN
     if (!c || !src || !out) return fail(CD_ERR_INVALID, "ctx/src/out is NULL");
+    CTX_GUARD(c);
     if (p != CD_FP32 && p != CD_FP16) return fail(CD_ERR_INVALID, "bad precision");
     if (dt != CD_C64 && dt != CD_C128) return fail(CD_ERR_INVALID, "bad dtype");
     cd_links *l = nullptr;
@@ -889,6 +918,7 @@ int coarse_links_generate(cd_context *c, cd_precision p, int kind, uint64_t seed
 {
     API_BEGIN
     if (!c || !out) return fail(CD_ERR_INVALID, "ctx/out is NULL");
+    CTX_GUARD(c);
     if (p != CD_FP32 && p != CD_FP16) return fail(CD_ERR_INVALID, "bad precision");
     if (kind < 0 || kind > 3) return fail(CD_ERR_INVALID, "bad links kind");
     if (scale_log2 < -60 || scale_log2 > 60) return fail(CD_ERR_INVALID, "scale_log2 out of range");
@@ -908,7 +938,7 @@ int coarse_links_generate(cd_context *c, cd_precision p, int kind, uint64_t seed
 
 size_t coarse_links_stored_bytes(const cd_links *l)
 {
-    if (!l) return 0;
+    if (!l || l->eo) return 0;
     const size_t nm = (l->compressed ? 5 : 9) * (size_t)l->ctx->V;
     const size_t NN = (size_t)l->ctx->N * l->ctx->N;
     return l->prec == CD_FP32 ? 8 * NN * nm : 4 * NN * nm + 4 * nm;
@@ -918,6 +948,8 @@ int coarse_links_read_stored(const cd_links *l, void *dst, int dst_on_device, vo
 {
     API_BEGIN
     if (!l || !dst) return fail(CD_ERR_INVALID, "links/dst is NULL");
+    if (l->eo) return fail(CD_ERR_INVALID, "even-odd prepared links have no canonical stored form");
+    CTX_GUARD(l->ctx);
     const size_t NN = (size_t)l->ctx->N * l->ctx->N;
     const bool f16 = l->prec == CD_FP16;
     return read_stored(l->base, (l->compressed ? 5 : 9) * l->ctx->V, f16 ? 4 * NN : 8 * NN,
@@ -929,6 +961,7 @@ int coarse_links_free(cd_links *l)
 {
     API_BEGIN
     if (!l) return fail(CD_ERR_INVALID, "links is NULL");
+    CTX_GUARD(l->ctx);
     if (l->aux) cudaFree(l->aux);
     if (l->tbuf) cudaFree(l->tbuf);
     cudaFree(l->base);
@@ -946,6 +979,7 @@ static int check_objs(const cd_links *l, const cd_field *out, const cd_field *in
     if (out->base == in->base) return fail(CD_ERR_INVALID, "out must not alias in");
     if (out->nrhs != 1 || in->nrhs != 1) return fail(CD_ERR_INVALID, "multi-RHS fields need coarse_dslash_apply_mrhs");
     if (out->parity >= 0 || in->parity >= 0) return fail(CD_ERR_INVALID, "parity fields need coarse_dslash_apply_eo");
+    if (l->eo) return fail(CD_ERR_INVALID, "even-odd prepared links need coarse_dslash_apply_eo");
     const char *ob = static_cast<const char *>(out->base), *ib = static_cast<const char *>(in->base);
     const size_t need = coarse_field_bytes(l->ctx, l->prec);
     if (ob < ib + need && ib < ob + need) return fail(CD_ERR_INVALID, "out overlaps in");
@@ -1062,7 +1096,11 @@ static int do_apply(const cd_links *l, cd_field *out, const cd_field *in, void *
     int r = check_objs(l, out, in);
     if (r != CD_OK) return r;
     cd_context *c = l->ctx;
+    CTX_GUARD(c);
     cudaStream_t s = S(stream);
+    if (l->compressed && l->split != c->kg.split)
+        return fail(CD_ERR_INVALID, "compressed links were built under a different halo split (set CD_OPT_HALO_SELF_MASK "
+                                    "before coarse_links_compress_hermitian)");
     c->applied = true;
     if (c->comm) {
         std::string err;
@@ -1189,6 +1227,7 @@ int coarse_field_alloc_parity(cd_context *c, cd_precision p, int parity, void *m
     if (!c || !out) return fail(CD_ERR_INVALID, "ctx/out is NULL");
     if (p != CD_FP32 && p != CD_FP16) return fail(CD_ERR_INVALID, "bad precision");
     if (parity != 0 && parity != 1) return fail(CD_ERR_INVALID, "parity must be 0 (even) or 1 (odd)");
+    CTX_GUARD(c);
     if (!eo_geometry_ok(c)) return fail(CD_ERR_UNSUPPORTED, "even-odd needs every local L_mu even");
     const size_t need = coarse_field_bytes_parity(c, p);
     bool owned = false;
@@ -1211,6 +1250,7 @@ int coarse_links_prepare_eo(const cd_links *full, void *stream, cd_links **out)
 {
     API_BEGIN
     if (!full || !out) return fail(CD_ERR_INVALID, "links/out is NULL");
+    CTX_GUARD(full->ctx);
     if (full->compressed || full->eo) return fail(CD_ERR_INVALID, "needs full (uncompressed) links");
     if (full->prec != CD_FP32) return fail(CD_ERR_UNSUPPORTED, "even-odd: fp32 storage only");
     cd_context *c = full->ctx;
@@ -1240,6 +1280,7 @@ int coarse_dslash_apply_eo(const cd_links *l, cd_field *out, const cd_field *in,
 {
     API_BEGIN
     if (!l || !out || !in) return fail(CD_ERR_INVALID, "links/out/in is NULL");
+    CTX_GUARD(l->ctx);
     if (!l->eo) return fail(CD_ERR_INVALID, "links not prepared with coarse_links_prepare_eo");
     if (l->ctx != out->ctx || l->ctx != in->ctx) return fail(CD_ERR_MISMATCH, "objects from different contexts");
     if (out->parity != 0 || in->parity != 0) return fail(CD_ERR_INVALID, "in/out must be even-parity fields");
@@ -1287,7 +1328,10 @@ int coarse_dslash_apply_mrhs(const cd_links *l, cd_field *out, const cd_field *i
 {
     API_BEGIN
     if (!l || !out || !in) return fail(CD_ERR_INVALID, "links/out/in is NULL");
+    CTX_GUARD(l->ctx);
     if (l->ctx != out->ctx || l->ctx != in->ctx) return fail(CD_ERR_MISMATCH, "objects from different contexts");
+    if (l->compressed || l->eo) return fail(CD_ERR_INVALID, "apply_mrhs needs full (uncompressed, not even-odd) links");
+    if (out->parity >= 0 || in->parity >= 0) return fail(CD_ERR_INVALID, "apply_mrhs needs full-lattice fields");
     if (l->prec != CD_FP16 || out->prec != CD_FP16 || in->prec != CD_FP16)
         return fail(CD_ERR_UNSUPPORTED, "the tensor-core multi-RHS path needs fp16 storage (links and fields)");
     if (in->nrhs != out->nrhs) return fail(CD_ERR_MISMATCH, "nrhs mismatch");
@@ -1373,8 +1417,10 @@ int coarse_dslash_apply_chain(const cd_links *l, cd_field *x, cd_field *y, int n
     API_BEGIN
     int r = check_objs(l, y, x);
     if (r != CD_OK) return r;
+    if (l->compressed) return fail(CD_ERR_INVALID, "apply_chain needs full (uncompressed) links");
     if (n < 0) return fail(CD_ERR_INVALID, "n must be >= 0");
     cd_context *c = l->ctx;
+    CTX_GUARD(c);
     if (c->kg.split != 0) return fail(CD_ERR_UNSUPPORTED, "apply_chain is single-rank (no halo split)");
     if (n == 0) return CD_OK;
     cudaStream_t s = S(stream);
@@ -1498,6 +1544,7 @@ int coarse_halo_pack(cd_context *c, const cd_field *in, void *dst, int dst_on_de
 {
     API_BEGIN
     if (!c || !in || !bytes) return fail(CD_ERR_INVALID, "ctx/in/bytes is NULL");
+    CTX_GUARD(c);
     if (in->ctx != c) return fail(CD_ERR_MISMATCH, "field from another context");
     if (c->kg.split == 0) {
         *bytes = 0;
@@ -1537,6 +1584,7 @@ int cd_flush_l2(cd_context *c, size_t bytes, void *stream)
 {
     API_BEGIN
     if (!c) return fail(CD_ERR_INVALID, "ctx is NULL");
+    CTX_GUARD(c);
     static void *buf = nullptr;
     static size_t cap = 0;
     if (bytes > cap) {
@@ -1557,6 +1605,7 @@ int coarse_transfer_create(cd_context *c, const cd_transfer_desc *d, const void 
 {
     API_BEGIN
     if (!c || !d || !basis || !out) return fail(CD_ERR_INVALID, "ctx/desc/basis/out is NULL");
+    CTX_GUARD(c);
     if (dt != CD_C64 && dt != CD_C128) return fail(CD_ERR_INVALID, "bad dtype");
     if (d->nspin != 2 && d->nspin != 4) return fail(CD_ERR_UNSUPPORTED, "nspin must be 2 or 4");
     if (d->ncolor < 1 || d->ncolor > 256) return fail(CD_ERR_INVALID, "ncolor must be in [1, 256]");
@@ -1606,6 +1655,7 @@ int coarse_transfer_free(cd_transfer *t)
 {
     API_BEGIN
     if (!t) return fail(CD_ERR_INVALID, "transfer is NULL");
+    CTX_GUARD(t->ctx);
     cudaFree(t->W);
     delete t;
     return CD_OK;
@@ -1621,6 +1671,7 @@ int coarse_transfer_read_basis(const cd_transfer *t, void *dst, int dst_on_devic
 {
     API_BEGIN
     if (!t || !dst) return fail(CD_ERR_INVALID, "transfer/dst is NULL");
+    CTX_GUARD(t->ctx);
     CUDA_TRY(cudaMemcpyAsync(dst, t->W, t->wbytes, dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                              S(stream)),
              "cudaMemcpyAsync(basis)");
@@ -1633,6 +1684,7 @@ int coarse_transfer_orthonormalise(cd_transfer *t, void *stream)
 {
     API_BEGIN
     if (!t) return fail(CD_ERR_INVALID, "transfer is NULL");
+    CTX_GUARD(t->ctx);
     if ((int64_t)t->tg.Bvol * (t->tg.nf / 2) < t->ctx->nvec)
         return fail(CD_ERR_INVALID, "aggregate has fewer rows per chirality than Nvec columns");
     if (t->tg.Bvol * (int64_t)sizeof(int) > 200 * 1024) return fail(CD_ERR_UNSUPPORTED, "aggregate too large");

@@ -143,6 +143,7 @@ struct cd_links {
     void *aux;        // eo: odd-site records
     void *tbuf;       // eo: odd half-field scratch t_o (fp32)
     int64_t lhoff[4] = {0, 0, 0, 0};   // compressed + multi-rank: aux = link halo, dim mu's records at lhoff[mu]
+    int split = 0;                     // compressed: the context's halo split mask when the link halo was built
 };
 
 struct cd_transfer {

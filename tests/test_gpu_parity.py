@@ -944,3 +944,64 @@ def test_random_geometry_sweep(dims, nvec, prec, mask, vseed):
     assert rel_l2(fout.export(), oracle.apply(dims, Lh, v)) <= tol
     L.apply_dagger(fout, fin)
     assert rel_l2(fout.export(), oracle.adjoint(dims, Lh, v)) <= tol
+
+
+# ---------------------------------------------------------------- link kinds (wrong kind -> CD_ERR_INVALID)
+def test_link_kinds_rejected_synchronously():
+    """Calls given a link kind they do not support fail with CD_ERR_INVALID and enqueue nothing
+    (an even-odd object holds 9V/2 + 8V/2 records, a compressed one 5V: indexing them as 9V
+    full links would read past the allocation)."""
+    dims, nvec = (4, 4, 4, 4), 24
+    ctx = cd.Context(dims, nvec)
+    L32 = ctx.links_generate("fp32", kind="hermitian", scale_log2=-4)
+    L16 = ctx.links_generate("fp16", kind="hermitian", scale_log2=-4)
+    a, b = ctx.field("fp32"), ctx.field("fp32")
+    a.generate()
+    E = L32.prepare_eo()
+    C32, _ = L32.compress_hermitian(check=False)
+    C16, _ = L16.compress_hermitian(check=False)
+    m1, m2 = ctx.field("fp16", nrhs=128), ctx.field("fp16", nrhs=128)
+    bad = [lambda: E.apply(b, a), lambda: E.apply_dagger(b, a), lambda: E.apply_chain(a, b, 2),
+           lambda: E.read_stored(), lambda: E.compress_hermitian(), lambda: C32.apply_chain(a, b, 2),
+           lambda: C16.apply_mrhs(m2, m1), lambda: C32.compress_hermitian()]
+    for i, f in enumerate(bad):
+        with pytest.raises(cd.CDError) as ei:
+            f()
+        assert ei.value.code == cd.CD_ERR_INVALID, i
+    torch.cuda.synchronize()
+    # the context is still healthy: a good apply after the rejected ones is correct
+    C32.apply(b, a)
+    y = b.export()
+    L32.apply(b, a)
+    assert rel_l2(y, b.export()) <= 1e-5
+
+
+def test_compressed_links_split_mismatch_rejected():
+    """Compressed links built with no halo split have no link halo; enabling a halo split
+    afterwards must not let an apply dereference it."""
+    dims, nvec = (4, 4, 4, 4), 24
+    ctx = cd.Context(dims, nvec)
+    L = ctx.links_generate("fp32", kind="hermitian", scale_log2=-4)
+    C, _ = L.compress_hermitian(check=False)
+    ctx.set_option(cd.CD_OPT_HALO_SELF_MASK, 0b1000)
+    a, b = ctx.field("fp32"), ctx.field("fp32")
+    a.generate()
+    with pytest.raises(cd.CDError) as ei:
+        C.apply(b, a)
+    assert ei.value.code == cd.CD_ERR_INVALID
+    C2, _ = L.compress_hermitian(check=False)   # rebuilt under the split: fine
+    C2.apply(b, a)
+    y = b.export()
+    L.apply(b, a)
+    assert rel_l2(y, b.export()) <= 1e-5
+
+
+def test_entry_points_restore_current_device():
+    dev0 = torch.cuda.current_device()
+    ctx = cd.Context((2, 2, 2, 2), 24, device=torch.cuda.device_count() - 1)
+    L = ctx.links_generate("fp32")
+    a, b = ctx.field("fp32"), ctx.field("fp32")
+    a.generate()
+    L.apply(b, a)
+    b.export()
+    assert torch.cuda.current_device() == dev0
