@@ -45,6 +45,8 @@ def _load():
             I4 = ctypes.POINTER(ctypes.c_int)
             lib.oracle_apply.argtypes = [I4, ctypes.c_int, P, P, P]
             lib.oracle_apply_dagger_tau3.argtypes = [I4, ctypes.c_int, P, P, P]
+            lib.oracle_apply_generated.argtypes = [I4, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_int, P, P]
+            lib.oracle_apply_generated.restype = ctypes.c_int
             lib.oracle_adjoint.argtypes = [I4, ctypes.c_int, P, P, P]
             lib.oracle_dense.argtypes = [I4, ctypes.c_int, P, P]
             lib.oracle_partitioned_apply.argtypes = [I4, I4, ctypes.c_int, P, P, P]
@@ -91,6 +93,24 @@ def apply(dims, links, v):
     x = _c128(v, (V, N))
     y = np.empty((V, N), np.complex128)
     _load().oracle_apply(_dims(dims), N, L.ctypes.data, x.ctypes.data, y.ctypes.data)
+    return y
+
+
+KINDS = {"general": 0, "hermitian": 1, "ti_general": 2, "ti_hermitian": 3}
+
+
+def apply_generated(dims, N, v, kind="general", seed=0x1612, scale_log2=0):
+    """Matrix-free y = D v: the links of recipe `kind` (synth.links(dims, N, seed, kind,
+    scale_log2)) are regenerated per site instead of being passed in, so whole
+    full-size lattices need memory for the vectors only.  Same term order as
+    apply(): bit-identical to apply(dims, synth.links(...), v) (pinned)."""
+    V = int(np.prod(dims))
+    v = _c128(v, (V, N))
+    y = np.empty((V, N), np.complex128)
+    rc = _load().oracle_apply_generated(_dims(dims), int(N), KINDS[kind], int(seed) & 0xFFFFFFFFFFFFFFFF,
+                                        int(scale_log2), v.ctypes.data, y.ctypes.data)
+    if rc != 0:
+        raise ValueError(f"oracle_apply_generated failed ({rc})")
     return y
 
 

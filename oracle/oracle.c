@@ -137,6 +137,115 @@ void oracle_apply(const int L[4], int N, const double *links_, const double *v_,
     }
 }
 
+/* ---------------------------------------------------------------- matrix-free mode
+ * y = D v exactly as oracle_apply, but every link matrix is regenerated from the test-input
+ * recipe when it is needed instead of being read from an array, so the full-size configs
+ * (M4 1.5 GB, M5 43.5 GB of fp64 links) can be checked on the whole
+ * lattice with memory for the vectors only.  The generator is the
+ * counter-based recipe of SURVEY §8(c) c.3 (splitmix64 over global indices), written out here
+ * independently of synth/ (and of the CUDA library's generator); a pin checks this function
+ * bit-for-bit against oracle_apply on synth.links() for every recipe.
+ *   kind 0 general:   L_k(x) = G(x,k)
+ *   kind 1 hermitian: L_{2mu}(x) = G(x,2mu); L_{2mu+1}(x)[i][j] = s_i s_j conj(G(x-mu,2mu)[j][i]);
+ *                     X(x)[i][j] = (G(x,8)[i][j] + s_i s_j conj(G(x,8)[j][i])) / 2   (s = tau3 signs)
+ *   kind 2 / 3: the same with gsite := 0 and tag 4 (translation invariant)
+ * every entry then multiplied by 2^scale_log2 (exact). */
+static uint64_t sm64(uint64_t z)
+{
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+static double u_of(uint64_t base, uint64_t ctr)
+{
+    const uint64_t h = sm64(base + ctr);
+    return (double)((int64_t)(h >> 42) - ((int64_t)1 << 21)) * 0x1p-21;
+}
+
+/* G(gsite, k)[i][j], counter ((((gsite*9 + k)*N + i)*N + j)*2 + part) */
+static void gen_G(uint64_t base, int64_t gsite, int k, int N, cplx *M)
+{
+    for (int i = 0; i < N; i++)
+        for (int j = 0; j < N; j++) {
+            const uint64_t c = (uint64_t)(((((gsite * 9 + k) * N + i) * N) + j) * 2);
+            M[(int64_t)i * N + j] = u_of(base, c) + I * u_of(base, c + 1);
+        }
+}
+
+/* the nine matrices of site x (global coordinates = local: the oracle holds the whole lattice) */
+static void gen_site_links(const int L[4], int N, int kind, uint64_t base, double scale, const int x[4], cplx *L9,
+                           cplx *tmp)
+{
+    const int ti = kind >= 2, herm = kind & 1;
+    const int64_t NN = (int64_t)N * N;
+    const int64_t gs = ti ? 0 : site_of(L, x);
+    for (int k = 0; k < 9; k++) gen_G(base, gs, k, N, L9 + k * NN);
+    if (herm) {
+        const int nvec = N / 2;
+        cplx *X = L9 + 8 * NN;
+        memcpy(tmp, X, sizeof(cplx) * NN);
+        for (int i = 0; i < N; i++)
+            for (int j = 0; j < N; j++) {
+                const double ss = ((i < nvec) == (j < nvec)) ? 1.0 : -1.0;
+                X[(int64_t)i * N + j] = 0.5 * (tmp[(int64_t)i * N + j] + ss * conj(tmp[(int64_t)j * N + i]));
+            }
+        for (int mu = 0; mu < 4; mu++) {
+            const int64_t gb = ti ? 0 : hop(L, x, mu, -1);
+            gen_G(base, gb, 2 * mu, N, tmp);
+            cplx *B = L9 + (2 * mu + 1) * NN;
+            for (int i = 0; i < N; i++)
+                for (int j = 0; j < N; j++) {
+                    const double ss = ((i < nvec) == (j < nvec)) ? 1.0 : -1.0;
+                    B[(int64_t)i * N + j] = ss * conj(tmp[(int64_t)j * N + i]);
+                }
+        }
+    }
+    if (scale != 1.0)
+        for (int64_t e = 0; e < 9 * NN; e++) L9[e] *= scale;
+}
+
+int oracle_apply_generated(const int L[4], int N, int kind, uint64_t seed, int scale_log2, const double *v_,
+                           double *y_)
+{
+    if (N > MAXN || kind < 0 || kind > 3) return -1;
+    const cplx *v = (const cplx *)v_;
+    cplx *y = (cplx *)y_;
+    const int64_t V = volume_of(L);
+    const int64_t NN = (int64_t)N * N;
+    const uint64_t tag = kind >= 2 ? 4 : 1;
+    const uint64_t base = sm64(seed ^ (tag << 56));
+    const double scale = ldexp(1.0, scale_log2);
+    int rc = 0;
+#pragma omp parallel
+    {
+        cplx *L9 = malloc(sizeof(cplx) * 10 * NN);
+        if (!L9) {
+#pragma omp atomic write
+            rc = -2;
+        } else {
+#pragma omp for schedule(dynamic, 16)
+            for (int64_t s = 0; s < V; s++) {
+                int x[4];
+                coords_of(L, s, x);
+                gen_site_links(L, N, kind, base, scale, x, L9, L9 + 9 * NN);
+                cplx acc[MAXN];
+                for (int i = 0; i < N; i++) acc[i] = 0;
+                matvec_acc(N, L9 + 8 * NN, v + s * N, acc);                              /* X(x) v(x)        */
+                for (int mu = 0; mu < 4; mu++) {
+                    int64_t sf = hop(L, x, mu, +1), sb = hop(L, x, mu, -1);
+                    matvec_acc(N, L9 + (2 * mu) * NN, v + sf * N, acc);                   /* L_{2mu} v(x+mu)   */
+                    matvec_acc(N, L9 + (2 * mu + 1) * NN, v + sb * N, acc);               /* L_{2mu+1} v(x-mu) */
+                }
+                for (int i = 0; i < N; i++) y[s * N + i] = acc[i];
+            }
+            free(L9);
+        }
+    }
+    return rc;
+}
+
 /* tau3 = diag(+1 x Nvec, -1 x Nvec) (PAPER.md:121 footnote 1; R5/R6). */
 static void tau3(int64_t V, int N, const cplx *in, cplx *out)
 {

@@ -305,3 +305,35 @@ def test_quantised_hermitian_links_stay_hermitian():
     w = synth.vector(dims, N, tag=synth.TAG_W)
     np.testing.assert_allclose(oracle.apply_dagger_tau3(dims, Lq, w), oracle.adjoint(dims, Lq, w),
                                rtol=0, atol=1e-13)
+
+
+# ---------------------------------------------------------------- matrix-free mode (full-size parity)
+@pytest.mark.parametrize("kind", ["general", "hermitian", "ti_general", "ti_hermitian"])
+@pytest.mark.parametrize("dims,N", [((2, 3, 2, 3), 48), ((3, 2, 1, 4), 64), ((1, 1, 1, 1), 48)])
+def test_apply_generated_is_apply_on_synth_links(kind, dims, N):
+    """The matrix-free oracle regenerates the links per site with its own copy of the c.3
+    recipe; it must equal oracle.apply on synth.links bit for bit (same values, same term
+    order) -- which pins its generator to synth (itself pinned by the splitmix64 test vector)
+    and its arithmetic to apply (pinned by P1-P10)."""
+    v = synth.vector(dims, N)
+    L = synth.links(dims, N, kind=kind, scale_log2=-4)
+    ref = oracle.apply(dims, L, v)
+    got = oracle.apply_generated(dims, N, v, kind=kind, scale_log2=-4)
+    np.testing.assert_array_equal(got, ref)
+
+
+def test_apply_generated_plane_wave_closed_form():
+    """Independent pin: translation-invariant links + a plane wave give the closed form of P4
+    (SURVEY c.4), without going through oracle.apply."""
+    dims, N = (3, 4, 3, 5), 48
+    L1 = synth.links((1, 1, 1, 1), N, kind="ti_general")[0]
+    n = np.array([1, 2, 0, 3])
+    p = 2 * np.pi * n / np.array(dims)
+    x = synth.site_coords(dims, np.arange(synth.volume(dims)))
+    u = synth.vector((1, 1, 1, 1), N)[0]
+    phase = np.exp(1j * (x @ p))
+    v = phase[:, None] * u[None, :]
+    M = L1[8] + sum(L1[2 * mu] * np.exp(1j * p[mu]) + L1[2 * mu + 1] * np.exp(-1j * p[mu]) for mu in range(4))
+    ref = phase[:, None] * (M @ u)[None, :]
+    got = oracle.apply_generated(dims, N, v, kind="ti_general")
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
