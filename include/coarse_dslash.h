@@ -72,7 +72,8 @@ typedef enum {
     CD_ERR_OOM = -3,          /* device or host allocation failed                      */
     CD_ERR_CUDA = -4,         /* CUDA runtime error (message has cudaGetErrorString)   */
     CD_ERR_NCCL = -5,         /* NCCL error or libnccl.so.2 not loadable               */
-    CD_ERR_MISMATCH = -6      /* objects from different contexts / precisions          */
+    CD_ERR_MISMATCH = -6,     /* objects from different contexts / precisions          */
+    CD_ERR_COMM = -7          /* peer halo transport fault (a neighbour's halo never arrived) */
 } cd_status;
 
 typedef enum { CD_FP32 = 0, CD_FP16 = 1 } cd_precision;    /* storage; arithmetic is fp32   */
@@ -91,7 +92,23 @@ typedef enum {
     CD_OPT_HALO_SELF_MASK = 2, /* bit mu: route dim mu through the halo path even when P_mu = 1
                                   (self exchange; exercises pack/exchange/halo kernels on 1 GPU).
                                   Only valid before the first apply. */
-    CD_OPT_PDL = 3             /* 1 = programmatic dependent launch between kernels (default 1) */
+    CD_OPT_PDL = 3,            /* 1 = programmatic dependent launch between kernels (default 1) */
+    CD_OPT_TRANSPORT = 4,      /* halo transport:
+                                    0 auto (default): peer if connected, else NCCL if the context
+                                      has a communicator, else device copy (self exchanges only);
+                                    1 NCCL: ncclSend/ncclRecv in one group on the comm stream; on a
+                                      1-rank context this creates a 1-rank communicator and the self
+                                      exchanges of CD_OPT_HALO_SELF_MASK go through NCCL self
+                                      send/recv (the multi-rank group code on one GPU);
+                                    2 peer: the halo pack kernel stores the faces straight into the
+                                      neighbours' CUDA-IPC-mapped receive windows over NVLink and
+                                      signals arrival counters; the receiver waits on the device
+                                      (needs cd_context_peer_handle / cd_context_peer_connect);
+                                    3 device copy (self exchanges only). */
+    CD_OPT_NCCL_SM_RESERVE = 5,/* SMs the persistent interior kernel leaves free while an NCCL halo
+                                  exchange is in flight (its kernels need SMs to progress); default 8 */
+    CD_OPT_PEER_TIMEOUT_MS = 6 /* peer transport: give up waiting for a neighbour's halo after this
+                                  long (the context then reports CD_ERR_COMM); default 60000 */
 } cd_option;
 
 typedef struct {
@@ -117,14 +134,29 @@ const char *cd_last_error(void);
 int cd_get_unique_id(uint8_t out_id[128]);
 
 /* Create a context on CUDA device `device` for rank `rank` of `nranks`.
- * nccl_id: NULL iff nranks == 1; else the 128-byte id from cd_get_unique_id (collective:
- * all ranks call this concurrently).  Allocates halo/scratch buffers (device memory).
+ * nccl_id: the 128-byte id from cd_get_unique_id (collective: all ranks call this
+ * concurrently; NCCL transport), or NULL -- always for nranks == 1; for nranks > 1 the
+ * context then has no NCCL communicator and must use the peer transport (connect it before
+ * the first collective call).  Allocates halo/scratch buffers (device memory).
  * Errors: CD_ERR_INVALID (geometry), CD_ERR_UNSUPPORTED (nvec), CD_ERR_CUDA, CD_ERR_NCCL. */
 int cd_context_create(const cd_geometry *geom, int device, int nranks, int rank, const uint8_t *nccl_id,
                       cd_context **out);
 
-/* Destroy a context (synchronises its device; fields/links of it must be freed first). */
+/* Destroy a context (synchronises its device; fields/links of it must be freed first).
+ * Peer-connected contexts: every rank must have finished its collective calls (e.g. a
+ * barrier) before any rank destroys its context -- a neighbour may still be writing into
+ * this rank's window. */
 int cd_context_destroy(cd_context *ctx);
+
+/* Peer transport setup (collective, two steps).  cd_context_peer_handle
+ * allocates this rank's receive window (zeroed, synchronously) and returns its 64-byte CUDA
+ * IPC handle; the caller all-gathers the handles of all ranks (e.g. torch.distributed) into
+ * handles[nranks][64] and passes them to cd_context_peer_connect, which maps the windows of
+ * this rank's halo neighbours (NVLink / NVSwitch peers, or the same GPU for several processes
+ * on one device).  Set CD_OPT_HALO_SELF_MASK before this.  After connect the transport option
+ * "auto" selects the peer transport. */
+int cd_context_peer_handle(cd_context *ctx, uint8_t out_handle[64]);
+int cd_context_peer_connect(cd_context *ctx, const uint8_t *handles, int nranks);
 
 /* Set a cd_option (see the enum).  CD_ERR_INVALID for an unknown option or bad value. */
 int cd_context_set_option(cd_context *ctx, int option, int64_t value);
@@ -316,6 +348,13 @@ int coarse_prolong(const cd_transfer *t, void *fine_out, const cd_field *coarse_
  * and copies to dst (host or device).  *bytes receives the size; dst may be NULL to query. */
 int coarse_halo_pack(cd_context *ctx, const cd_field *in, void *dst, int dst_on_device, size_t *bytes,
                      void *stream);
+
+/* One halo exchange of `in` with the context's transport and nothing else (no stencil): the
+ * pack (+ transfer), the exchange and the arrival wait, all ordered on `stream`; then the
+ * received buffer (R13 wire order, *bytes long) is copied to dst (host or device;
+ * NULL: no copy -- e.g. to time the exchange alone).  Collective like coarse_dslash_apply. */
+int coarse_halo_exchange(cd_context *ctx, const cd_field *in, void *dst, int dst_on_device, size_t *bytes,
+                         void *stream);
 
 /* Write the L2-flush scratch (bench utility): a kernel writing `bytes` of device memory. */
 int cd_flush_l2(cd_context *ctx, size_t bytes, void *stream);

@@ -23,10 +23,13 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CD_LIB_PATH") or os.path.join(_HERE, "libcoarse_dslash.so")   # override: A/B experiments
 
 CD_OK, CD_ERR_INVALID, CD_ERR_UNSUPPORTED, CD_ERR_OOM, CD_ERR_CUDA, CD_ERR_NCCL, CD_ERR_MISMATCH = 0, -1, -2, -3, -4, -5, -6
+CD_ERR_COMM = -7
 CD_FP32, CD_FP16 = 0, 1
 CD_C64, CD_C128 = 0, 1
 CD_LINKS_GENERAL, CD_LINKS_HERMITIAN, CD_LINKS_TI_GENERAL, CD_LINKS_TI_HERMITIAN = 0, 1, 2, 3
 CD_OPT_VARIANT, CD_OPT_TUNE, CD_OPT_HALO_SELF_MASK, CD_OPT_PDL = 0, 1, 2, 3
+CD_OPT_TRANSPORT, CD_OPT_NCCL_SM_RESERVE, CD_OPT_PEER_TIMEOUT_MS = 4, 5, 6
+TRANSPORT = {"auto": 0, "nccl": 1, "peer": 2, "copy": 3}
 
 PREC = {"fp32": CD_FP32, "fp16": CD_FP16, CD_FP32: CD_FP32, CD_FP16: CD_FP16}
 LINK_KIND = {"general": 0, "hermitian": 1, "ti_general": 2, "ti_hermitian": 3}
@@ -44,7 +47,7 @@ EXPORTS = (
     "coarse_links_compress_hermitian", "coarse_field_bytes_parity", "coarse_field_alloc_parity",
     "coarse_links_prepare_eo", "coarse_dslash_apply_eo", "coarse_transfer_create", "coarse_transfer_free",
     "coarse_transfer_fine_bytes", "coarse_transfer_read_basis", "coarse_transfer_orthonormalise", "coarse_restrict",
-    "coarse_prolong",
+    "coarse_prolong", "cd_context_peer_handle", "cd_context_peer_connect", "coarse_halo_exchange",
 )
 
 
@@ -126,6 +129,9 @@ def _load():
         "coarse_transfer_orthonormalise": ([P, P], I),
         "coarse_restrict": ([P, P, P, P], I),
         "coarse_prolong": ([P, P, P, P], I),
+        "cd_context_peer_handle": ([P, P], I),
+        "cd_context_peer_connect": ([P, P, I], I),
+        "coarse_halo_exchange": ([P, P, P, I, ctypes.POINTER(SZ), P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -306,6 +312,44 @@ class Context:
 
     def links_generate(self, prec="fp32", kind="general", seed=0x1612, scale_log2=0, stream=None):
         return Links(self, prec, coarse_links_generate(self.handle, prec, kind, seed, scale_log2, stream))
+
+    def set_transport(self, name):
+        """Halo transport: "auto", "nccl", "peer" or "copy" (CD_OPT_TRANSPORT)."""
+        self.set_option(CD_OPT_TRANSPORT, TRANSPORT[name] if isinstance(name, str) else int(name))
+
+    def peer_handle(self) -> bytes:
+        """Allocate + export this rank's peer window (64-byte CUDA IPC handle)."""
+        buf = (ctypes.c_uint8 * 64)()
+        _check(lib.cd_context_peer_handle(self.handle, buf))
+        return bytes(buf)
+
+    def peer_connect(self, handles):
+        """Map the neighbours' windows; handles: the 64-byte handles of ranks 0..nranks-1."""
+        blob = b"".join(bytes(h) for h in handles)
+        buf = (ctypes.c_uint8 * len(blob)).from_buffer_copy(blob)
+        _check(lib.cd_context_peer_connect(self.handle, buf, len(handles)))
+
+    def connect_peers(self, group=None):
+        """Collective: exchange peer-window handles over torch.distributed and connect."""
+        import torch.distributed as dist
+        h = self.peer_handle()
+        allh = [None] * dist.get_world_size(group)
+        dist.all_gather_object(allh, h, group=group)
+        self.peer_connect(allh)
+
+    def halo_exchange(self, field, stream=None, copy_out=True) -> bytes:
+        """One halo exchange of `field` (pack + transport + arrival wait); returns the received
+        buffer in the DESIGN.md R13 wire order (collective)."""
+        n = ctypes.c_size_t()
+        if not copy_out:
+            _check(lib.coarse_halo_exchange(self.handle, field.handle, None, 0, ctypes.byref(n),
+                                            _stream(stream, self.device)))
+            return b""
+        _check(lib.coarse_halo_pack(self.handle, field.handle, None, 0, ctypes.byref(n), _stream(stream, self.device)))
+        buf = np.zeros(max(n.value, 16), np.uint8)
+        _check(lib.coarse_halo_exchange(self.handle, field.handle, buf.ctypes.data, 0, ctypes.byref(n),
+                                        _stream(stream, self.device)))
+        return buf[:n.value].tobytes()
 
     def halo_pack(self, field, stream=None) -> bytes:
         n = ctypes.c_size_t()

@@ -26,7 +26,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
           "-I", os.path.join(ROOT, "include"), "-I", CSRC] + os.environ.get("CD_EXTRA_NVCC_FLAGS", "").split()
-SOURCES = ["api.cpp", "comm.cpp", "fields.cu", "mrhs.cu", "eo.cu", "transfer.cu", "dslash_f32_24.cu", "dslash_f32_32.cu", "dslash_f16_24.cu",
+SOURCES = ["api.cpp", "comm.cpp", "fields.cu", "mrhs.cu", "eo.cu", "transfer.cu", "peer.cu", "dslash_f32_24.cu", "dslash_f32_32.cu", "dslash_f16_24.cu",
            "dslash_f16_32.cu"]
 
 

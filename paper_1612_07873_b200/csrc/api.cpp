@@ -28,10 +28,10 @@ cudaError_t launch_halo_f32_24(const ApplyArgs &, cudaStream_t);
 cudaError_t launch_halo_f32_32(const ApplyArgs &, cudaStream_t);
 cudaError_t launch_halo_f16_24(const ApplyArgs &, cudaStream_t);
 cudaError_t launch_halo_f16_32(const ApplyArgs &, cudaStream_t);
-cudaError_t launch_pack_f32_24(const void *, void *, const KGeom &, cudaStream_t);
-cudaError_t launch_pack_f32_32(const void *, void *, const KGeom &, cudaStream_t);
-cudaError_t launch_pack_f16_24(const void *, void *, const KGeom &, cudaStream_t);
-cudaError_t launch_pack_f16_32(const void *, void *, const KGeom &, cudaStream_t);
+cudaError_t launch_pack_f32_24(const void *, const PackDst &, const KGeom &, cudaStream_t);
+cudaError_t launch_pack_f32_32(const void *, const PackDst &, const KGeom &, cudaStream_t);
+cudaError_t launch_pack_f16_24(const void *, const PackDst &, const KGeom &, cudaStream_t);
+cudaError_t launch_pack_f16_32(const void *, const PackDst &, const KGeom &, cudaStream_t);
 int variant_count_f32_24();
 int variant_count_f32_32();
 int variant_count_f16_24();
@@ -155,7 +155,7 @@ cudaError_t launch_hermdev(cd_precision p, int nv, const void *f, const KGeom &g
     return PICK(p, nv, launch_hermdev_f32_24(f, g, d, s, lh, lo), launch_hermdev_f32_32(f, g, d, s, lh, lo),
                 launch_hermdev_f16_24(f, g, d, s, lh, lo), launch_hermdev_f16_32(f, g, d, s, lh, lo));
 }
-cudaError_t launch_pack(cd_precision p, int nv, const void *f, void *d, const KGeom &g, cudaStream_t s)
+cudaError_t launch_pack(cd_precision p, int nv, const void *f, const PackDst &d, const KGeom &g, cudaStream_t s)
 {
     return PICK(p, nv, launch_pack_f32_24(f, d, g, s), launch_pack_f32_32(f, d, g, s), launch_pack_f16_24(f, d, g, s),
                 launch_pack_f16_32(f, d, g, s));
@@ -344,7 +344,11 @@ static int setup_halo(cd_context *c)
     if (!faces.empty())
         CUDA_TRY(cudaMemcpy(c->face_sites, faces.data(), sizeof(int) * faces.size(), cudaMemcpyHostToDevice),
                  "cudaMemcpy(faces)");
-    if (!c->comm_stream) CUDA_TRY(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking), "stream");
+    if (!c->comm_stream) {   // highest priority: the pack (+ peer put) is dispatched ahead of the interior
+        int lo = 0, hi = 0;
+        CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi), "cudaDeviceGetStreamPriorityRange");
+        CUDA_TRY(cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi), "stream");
+    }
     if (!c->ev_in) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming), "event");
     if (!c->ev_halo) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming), "event");
     c->halo_ready = true;
@@ -396,6 +400,7 @@ static void ctx_release(cd_context *c)
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->ev_in) cudaEventDestroy(c->ev_in);
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+    peer_release(c);
     comm_destroy(c->comm);
     delete c;
 }
@@ -425,7 +430,7 @@ int cd_context_create(const cd_geometry *geom, int device, int nranks, int rank,
     *out = nullptr;
     int r0 = check_geometry(geom, nranks, rank);
     if (r0 != CD_OK) return r0;
-    if ((nranks > 1) != (nccl_id != nullptr)) return fail(CD_ERR_INVALID, "nccl_id must be given iff nranks > 1");
+    if (nranks == 1 && nccl_id != nullptr) return fail(CD_ERR_INVALID, "nccl_id must be NULL for nranks == 1");
     int ndev = 0;
     CUDA_TRY(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
     if (device < 0 || device >= ndev) return fail(CD_ERR_INVALID, "bad device");
@@ -473,7 +478,7 @@ int cd_context_create(const cd_geometry *geom, int device, int nranks, int rank,
     if (const char *ev = getenv("CD_TUNE")) c->tune = atoi(ev) ? 1 : 0;
     if (const char *ev = getenv("CD_VARIANT")) c->force_variant = atoi(ev);
     if (const char *ev = getenv("CD_PDL")) c->pdl = atoi(ev) ? 1 : 0;
-    if (nranks > 1) {
+    if (nranks > 1 && nccl_id) {
         std::string err;
         int r = comm_create(nccl_id, nranks, rank, &c->comm, err);
         if (r != CD_OK) {
@@ -518,9 +523,35 @@ int cd_context_set_option(cd_context *c, int option, int64_t value)
     case CD_OPT_PDL:
         c->pdl = value ? 1 : 0;
         return CD_OK;
+    case CD_OPT_TRANSPORT: {
+        if (value < TR_AUTO || value > TR_COPY) return fail(CD_ERR_INVALID, "transport must be 0 (auto), 1 (NCCL), 2 (peer), 3 (copy)");
+        if (value == TR_NCCL && !c->comm) {
+            if (c->nranks != 1)
+                return fail(CD_ERR_INVALID, "NCCL transport on a multi-rank context needs the nccl_id at creation");
+            std::string err;
+            int r = comm_create_self(&c->comm, err);   // 1 rank: the halo self exchanges go through NCCL
+            if (r != CD_OK) return fail(r, err);
+        }
+        if (value == TR_PEER && !c->peer_ready)
+            return fail(CD_ERR_INVALID, "peer transport needs cd_context_peer_handle + cd_context_peer_connect first");
+        if (value == TR_COPY && c->nranks != 1) return fail(CD_ERR_INVALID, "device-copy transport is single-rank");
+        c->transport = (int)value;
+        c->chosen.clear();   // the interior's SM budget depends on the transport
+        return CD_OK;
+    }
+    case CD_OPT_NCCL_SM_RESERVE:
+        if (value < 0 || value >= c->num_sms) return fail(CD_ERR_INVALID, "SM reserve must be in [0, num_sms)");
+        c->nccl_sm_reserve = (int)value;
+        c->chosen.clear();
+        return CD_OK;
+    case CD_OPT_PEER_TIMEOUT_MS:
+        if (value < 1) return fail(CD_ERR_INVALID, "timeout must be >= 1 ms");
+        c->peer_timeout_ns = (unsigned long long)value * 1000000ull;
+        return CD_OK;
     case CD_OPT_HALO_SELF_MASK: {
         if (value < 0 || value > 15) return fail(CD_ERR_INVALID, "mask must be in [0, 15]");
         if (c->applied) return fail(CD_ERR_INVALID, "HALO_SELF_MASK must be set before the first apply");
+        if (c->win) return fail(CD_ERR_INVALID, "HALO_SELF_MASK must be set before cd_context_peer_handle");
         for (int mu = 0; mu < 4; mu++)
             if (((value >> mu) & 1) && c->geom.proc_grid[mu] != 1)
                 return fail(CD_ERR_INVALID, "HALO_SELF_MASK dims must have proc_grid == 1");
@@ -654,8 +685,7 @@ int coarse_field_free(cd_field *f)
 {
     API_BEGIN
     if (!f) return fail(CD_ERR_INVALID, "field is NULL");
-    CTX_GUARD(f->ctx);
-    if (f->owned) cudaFree(f->base);
+    if (f->owned) cudaFree(f->base);   // cudaFree needs no current device (and f->ctx may be gone)
     delete f;
     return CD_OK;
     API_END
@@ -961,7 +991,6 @@ int coarse_links_free(cd_links *l)
 {
     API_BEGIN
     if (!l) return fail(CD_ERR_INVALID, "links is NULL");
-    CTX_GUARD(l->ctx);
     if (l->aux) cudaFree(l->aux);
     if (l->tbuf) cudaFree(l->tbuf);
     cudaFree(l->base);
@@ -990,11 +1019,50 @@ static int check_objs(const cd_links *l, const cd_field *out, const cd_field *in
 // Tuning (first call of a key, "auto-tuned upon first call and cached") times
 // every variant with CUDA events on the caller's stream; trial launches write `out` only.
 // Every dslash launch gets the next sequence number (the ring kernel's ticket slot).
+// While an NCCL halo exchange is in flight the persistent interior kernel leaves
+// CD_OPT_NCCL_SM_RESERVE SMs free: NCCL's copy kernels need SMs to make progress, and the ring
+// (one 227 KB CTA per SM) would otherwise hold every SM until the interior is done.
 static cudaError_t launch_next(cd_context *c, cd_precision p, int id, ApplyArgs a, cudaStream_t s, bool pdl)
 {
     a.seq = c->seq++;
-    return launch_dslash(p, id, a, s, pdl, c->num_sms);
+    const int sms = (a.halo && transport_of(c) == TR_NCCL) ? c->num_sms - c->nccl_sm_reserve : c->num_sms;
+    return launch_dslash(p, id, a, s, pdl, sms);
 }
+
+// Split (multi-rank or self-halo) apply: pack (+ transfer) on the high-priority
+// comm stream overlapped with the interior kernel on s, then -- once the halo has landed -- the
+// halo-term kernel for the remote hops of the face sites.
+extern "C++" {
+template <class Interior, class Term>
+static int run_split(cd_context *c, cd_precision p, const void *in, ApplyArgs &a, cudaStream_t s, Interior interior,
+                     Term term)
+{
+    const cd_halo_plan pl = ctx_plan(c, p);
+    std::string err;
+    if (transport_of(c) == TR_PEER) {   // exchange epochs are host counters baked into the launches
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(s, &cap);
+        if (cap != cudaStreamCaptureStatusNone)
+            return fail(CD_ERR_UNSUPPORTED, "peer-transport applies cannot be captured in a CUDA graph (per-exchange epochs)");
+    }
+    HaloX x;
+    int r = halo_begin(c, pl, &x, err);
+    if (r != CD_OK) return fail(r, err);
+    a.recv = x.recv;
+    CUDA_TRY(cudaEventRecord(c->ev_in, s), "cudaEventRecord");
+    CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->ev_in, 0), "cudaStreamWaitEvent");
+    CUDA_TRY(launch_pack(p, c->nvec, in, x.pd, a.g, c->comm_stream), "halo pack");
+    r = halo_post(c, pl, x, c->comm_stream, err);
+    if (r != CD_OK) return fail(r, err);
+    CUDA_TRY(cudaEventRecord(c->ev_halo, c->comm_stream), "cudaEventRecord");
+    CUDA_TRY(interior(), "dslash interior launch");
+    CUDA_TRY(cudaStreamWaitEvent(s, c->ev_halo, 0), "cudaStreamWaitEvent");
+    r = halo_finish(c, x, s, err);
+    if (r != CD_OK) return fail(r, err);
+    CUDA_TRY(term(), "halo kernel");
+    return CD_OK;
+}
+}  // extern "C++"
 
 static int resolve_variant(cd_context *c, cd_precision p, int dag, const ApplyArgs &a, cudaStream_t s, int *id)
 {
@@ -1102,9 +1170,9 @@ static int do_apply(const cd_links *l, cd_field *out, const cd_field *in, void *
         return fail(CD_ERR_INVALID, "compressed links were built under a different halo split (set CD_OPT_HALO_SELF_MASK "
                                     "before coarse_links_compress_hermitian)");
     c->applied = true;
-    if (c->comm) {
+    {
         std::string err;
-        r = comm_check(c->comm, err);
+        r = transport_check(c, err);
         if (r != CD_OK) return fail(r, err);
     }
     ApplyArgs a{};
@@ -1126,24 +1194,13 @@ static int do_apply(const cd_links *l, cd_field *out, const cd_field *in, void *
         a.g = halo_geom(c, l->prec);
         a.halo = 1;
         a.scratch = c->face_scratch;
-        a.recv = c->recv_buf;
         a.face_sites = c->face_sites;
         a.n_face = c->n_face;
         a.lhalo = l->aux;
         for (int mu = 0; mu < 4; mu++) a.lhoff[mu] = l->lhoff[mu];
-        CUDA_TRY(cudaEventRecord(c->ev_in, s), "cudaEventRecord");
-        CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->ev_in, 0), "cudaStreamWaitEvent");
-        CUDA_TRY(launch_pack(l->prec, c->nvec, in->base, c->send_buf, a.g, c->comm_stream), "halo pack");
-        {
-            std::string err;
-            r = halo_exchange(c, ctx_plan(c, l->prec), c->comm_stream, err);
-            if (r != CD_OK) return fail(r, err);
-        }
-        CUDA_TRY(cudaEventRecord(c->ev_halo, c->comm_stream), "cudaEventRecord");
-        CUDA_TRY(launch_fgh(l->prec, a, s, false), "compressed dslash interior launch");
-        CUDA_TRY(cudaStreamWaitEvent(s, c->ev_halo, 0), "cudaStreamWaitEvent");
-        CUDA_TRY(launch_fgh_halo(l->prec, a, s), "compressed halo kernel");
-        return CD_OK;
+        return run_split(
+            c, l->prec, in->base, a, s, [&] { return launch_fgh(l->prec, a, s, false); },
+            [&] { return launch_fgh_halo(l->prec, a, s); });
     }
     a.g = halo ? halo_geom(c, l->prec) : c->kg;
     a.halo = halo ? 1 : 0;
@@ -1162,21 +1219,9 @@ static int do_apply(const cd_links *l, cd_field *out, const cd_field *in, void *
         CUDA_TRY(launch_next(c, l->prec, id, a, s, c->pdl != 0), "dslash launch");
         return CD_OK;
     }
-    // multi-rank: pack + exchange on the comm stream, interior on the caller's stream,
-    // then the halo-term kernel once the exchange has landed (overlap).
-    CUDA_TRY(cudaEventRecord(c->ev_in, s), "cudaEventRecord");
-    CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->ev_in, 0), "cudaStreamWaitEvent");
-    CUDA_TRY(launch_pack(l->prec, c->nvec, in->base, c->send_buf, a.g, c->comm_stream), "halo pack");
-    {
-        std::string err;
-        r = halo_exchange(c, ctx_plan(c, l->prec), c->comm_stream, err);
-        if (r != CD_OK) return fail(r, err);
-    }
-    CUDA_TRY(cudaEventRecord(c->ev_halo, c->comm_stream), "cudaEventRecord");
-    CUDA_TRY(launch_next(c, l->prec, id, a, s, false), "dslash interior launch");
-    CUDA_TRY(cudaStreamWaitEvent(s, c->ev_halo, 0), "cudaStreamWaitEvent");
-    CUDA_TRY(launch_halo(l->prec, a, s), "halo kernel");
-    return CD_OK;
+    return run_split(
+        c, l->prec, in->base, a, s, [&] { return launch_next(c, l->prec, id, a, s, false); },
+        [&] { return launch_halo(l->prec, a, s); });
 }
 
 int coarse_dslash_apply(const cd_links *l, cd_field *out, const cd_field *in, void *stream)
@@ -1203,16 +1248,34 @@ static bool eo_geometry_ok(const cd_context *c)
     return true;
 }
 
+// The even-odd stages reuse the full operator's fp32 vector-halo plan and transport.
 struct EoExchange {
     cd_context *c;
+    cd_halo_plan pl;
+    HaloX x;
+    cudaStream_t s;
     int status = CD_OK;
     std::string err;
 };
-static cudaError_t eo_exchange(void *p)
+static cudaError_t eo_begin(void *p, PackDst *pd, const void **recv)
 {
-    EoExchange *x = static_cast<EoExchange *>(p);
-    x->status = halo_exchange(x->c, ctx_plan(x->c, CD_FP32), x->c->comm_stream, x->err);
-    return x->status == CD_OK ? cudaSuccess : cudaErrorUnknown;
+    EoExchange *e = static_cast<EoExchange *>(p);
+    e->status = halo_begin(e->c, e->pl, &e->x, e->err);
+    *pd = e->x.pd;
+    *recv = e->x.recv;
+    return e->status == CD_OK ? cudaSuccess : cudaErrorUnknown;
+}
+static cudaError_t eo_post(void *p)
+{
+    EoExchange *e = static_cast<EoExchange *>(p);
+    e->status = halo_post(e->c, e->pl, e->x, e->c->comm_stream, e->err);
+    return e->status == CD_OK ? cudaSuccess : cudaErrorUnknown;
+}
+static cudaError_t eo_finish(void *p)
+{
+    EoExchange *e = static_cast<EoExchange *>(p);
+    e->status = halo_finish(e->c, e->x, e->s, e->err);
+    return e->status == CD_OK ? cudaSuccess : cudaErrorUnknown;
 }
 
 size_t coarse_field_bytes_parity(const cd_context *c, cd_precision p)
@@ -1288,9 +1351,9 @@ int coarse_dslash_apply_eo(const cd_links *l, cd_field *out, const cd_field *in,
     if (out->base == in->base) return fail(CD_ERR_INVALID, "out must not alias in");
     cd_context *c = l->ctx;
     c->applied = true;
-    if (c->comm) {
+    {
         std::string err;
-        const int r = comm_check(c->comm, err);
+        const int r = transport_check(c, err);
         if (r != CD_OK) return fail(r, err);
     }
     EoApply e{};
@@ -1304,17 +1367,17 @@ int coarse_dslash_apply_eo(const cd_links *l, cd_field *out, const cd_field *in,
     e.pdl = c->pdl != 0;
     e.halo = c->kg.split != 0 ? 1 : 0;
     e.g = e.halo ? halo_geom(c, CD_FP32) : c->kg;
-    EoExchange ex{c};
+    EoExchange ex{c, ctx_plan(c, CD_FP32), {}, e.s};
     if (e.halo) {
         e.comm_stream = c->comm_stream;
         e.ev_in = c->ev_in;
         e.ev_halo = c->ev_halo;
-        e.send = c->send_buf;
-        e.recv = c->recv_buf;
         e.scratch = c->face_scratch;
         e.face_sites = c->face_sites;
         e.n_face = c->n_face;
-        e.exchange = eo_exchange;
+        e.begin = eo_begin;
+        e.post = eo_post;
+        e.finish = eo_finish;
         e.exchange_arg = &ex;
     }
     const cudaError_t ce = launch_eo_apply(c->nvec, e);
@@ -1348,9 +1411,9 @@ int coarse_dslash_apply_mrhs(const cd_links *l, cd_field *out, const cd_field *i
     // multi-rank: the face blocks of every split dim travel in the tensor-core layout
     // ([f][rhs block] records of 128 rhs); the interior sites run while the exchange is in flight,
     // the face sites after it (their remote hops read the receive buffer).
-    if (c->comm) {
+    {
         std::string err;
-        const int r = comm_check(c->comm, err);
+        const int r = transport_check(c, err);
         if (r != CD_OK) return fail(r, err);
     }
     const int nrb = in->nrhs / 128;
@@ -1555,10 +1618,75 @@ int coarse_halo_pack(cd_context *c, const cd_field *in, void *dst, int dst_on_de
     if (!dst) return CD_OK;
     cudaStream_t s = S(stream);
     KGeom g = halo_geom(c, in->prec);
-    CUDA_TRY(launch_pack(in->prec, c->nvec, in->base, c->send_buf, g, s), "halo pack");
+    const cd_halo_plan pl = ctx_plan(c, in->prec);
+    PackDst pd{};
+    for (int mu = 0; mu < 4; mu++)
+        for (int b = 0; b < 2; b++) pd.dst[mu][b] = static_cast<unsigned char *>(c->send_buf) + pl.block_offset[mu][b];
+    CUDA_TRY(launch_pack(in->prec, c->nvec, in->base, pd, g, s), "halo pack");
     CUDA_TRY(cudaMemcpyAsync(dst, c->send_buf, n, dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s),
              "cudaMemcpyAsync(pack)");
     if (!dst_on_device) CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    return CD_OK;
+    API_END
+}
+
+int coarse_halo_exchange(cd_context *c, const cd_field *in, void *dst, int dst_on_device, size_t *bytes, void *stream)
+{
+    API_BEGIN
+    if (!c || !in || !bytes) return fail(CD_ERR_INVALID, "ctx/in/bytes is NULL");
+    if (in->ctx != c) return fail(CD_ERR_MISMATCH, "field from another context");
+    if (in->nrhs != 1 || in->parity >= 0) return fail(CD_ERR_INVALID, "needs an ordinary full-lattice field");
+    CTX_GUARD(c);
+    if (c->kg.split == 0) {
+        *bytes = 0;
+        return CD_OK;
+    }
+    std::string err;
+    int r = transport_check(c, err);
+    if (r != CD_OK) return fail(r, err);
+    c->applied = true;
+    cudaStream_t s = S(stream);
+    const cd_halo_plan pl = ctx_plan(c, in->prec);
+    *bytes = (size_t)pl.total_bytes;
+    HaloX x;
+    r = halo_begin(c, pl, &x, err);
+    if (r != CD_OK) return fail(r, err);
+    CUDA_TRY(launch_pack(in->prec, c->nvec, in->base, x.pd, halo_geom(c, in->prec), s), "halo pack");
+    r = halo_post(c, pl, x, s, err);
+    if (r != CD_OK) return fail(r, err);
+    r = halo_finish(c, x, s, err);
+    if (r != CD_OK) return fail(r, err);
+    if (dst) {
+        CUDA_TRY(cudaMemcpyAsync(dst, x.recv, *bytes, dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s),
+                 "cudaMemcpyAsync(recv)");
+        if (!dst_on_device) CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    }
+    return CD_OK;
+    API_END
+}
+
+int cd_context_peer_handle(cd_context *c, uint8_t out_handle[64])
+{
+    API_BEGIN
+    if (!c || !out_handle) return fail(CD_ERR_INVALID, "ctx/out is NULL");
+    CTX_GUARD(c);
+    std::string err;
+    const size_t slot = std::max(halo_bytes(c, CD_FP32), halo_bytes(c, CD_FP16));
+    int r = peer_window_export(c, slot, out_handle, err);
+    if (r != CD_OK) return fail(r, err);
+    return CD_OK;
+    API_END
+}
+
+int cd_context_peer_connect(cd_context *c, const uint8_t *handles, int nranks)
+{
+    API_BEGIN
+    if (!c || !handles) return fail(CD_ERR_INVALID, "ctx/handles is NULL");
+    CTX_GUARD(c);
+    std::string err;
+    int r = peer_connect(c, handles, nranks, err);
+    if (r != CD_OK) return fail(r, err);
+    c->chosen.clear();
     return CD_OK;
     API_END
 }
@@ -1655,7 +1783,6 @@ int coarse_transfer_free(cd_transfer *t)
 {
     API_BEGIN
     if (!t) return fail(CD_ERR_INVALID, "transfer is NULL");
-    CTX_GUARD(t->ctx);
     cudaFree(t->W);
     delete t;
     return CD_OK;

@@ -72,6 +72,32 @@ struct TGeom {
 
 struct Comm;  // comm.cpp
 
+// Halo transports (CD_OPT_TRANSPORT).
+enum Transport { TR_AUTO = 0, TR_NCCL = 1, TR_PEER = 2, TR_COPY = 3 };
+
+// Peer window (TR_PEER): one cudaMalloc per rank, exported with CUDA IPC and mapped by the
+// neighbours.  Header: arrival counters [mu][blk] (u64), padded to kWinHeader; then two
+// receive slots of win_slot bytes (exchange e uses slot e % 2).
+constexpr size_t kWinHeader = 4096;
+constexpr int kPutCtas = 16;   // CTAs per (mu, blk) of every signalling kernel: +16 per block per exchange
+
+// Where the halo pack kernel writes block (mu, blk) (dst = block base incl. its offset) and,
+// for the peer transport, the receiver's arrival counter it bumps once per CTA (nullptr: none).
+struct PackDst {
+    unsigned char *dst[4][2];
+    unsigned long long *flag[4][2];
+};
+
+// Receiver side of one peer exchange: spin (acquire, system scope) until every block in `mask`
+// (bit 2mu+blk) has counter >= target; on timeout set *err and return (no hang).
+struct PeerWait {
+    const unsigned long long *flag;
+    unsigned mask;
+    unsigned long long target;
+    int *err;
+    unsigned long long timeout_ns;
+};
+
 struct TuneKey {
     int prec, dagger;
     bool operator<(const TuneKey &o) const { return prec != o.prec ? prec < o.prec : dagger < o.dagger; }
@@ -111,6 +137,18 @@ struct cd_context {
     cudaStream_t comm_stream = nullptr;
     cudaEvent_t ev_in = nullptr, ev_halo = nullptr;
     cd::Comm *comm = nullptr;
+    // halo transport
+    int transport = 0;                // CD_OPT_TRANSPORT
+    int nccl_sm_reserve = 8;          // CD_OPT_NCCL_SM_RESERVE: SMs the interior leaves to NCCL's kernels
+    unsigned char *win = nullptr;     // own peer window (kWinHeader + 2 slots)
+    size_t win_slot = 0;
+    unsigned char *peer_win[4][2] = {};   // window of the rank at +mu (dir 0) / -mu (dir 1)
+    std::vector<void *> ipc_opened;   // IPC mappings to close
+    bool peer_ready = false;
+    uint64_t epoch = 0;               // peer exchanges issued so far (identical sequence on every rank)
+    int *err_host = nullptr;          // host-mapped transport error word (peer wait timeouts)
+    int *err_dev = nullptr;
+    unsigned long long peer_timeout_ns = 60ull * 1000 * 1000 * 1000;
     // options
     int force_variant = -1;
     int tune = 1;
@@ -197,7 +235,14 @@ bool variant_valid(cd_precision p, int nvec, int id, const KGeom &g);
 int variant_heuristic(cd_precision p, int nvec, const KGeom &g, int num_sms);
 cudaError_t launch_dslash(cd_precision p, int id, const ApplyArgs &a, cudaStream_t s, bool pdl, int num_sms);
 cudaError_t launch_halo(cd_precision p, const ApplyArgs &a, cudaStream_t s);
-cudaError_t launch_pack(cd_precision p, int nvec, const void *field, void *send, const KGeom &g, cudaStream_t s);
+cudaError_t launch_pack(cd_precision p, int nvec, const void *field, const PackDst &d, const KGeom &g, cudaStream_t s);
+cudaError_t launch_peer_wait(const PeerWait &w, cudaStream_t s);
+// bulk peer put of one chunk: for every block in `mask`, len[mu][blk] bytes from src[mu][blk] to
+// d.dst[mu][blk], then bump d.flag[mu][blk] once per CTA (kPutCtas CTAs per block)
+cudaError_t launch_peer_put(const unsigned char *const src[4][2], const int64_t len[4][2], unsigned mask,
+                            const PackDst &d, cudaStream_t s);
+cudaError_t launch_copy_blocks(const unsigned char *const src[4][2], unsigned char *const dst[4][2],
+                               const int64_t len[4][2], unsigned mask, cudaStream_t s);
 
 cudaError_t launch_import(cd_precision p, int nvec, int64_t nsites, const void *src, int src_c128, void *dst,
                           cudaStream_t s, int nrhs = 1);
@@ -223,12 +268,15 @@ struct EoApply {              // one even-odd Schur apply (coarse_dslash_apply_e
     int halo;
     cudaStream_t comm_stream;
     cudaEvent_t ev_in, ev_halo;
-    void *send;
-    const void *recv;
     float2 *scratch;
     const int *face_sites;
     int n_face;
-    cudaError_t (*exchange)(void *);   // posts the halo exchange on comm_stream
+    // one halo exchange per stage: begin() gives the pack destinations and the receive buffer,
+    // post() starts the transfer on comm_stream after the pack, finish() orders the arrival
+    // before the halo kernel on s (peer transport: the wait kernel)
+    cudaError_t (*begin)(void *, PackDst *, const void **recv);
+    cudaError_t (*post)(void *);
+    cudaError_t (*finish)(void *);
     void *exchange_arg;
 };
 cudaError_t launch_eo_apply(int nvec, const EoApply &e);

@@ -279,4 +279,16 @@ __device__ __forceinline__ int kseq(int i) { return i == 0 ? 8 : i - 1; }
 template <typename T>
 __device__ __forceinline__ T shfl_xor(T v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
 
+// Peer transport: after a CTA has stored its part of a halo block into the
+// receiver's window, bump the receiver's arrival counter once (release, system scope; the
+// CTA barrier orders every thread's stores before thread 0's fence).
+__device__ __forceinline__ void signal_block(unsigned long long *flag)
+{
+    __syncthreads();
+    if (threadIdx.x == 0 && flag) {
+        __threadfence_system();
+        asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(flag) : "memory");
+    }
+}
+
 }  // namespace cd

@@ -2221,9 +2221,12 @@ __global__ void __launch_bounds__(32 * (2 * NV / Cfg<P, NV>::R)) dslash_halo(App
 
 // ------------------------------------------------------------------ halo pack
 // One launch for all split dims: blockIdx.y = (mu, block) pair index,
-// threads over the face's 16-B payload chunks and then its scales (fp16).
+// threads over the face's 16-B payload chunks and then its scales (fp16).  The destination of
+// block (mu, blk) is d.dst[mu][blk]: the local send buffer (NCCL / copy transports) or, for the
+// peer transport, the receive slot in the neighbour's window -- the pack IS the transfer (stores
+// over NVLink), and each CTA then bumps the receiver's arrival counter for that block.
 template <cd_precision P, int NV>
-__global__ void halo_pack(const unsigned char *field, unsigned char *send, KGeom g, int4 pairs)
+__global__ void halo_pack(const unsigned char *field, PackDst d, KGeom g, int4 pairs)
 {
     using Q = Cfg<P, NV>;
     constexpr int PREC = Q::F16 ? 4 * Q::N : 8 * Q::N;
@@ -2234,7 +2237,7 @@ __global__ void halo_pack(const unsigned char *field, unsigned char *send, KGeom
     int o3[3], n = 0;
     for (int nu = 0; nu < 4; nu++)
         if (nu != mu) o3[n++] = nu;
-    unsigned char *dst = send + g.blk_off[mu][blk];
+    unsigned char *dst = d.dst[mu][blk];
     const int total = F * CPR + (Q::F16 ? F : 0);
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
         const bool sc = e >= F * CPR;
@@ -2251,6 +2254,7 @@ __global__ void halo_pack(const unsigned char *field, unsigned char *send, KGeom
         if (!sc) *reinterpret_cast<uint4 *>(dst + (size_t)f * PREC + ch * 16) = *reinterpret_cast<const uint4 *>(rec + ch * 16);
         else *reinterpret_cast<float *>(dst + (size_t)F * PREC + (size_t)f * 4) = *reinterpret_cast<const float *>(rec + Q::VSCALE);
     }
+    signal_block(d.flag[mu][blk]);
 }
 
 // ------------------------------------------------------------------ variant table
@@ -2447,7 +2451,7 @@ cudaError_t launch_halo_t(const ApplyArgs &a, cudaStream_t s)
 }
 
 template <cd_precision P, int NV>
-cudaError_t launch_pack_t(const void *field, void *send, const KGeom &g, cudaStream_t s)
+cudaError_t launch_pack_t(const void *field, const PackDst &d, const KGeom &g, cudaStream_t s)
 {
     int4 pairs = make_int4(0, 0, 0, 0);
     int np = 0;
@@ -2456,10 +2460,10 @@ cudaError_t launch_pack_t(const void *field, void *send, const KGeom &g, cudaStr
         if ((g.split >> mu) & 1) pp[np++] = mu;
     if (np == 0) return cudaSuccess;
     const unsigned char *f = static_cast<const unsigned char *>(field);
-    unsigned char *d = static_cast<unsigned char *>(send);
+    PackDst dd = d;
     KGeom gg = g;
-    void *args[] = {&f, &d, &gg, &pairs};
-    return launch_ex((const void *)halo_pack<P, NV>, dim3(16, 2 * np), dim3(256), 0, s, false, args);
+    void *args[] = {&f, &dd, &gg, &pairs};
+    return launch_ex((const void *)halo_pack<P, NV>, dim3(kPutCtas, 2 * np), dim3(256), 0, s, false, args);
 }
 
 }  // namespace cd
@@ -2549,7 +2553,7 @@ cudaError_t launch_pack_t(const void *field, void *send, const KGeom &g, cudaStr
         }                                                                                                         \
         return dispatch_chain<P, NV, 0>(id, a, n, base, s, sms, nrb);                                             \
     }                                                                                                             \
-    cudaError_t launch_pack_##TAG(const void *f, void *d, const KGeom &g, cudaStream_t s)                         \
+    cudaError_t launch_pack_##TAG(const void *f, const PackDst &d, const KGeom &g, cudaStream_t s)                \
     {                                                                                                             \
         return launch_pack_t<P, NV>(f, d, g, s);                                                                  \
     }                                                                                                             \

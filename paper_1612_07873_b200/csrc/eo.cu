@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(288) dslash_parity(const unsigned char *__rest
 // other parity are simply not written (never read), so the plan, buffers and NCCL exchange of
 // the full operator are reused unchanged.
 template <int NV>
-__global__ void eo_pack(const unsigned char *half, unsigned char *send, KGeom g, int4 pairs, int parity)
+__global__ void eo_pack(const unsigned char *half, PackDst d, KGeom g, int4 pairs, int parity)
 {
     using Q = Cfg<CD_FP32, NV>;
     constexpr int PREC = 8 * Q::N, CPR = PREC / 16;
@@ -237,7 +237,7 @@ __global__ void eo_pack(const unsigned char *half, unsigned char *send, KGeom g,
     int o3[3], n = 0;
     for (int nu = 0; nu < 4; nu++)
         if (nu != mu) o3[n++] = nu;
-    unsigned char *dst = send + g.blk_off[mu][blk];
+    unsigned char *dst = d.dst[mu][blk];
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < F * CPR; e += gridDim.x * blockDim.x) {
         const int f = e / CPR, ch = e - f * CPR;
         int x[4];
@@ -251,6 +251,7 @@ __global__ void eo_pack(const unsigned char *half, unsigned char *send, KGeom g,
         const unsigned char *rec = half + (size_t)(encode(g, x) >> 1) * Q::VREC;
         *reinterpret_cast<uint4 *>(dst + (size_t)f * PREC + ch * 16) = *reinterpret_cast<const uint4 *>(rec + ch * 16);
     }
+    signal_block(d.flag[mu][blk]);
 }
 
 // one CTA per face site of the output parity: partial + the remote hops, then the final store
@@ -373,26 +374,28 @@ static cudaError_t eo_apply_t(const EoApply &e)
         if ((e.g.split >> mu) & 1) (&pairs.x)[np++] = mu;
     for (int mode = 0; mode < 2; mode++) {
         const unsigned char *src = mode == 0 ? vi : t;   // the half field the hops read
-        cudaError_t r = cudaEventRecord(e.ev_in, e.s);
+        PackDst pd;
+        const void *recv = nullptr;
+        cudaError_t r = e.begin(e.exchange_arg, &pd, &recv);
+        if (r == cudaSuccess) r = cudaEventRecord(e.ev_in, e.s);
         if (r == cudaSuccess) r = cudaStreamWaitEvent(e.comm_stream, e.ev_in, 0);
         if (r != cudaSuccess) return r;
         count_launch();
-        eo_pack<NV><<<dim3(16, 2 * np), 256, 0, e.comm_stream>>>(src, static_cast<unsigned char *>(e.send), e.g, pairs,
-                                                                 mode == 0 ? 0 : 1);
+        eo_pack<NV><<<dim3(kPutCtas, 2 * np), 256, 0, e.comm_stream>>>(src, pd, e.g, pairs, mode == 0 ? 0 : 1);
         if ((r = cudaGetLastError()) != cudaSuccess) return r;
-        if ((r = e.exchange(e.exchange_arg)) != cudaSuccess) return r;
+        if ((r = e.post(e.exchange_arg)) != cudaSuccess) return r;
         if ((r = cudaEventRecord(e.ev_halo, e.comm_stream)) != cudaSuccess) return r;
         r = mode == 0 ? eo_mode_launch<NV>(0, od, nullptr, vi, t, e.g, e.dagger, 1, e.scratch, e.s, false)
                       : eo_mode_launch<NV>(1, ev, vi, t, y, e.g, e.dagger, 1, e.scratch, e.s, false);
         if (r != cudaSuccess) return r;
         if ((r = cudaStreamWaitEvent(e.s, e.ev_halo, 0)) != cudaSuccess) return r;
+        if ((r = e.finish(e.exchange_arg)) != cudaSuccess) return r;
         count_launch();
+        const unsigned char *rv = static_cast<const unsigned char *>(recv);
         if (mode == 0)
-            eo_halo<NV, 0><<<e.n_face, 32 * (2 * NV / 4), 0, e.s>>>(od, static_cast<const unsigned char *>(e.recv),
-                                                                     e.face_sites, e.scratch, t, e.g, e.dagger);
+            eo_halo<NV, 0><<<e.n_face, 32 * (2 * NV / 4), 0, e.s>>>(od, rv, e.face_sites, e.scratch, t, e.g, e.dagger);
         else
-            eo_halo<NV, 1><<<e.n_face, 32 * (2 * NV / 4), 0, e.s>>>(ev, static_cast<const unsigned char *>(e.recv),
-                                                                     e.face_sites, e.scratch, y, e.g, e.dagger);
+            eo_halo<NV, 1><<<e.n_face, 32 * (2 * NV / 4), 0, e.s>>>(ev, rv, e.face_sites, e.scratch, y, e.g, e.dagger);
         if ((r = cudaGetLastError()) != cudaSuccess) return r;
     }
     return cudaSuccess;

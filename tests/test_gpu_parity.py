@@ -237,18 +237,24 @@ def test_linearity_fp32():
 
 
 # ---------------------------------------------------------------- halo path on one GPU (self exchange)
+@pytest.mark.parametrize("transport", ["copy", "nccl", "peer"])
 @pytest.mark.parametrize("mask", [0b1000, 0b1100, 0b0101, 0b1111])
 @pytest.mark.parametrize("prec", ["fp32", "fp16"])
-def test_halo_self_exchange(mask, prec):
+def test_halo_self_exchange(mask, prec, transport):
     """Route split dims through pack -> exchange -> interior + halo-term kernels with P_mu = 1
     (the +mu neighbour is this rank): results match the oracle and the pack buffer is
-    bit-exact against oracle.pack_halo."""
+    bit-exact against oracle.pack_halo.  transport "nccl": a 1-rank communicator, so the real
+    ncclGroupStart/Send/Recv/GroupEnd code runs on one GPU (self send/recv); "peer": the pack
+    kernel stores into this rank's own IPC window and the wait kernel checks the counters."""
     dims, nvec = (2, 3, 4, 3), 24
     N = 2 * nvec
     Lh = synth.links(dims, N)
     v = synth.vector(dims, N)
     ctx = cd.Context(dims, nvec)
     ctx.set_option(cd.CD_OPT_HALO_SELF_MASK, mask)
+    if transport == "peer":
+        ctx.peer_connect([ctx.peer_handle()])
+    ctx.set_transport(transport)
     L = ctx.links_upload(Lh, prec)
     fin, fout = ctx.field(prec), ctx.field(prec)
     fin.import_(v)
@@ -261,6 +267,7 @@ def test_halo_self_exchange(mask, prec):
         nb = vol(dims) * N * 4
         ref_buf = oracle.pack_halo(dims, split, raw[:nb].copy(), 4 * N, raw[nb:].copy(), 4)
     assert buf == ref_buf
+    assert ctx.halo_exchange(fin) == ref_buf   # self exchange: what arrives is what was packed
     ref = oracle.apply(dims, Lh, v)
     for var in range(len(ctx.variants(prec))):
         ctx.set_option(cd.CD_OPT_VARIANT, var)
