@@ -47,6 +47,8 @@ def _load():
             lib.oracle_apply_dagger_tau3.argtypes = [I4, ctypes.c_int, P, P, P]
             lib.oracle_apply_generated.argtypes = [I4, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_int, P, P]
             lib.oracle_apply_generated.restype = ctypes.c_int
+            lib.oracle_set_threads.argtypes = [ctypes.c_int]
+            lib.oracle_get_threads.restype = ctypes.c_int
             lib.oracle_adjoint.argtypes = [I4, ctypes.c_int, P, P, P]
             lib.oracle_dense.argtypes = [I4, ctypes.c_int, P, P]
             lib.oracle_partitioned_apply.argtypes = [I4, I4, ctypes.c_int, P, P, P]
@@ -94,6 +96,15 @@ def apply(dims, links, v):
     y = np.empty((V, N), np.complex128)
     _load().oracle_apply(_dims(dims), N, L.ctypes.data, x.ctypes.data, y.ctypes.data)
     return y
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads of the oracle's site loops (timing only)."""
+    _load().oracle_set_threads(int(n))
+
+
+def get_threads() -> int:
+    return int(_load().oracle_get_threads())
 
 
 KINDS = {"general": 0, "hermitian": 1, "ti_general": 2, "ti_hermitian": 3}

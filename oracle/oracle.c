@@ -32,8 +32,13 @@
 #include <stdlib.h>
 #include <string.h>
 #include <math.h>
+#include <omp.h>
 
 typedef double complex cplx;
+
+/* Thread count of the OpenMP loops (bench.py reports the oracle at 1 thread and at all cores). */
+void oracle_set_threads(int n) { omp_set_num_threads(n > 0 ? n : 1); }
+int oracle_get_threads(void) { return omp_get_max_threads(); }
 
 #define MAXN 128
 

@@ -2238,8 +2238,14 @@ __global__ void halo_pack(const unsigned char *field, PackDst d, KGeom g, int4 p
     for (int nu = 0; nu < 4; nu++)
         if (nu != mu) o3[n++] = nu;
     unsigned char *dst = d.dst[mu][blk];
-    const int total = F * CPR + (Q::F16 ? F : 0);
+    // fp16: F payload records, F scales, then zero padding of the block to 16 bytes (R13)
+    const int npad = Q::F16 ? ((4 - (F & 3)) & 3) : 0;
+    const int total = F * CPR + (Q::F16 ? F + npad : 0);
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        if (e >= F * CPR + F) {
+            *reinterpret_cast<float *>(dst + (size_t)F * PREC + (size_t)(e - F * CPR) * 4) = 0.0f;
+            continue;
+        }
         const bool sc = e >= F * CPR;
         const int f = sc ? e - F * CPR : e / CPR;
         const int ch = sc ? 0 : e - f * CPR;

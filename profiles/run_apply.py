@@ -17,7 +17,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import paper_1612_07873_b200 as cd  # noqa: E402
-from paper_1612_07873_b200 import perfmodel  # noqa: E402
+import perfmodel  # noqa: E402
 
 
 def setup(dims, nvec, prec):

@@ -10,7 +10,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import paper_1612_07873_b200 as cd  # noqa: E402
-from paper_1612_07873_b200 import perfmodel  # noqa: E402
+import perfmodel  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--dims", type=int, nargs=4, default=[8, 8, 8, 8])
