@@ -56,6 +56,12 @@ WORKLOADS = {
            "name": "coarse lattice 16^3x32, Nvec=24, fp16 storage (Iso64 64^3x128 blocked 4^4)"},
 }
 HEADLINE = "M5"
+_RESULT_FD = 1
+
+
+def emit(obj):
+    """Write the result line to the process's real stdout (see main())."""
+    os.write(_RESULT_FD, (json.dumps(obj) + "\n").encode())
 SEG = 400   # applies per timed segment (keeps the chained iterate finite)
 
 
@@ -188,7 +194,7 @@ def dist_setup():
     local = env_int("LOCAL_RANK", 0)
     if world > 1:
         import torch.distributed as dist
-        backend = os.environ.get("CD_BENCH_BACKEND", "nccl")
+        backend = os.environ.get("CD_BENCH_BACKEND", "gloo" if "--same-gpu" in sys.argv else "nccl")
         dist.init_process_group(backend)
     return world, rank, local
 
@@ -198,6 +204,8 @@ def dist_max(x: float, world: int, device=None) -> float:
         return x
     import torch
     import torch.distributed as dist
+    if dist.get_backend() != "nccl":
+        device = None   # gloo: host tensor
     t = torch.tensor([x], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -354,6 +362,55 @@ def measure_chain(cd, torch, pm, sampler):
             "clocks": sampler.summary(t0, t1)}
 
 
+def measure_overlap(cd, torch, pm, sampler):
+    """Overlap of the halo exchange with the interior, on one GPU: M5 with T routed through the
+    halo path (CD_OPT_HALO_SELF_MASK: the T faces are packed, exchanged with this rank itself
+    and added by the halo-term kernel, exactly the multi-rank code path) for the peer and NCCL
+    transports, against the same apply with no split and the exchange alone."""
+    w = WORKLOADS["M5"]
+    dims, nvec, prec = w["dims"], w["nvec"], w["prec"]
+    V = dims[0] * dims[1] * dims[2] * dims[3]
+    t0 = time.perf_counter()
+
+    def chained_us(ctx, L, a, b, n=20):
+        L.apply(b, a)
+        torch.cuda.synchronize()
+        return statistics.median(_events_us(torch, lambda k: [L.apply(b, a) if i % 2 == 0 else L.apply(a, b)
+                                                            for i in range(k)], n) for _ in range(3))
+    base = cd.Context(dims, nvec)
+    L = base.links_generate(prec, scale_log2=-4)
+    a, b = base.field(prec), base.field(prec)
+    a.generate()
+    us_plain = chained_us(base, L, a, b)
+    del L, a, b, base
+    out = {"workload": w["name"], "split": "T through the halo path, self exchange", "us_no_split": round(us_plain, 2)}
+    for tr in ("peer", "nccl"):
+        ctx = cd.Context(dims, nvec)
+        ctx.set_option(cd.CD_OPT_HALO_SELF_MASK, 8)
+        if tr == "peer":
+            ctx.peer_connect([ctx.peer_handle()])
+        ctx.set_transport(tr)
+        L = ctx.links_generate(prec, scale_log2=-4)
+        a, b = ctx.field(prec), ctx.field(prec)
+        a.generate()
+        us_split = chained_us(ctx, L, a, b)
+        ctx.halo_exchange(a, copy_out=False)
+        torch.cuda.synchronize()
+        us_x = statistics.median(_events_us(torch, lambda k: [ctx.halo_exchange(a, copy_out=False) for _ in range(k)], 50)
+                                 for _ in range(3))
+        pl = cd.cd_halo_plan_create(dims, nvec, (1, 1, 1, 1), 0, prec, 8)
+        out[tr] = {"us_split_apply": round(us_split, 2), "us_exchange_only": round(us_x, 2),
+                   "halo_bytes": int(pl.total_bytes), "variant": ctx.variants(prec)[ctx.chosen_variant(prec)],
+                   "exposed_us": round(us_split - us_plain, 2),
+                   "hidden_frac_of_exchange": round(max(-1.0, min(1.0, 1 - (us_split - us_plain) / us_x)), 3)
+                   if us_x > 0 else None}
+        del L, a, b, ctx
+    out["note"] = ("exposed = split apply - unsplit apply (the halo-term kernel over the face sites and any "
+                   "exchange time not hidden behind the interior); exchange only = coarse_halo_exchange")
+    out["clocks"] = sampler.summary(t0, time.perf_counter())
+    return out
+
+
 def extras(cd, torch, pm, sampler):
     """NEXT-row kernels at 8^4, Nvec 24 (informational)."""
     out = {}
@@ -430,6 +487,8 @@ def extras(cd, torch, pm, sampler):
 def run_ours(args):
     import torch
     world, rank, local = dist_setup()
+    if args.same_gpu:   # functional check of the multi-rank path on a one-GPU box (timings time-sliced)
+        local = 0
     torch.cuda.set_device(local)
     import paper_1612_07873_b200 as cd
     pm = _perfmodel()
@@ -613,6 +672,7 @@ def run_ours(args):
                             ("M4", "fp32"), ("M4", "fp16")):
             configs[f"{key}_{prec_k}"] = measure_config(cd, torch, pm, sampler, key, prec_k, peak)
         configs["M1_fp32_chain"] = measure_chain(cd, torch, pm, sampler)
+        configs["M5_fp16_self_halo_overlap"] = measure_overlap(cd, torch, pm, sampler)
         also = extras(cd, torch, pm, sampler)
     sampler.stop()
 
@@ -667,7 +727,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "also": also,
         }
-        print(json.dumps(out), flush=True)
+        emit(out)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
@@ -721,7 +781,7 @@ def run_reference(args):
                          "sample": sample},
         "e2e": {"value": round(gflops, 3), "unit": "GFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(out), flush=True)
+    emit(out)
 
 
 def main():
@@ -734,6 +794,8 @@ def main():
     ap.add_argument("--prec", choices=["fp32", "fp16"], default=None, help="override the workload's storage")
     ap.add_argument("--pgrid", default=None, help="process grid P0,P1,P2,P3 (default 1,1,1,N: T split)")
     ap.add_argument("--transport", choices=["peer", "nccl", "auto"], default="peer")
+    ap.add_argument("--same-gpu", action="store_true",
+                    help="all ranks on cuda:0 (functional check of the N > 1 path on a one-GPU box; peer transport)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-extras", action="store_true", help="skip the per-config and NEXT-row measurements")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
@@ -741,6 +803,13 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    # exactly ONE line on stdout: anything the libraries print there (e.g. NCCL's version banner
+    # when a communicator is created) is sent to stderr; the JSON line goes to the real stdout
+    sys.stdout.flush()
+    real_out = os.dup(1)
+    os.dup2(2, 1)
+    global _RESULT_FD
+    _RESULT_FD = real_out
     if args.impl == "reference":
         run_reference(args)
     else:

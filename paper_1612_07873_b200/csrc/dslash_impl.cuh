@@ -229,44 +229,58 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
         int x[4];
         decode(a.g, site, x);
         float re = 0.0f, im = 0.0f;
+        // one hop: row `row` of matrix j of stage `st` times its vector record
+        auto hop = [&](const unsigned char *st, int j) {
+            const unsigned char *mrec = st + j * Q::MREC;
+            const unsigned char *mrow = mrec + row * Q::ROWB;
+            const unsigned char *vrec = st + RC::VOFF + j * Q::VREC;
+            if constexpr (P == CD_FP32) {
+                float pr[Q::C], pi[Q::C];
+#pragma unroll
+                for (int c = 0; c < Q::C; c++) {
+                    pr[c] = 0.0f;
+                    pi[c] = 0.0f;
+                    const int q = d + Q::D * c;
+                    uint4 vq = lds128(vrec + q * 16);
+                    if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<false>(vq);
+                    cmac2(lds128(mrow + q * 16), vq, pr[c], pi[c]);
+                }
+#pragma unroll
+                for (int c = 0; c < Q::C; c++) { re += pr[c]; im += pi[c]; }
+            } else {
+                float ra = 0.f, rb = 0.f, ia = 0.f, ib = 0.f;
+#pragma unroll
+                for (int c = 0; c < Q::C; c++) {
+                    const int cc = ROT ? ((c + (r & 1)) % Q::C) : c;
+                    const int q = d + Q::D * cc;
+                    uint4 vq = lds128(vrec + q * 16);
+                    if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<true>(vq);
+                    hmac4(lds128(mrow + q * 16), vq, ra, rb, ia, ib);
+                }
+                const float sc = *reinterpret_cast<const float *>(mrec + Q::MSCALE) *
+                                 *reinterpret_cast<const float *>(vrec + Q::VSCALE);
+                re = fmaf(ra - rb, sc, re);
+                im = fmaf(ia + ib, sc, im);
+            }
+        };
+        // only face sites of a split dim have remote hops; every other site takes the
+        // straight-line path even when the context is split (the interior kernel of run_split)
+        const bool checked = a.halo && is_face<P, NV>(a.g, x);
         for (int gi = 0; gi < G; gi++) {
             if (gi > 0) mbar_wait(&full[stage], phase);
             const unsigned char *st = stages + (size_t)stage * RC::STAGE;
+            if (!checked) {
+                // straight-line stage (no per-hop branch): the compiler interleaves the MPS
+                // independent hops' loads and FMA chains -- one CTA per SM leaves few consumer
+                // warps, so this ILP is what keeps up with HBM at power-capped clocks (m9 fp16 at
+                // 16^3x32: 1.69 -> 1.55 ms, profiles/r02/ring_ilp_ab.txt).  Waiting for a whole
+                // site's stages before computing (more ILP for m1 / m3) measured slower for fp32.
 #pragma unroll
-            for (int j = 0; j < MPS; j++) {
-                const int k = gi * MPS + j;
-                if (a.halo && remote_hop(a.g, x, k)) continue;
-                const unsigned char *mrec = st + j * Q::MREC;
-                const unsigned char *mrow = mrec + row * Q::ROWB;
-                const unsigned char *vrec = st + RC::VOFF + j * Q::VREC;
-                if constexpr (P == CD_FP32) {
-                    float pr[Q::C], pi[Q::C];
+                for (int j = 0; j < MPS; j++) hop(st, j);
+            } else {
 #pragma unroll
-                    for (int c = 0; c < Q::C; c++) {
-                        pr[c] = 0.0f;
-                        pi[c] = 0.0f;
-                        const int q = d + Q::D * c;
-                        uint4 vq = lds128(vrec + q * 16);
-                        if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<false>(vq);
-                        cmac2(lds128(mrow + q * 16), vq, pr[c], pi[c]);
-                    }
-#pragma unroll
-                    for (int c = 0; c < Q::C; c++) { re += pr[c]; im += pi[c]; }
-                } else {
-                    float ra = 0.f, rb = 0.f, ia = 0.f, ib = 0.f;
-#pragma unroll
-                    for (int c = 0; c < Q::C; c++) {
-                        const int cc = ROT ? ((c + (r & 1)) % Q::C) : c;
-                        const int q = d + Q::D * cc;
-                        uint4 vq = lds128(vrec + q * 16);
-                        if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<true>(vq);
-                        hmac4(lds128(mrow + q * 16), vq, ra, rb, ia, ib);
-                    }
-                    const float sc = *reinterpret_cast<const float *>(mrec + Q::MSCALE) *
-                                     *reinterpret_cast<const float *>(vrec + Q::VSCALE);
-                    re = fmaf(ra - rb, sc, re);
-                    im = fmaf(ia + ib, sc, im);
-                }
+                for (int j = 0; j < MPS; j++)
+                    if (!remote_hop(a.g, x, gi * MPS + j)) hop(st, j);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);

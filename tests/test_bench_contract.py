@@ -42,7 +42,7 @@ def test_reference_arm_maps_no_product_library():
             "assert 'libcoarse_dslash' not in maps, 'product library mapped'; "
             "assert 'paper_1612_07873_b200' not in sys.modules; print('clean')")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, cwd=ROOT)
-    assert r.returncode == 0 and "clean" in r.stdout, r.stderr[-2000:]
+    assert r.returncode == 0 and "clean" in r.stdout + r.stderr, r.stderr[-2000:]
 
 
 @pytest.mark.gpu

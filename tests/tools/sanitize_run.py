@@ -35,6 +35,28 @@ for prec in ("fp32", "fp16"):
         for v in range(len(h.variants(prec))):
             h.set_option(cd.CD_OPT_VARIANT, v)
             Lh.apply(y, x)
+    if which in ("all", "transport"):
+        # halo self exchanges through the peer transport (pack kernel -> own IPC window, arrival
+        # wait kernel) and through a 1-rank NCCL communicator; the chunked bulk path (compressed
+        # links' link halo, multi-RHS faces) under the peer transport
+        for tr in ("peer", "nccl"):
+            h = cd.Context((2, 2, 2, 4), 24)
+            h.set_option(cd.CD_OPT_HALO_SELF_MASK, 0b1010)
+            if tr == "peer":
+                h.peer_connect([h.peer_handle()])
+            h.set_transport(tr)
+            Lh = h.links_generate(prec, kind="hermitian", scale_log2=-4)
+            x, y = h.field(prec), h.field(prec)
+            x.generate()
+            Lh.apply(y, x)
+            Lh.apply_dagger(x, y)
+            h.halo_exchange(x)
+            Ch, _ = Lh.compress_hermitian()
+            Ch.apply(y, x)
+            if prec == "fp16":
+                mx, my = h.field("fp16", nrhs=128), h.field("fp16", nrhs=128)
+                mx.generate()
+                Lh.apply_mrhs(my, mx)
     if which in ("all", "mrhs") and prec == "fp16":
         x, y = ctx.field("fp16", nrhs=128), ctx.field("fp16", nrhs=128)
         x.generate()
