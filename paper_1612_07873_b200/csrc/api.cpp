@@ -394,7 +394,7 @@ static void ctx_release(cd_context *c)
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     void *bufs[] = {c->send_buf, c->recv_buf, c->face_scratch, c->face_sites, c->interior_sites, c->mrhs_send,
-                    c->mrhs_recv, c->work, c->ysplit, c->site_cnt, c->chain_cnt, c->llbuf};
+                    c->mrhs_recv, c->work, c->ysplit, c->site_cnt, c->chain_cnt, c->llbuf, c->pack_cnt};
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
@@ -469,6 +469,8 @@ int cd_context_create(const cd_geometry *geom, int device, int nranks, int rank,
     if (e == cudaSuccess) e = cudaMalloc(&c->ysplit, sizeof(float2) * c->V * c->N);
     if (e == cudaSuccess) e = cudaMalloc(&c->site_cnt, sizeof(int) * c->V);
     if (e == cudaSuccess) e = cudaMemset(c->site_cnt, 0, sizeof(int) * c->V);
+    if (e == cudaSuccess) e = cudaMalloc(&c->pack_cnt, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(c->pack_cnt, 0, sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc(&c->chain_cnt, sizeof(unsigned) * c->V);
     if (e == cudaSuccess) e = cudaMemset(c->chain_cnt, 0, sizeof(unsigned) * c->V);
     if (e != cudaSuccess) {
@@ -478,6 +480,7 @@ int cd_context_create(const cd_geometry *geom, int device, int nranks, int rank,
     if (const char *ev = getenv("CD_TUNE")) c->tune = atoi(ev) ? 1 : 0;
     if (const char *ev = getenv("CD_VARIANT")) c->force_variant = atoi(ev);
     if (const char *ev = getenv("CD_PDL")) c->pdl = atoi(ev) ? 1 : 0;
+    if (const char *ev = getenv("CD_FUSE_SPLIT")) c->fuse_split = atoi(ev) ? 1 : 0;
     if (nranks > 1 && nccl_id) {
         std::string err;
         int r = comm_create(nccl_id, nranks, rank, &c->comm, err);
@@ -1239,6 +1242,34 @@ static int do_apply(const cd_links *l, cd_field *out, const cd_field *in, void *
     if (r != CD_OK) return r;
     if (!halo) {
         CUDA_TRY(launch_next(c, l->prec, id, a, s, c->pdl != 0), "dslash launch");
+        return CD_OK;
+    }
+    int kw = 0, wr = 0;
+    if (transport_of(c) == TR_PEER && variant_kind(l->prec, c->nvec, id, &kw, &wr) == 0 && c->fuse_split) {
+        // fused split apply: ONE persistent launch packs its face slices straight
+        // into the neighbours' windows, streams the interior sites, then the face sites with
+        // their remote records read from this rank's window after an in-kernel arrival wait
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(s, &cap);
+        if (cap != cudaStreamCaptureStatusNone)
+            return fail(CD_ERR_UNSUPPORTED, "peer-transport applies cannot be captured in a CUDA graph (per-exchange epochs)");
+        const cd_halo_plan pl = ctx_plan(c, l->prec);
+        std::string err;
+        HaloX x;
+        r = halo_begin(c, pl, &x, err);
+        if (r != CD_OK) return fail(r, err);
+        a.fused = 1;
+        a.pd = x.pd;
+        a.recv = x.recv;
+        a.wflag = reinterpret_cast<const unsigned long long *>(c->win);
+        a.wmask = x.mask;
+        a.wtarget = x.target;
+        a.wtimeout = c->peer_timeout_ns;
+        a.werr = c->err_dev;
+        a.pack_cnt = c->pack_cnt;
+        a.interior_sites = c->interior_sites;
+        a.n_interior = c->n_interior;
+        CUDA_TRY(launch_next(c, l->prec, id, a, s, false), "fused split apply");
         return CD_OK;
     }
     return run_split(

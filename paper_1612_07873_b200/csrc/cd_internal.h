@@ -123,6 +123,7 @@ struct cd_context {
     int n_interior = 0;
     void *mrhs_send = nullptr, *mrhs_recv = nullptr;   // multi-RHS halo buffers (lazy)
     size_t mrhs_cap = 0;
+    int *pack_cnt = nullptr;          // fused split apply: pack-completion counter (zero between launches)
     int *work = nullptr;              // ring kernel ticket counters (4 slots x 2 ints, zero between
                                       // launches); applies on one context must be stream-ordered
     uint32_t seq = 0;                 // dslash launch sequence number
@@ -154,6 +155,7 @@ struct cd_context {
     int tune = 1;
     int halo_self_mask = 0;
     int pdl = 1;
+    int fuse_split = 1;               // CD_FUSE_SPLIT=0: peer-transport ring applies use the unfused path
     bool applied = false;
     int num_sms = 148;
     // tuning results per (prec, dagger)
@@ -220,6 +222,21 @@ struct ApplyArgs {
     const void *lhalo;     // compressed links, multi-rank: the -mu neighbours' x_mu = L-1 forward records
     int64_t lhoff[4];      // byte offset of dim mu's records in lhalo
     long long *trace;      // LL-register chain diagnostic (CD_CHAIN_TRACE): clock64 events of CTA 0
+    // fused split apply (ring variants + peer transport): the ring kernel packs its
+    // slice of the face records straight into the neighbours' windows in its prologue (the last
+    // CTA to finish signals kPutCtas per block), takes interior sites before face sites, and its
+    // producer reads a face site's remote records from this rank's window after an in-kernel
+    // arrival wait -- one launch per apply, no halo-term kernel, no partials
+    int fused;
+    PackDst pd;                          // pack destinations + the peers' arrival counters
+    const unsigned long long *wflag;     // this rank's arrival counters [mu][blk]
+    unsigned wmask;                      // blocks to wait for (bit 2mu+blk)
+    unsigned long long wtarget;          // counter value of this exchange
+    unsigned long long wtimeout;         // ns
+    int *werr;                           // host-mapped error word (timeout)
+    int *pack_cnt;                       // CTAs done with their pack slice (last one resets it)
+    const int *interior_sites;           // site order: interior sites, then face_sites
+    int n_interior;
 };
 
 constexpr int CLUSTER_CHAIN_ID = 1000;   // apply_chain variant: whole lattice in one cluster

@@ -74,6 +74,114 @@ __device__ __forceinline__ void store_site(unsigned char *out, int site, int row
     }
 }
 
+// ------------------------------------------------------------------ fused split apply helpers
+// (ring + peer transport).  The pack: every CTA of the persistent ring stores its
+// grid-stride slice of every face block (wire format R13: payload records, fp16 scales, zero
+// padding) straight into the neighbours' windows.
+template <cd_precision P, int NV>
+__device__ __forceinline__ void fused_pack(const ApplyArgs &a)
+{
+    using Q = Cfg<P, NV>;
+    constexpr int PREC = Q::F16 ? 4 * Q::N : 8 * Q::N;
+    constexpr int CPR = PREC / 16;
+    const unsigned char *field = static_cast<const unsigned char *>(a.in);
+    const KGeom &g = a.g;
+#pragma unroll 1
+    for (int mu = 0; mu < 4; mu++) {
+        if (!((g.split >> mu) & 1)) continue;
+        const int F = g.F[mu];
+        int o3[3], n = 0;
+        for (int nu = 0; nu < 4; nu++)
+            if (nu != mu) o3[n++] = nu;
+        const int npad = Q::F16 ? ((4 - (F & 3)) & 3) : 0;
+        const int total = F * CPR + (Q::F16 ? F + npad : 0);
+#pragma unroll 1
+        for (int blk = 0; blk < 2; blk++) {
+            unsigned char *dst = blk ? a.pd.dst[mu][1] : a.pd.dst[mu][0];
+            for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+                if (e >= F * CPR + F) {
+                    *reinterpret_cast<float *>(dst + (size_t)F * PREC + (size_t)(e - F * CPR) * 4) = 0.0f;
+                    continue;
+                }
+                const bool sc = e >= F * CPR;
+                const int f = sc ? e - F * CPR : e / CPR;
+                const int ch = sc ? 0 : e - f * CPR;
+                int x[4];
+                int t = f;
+                x[o3[0]] = t % g.L[o3[0]];
+                t /= g.L[o3[0]];
+                x[o3[1]] = t % g.L[o3[1]];
+                x[o3[2]] = t / g.L[o3[1]];
+                x[mu] = blk == 0 ? g.L[mu] - 1 : 0;
+                const unsigned char *rec = field + (size_t)encode(g, x) * Q::VREC;
+                if (!sc)
+                    *reinterpret_cast<uint4 *>(dst + (size_t)f * PREC + ch * 16) =
+                        *reinterpret_cast<const uint4 *>(rec + ch * 16);
+                else
+                    *reinterpret_cast<float *>(dst + (size_t)F * PREC + (size_t)f * 4) =
+                        *reinterpret_cast<const float *>(rec + Q::VSCALE);
+            }
+        }
+    }
+}
+
+// All CTAs: pack, then the last CTA to finish releases kPutCtas per block to the receivers (the
+// same total a separate halo_pack launch signals, so ranks may mix fused and unfused applies).
+template <cd_precision P, int NV>
+__device__ __forceinline__ void fused_pack_and_signal(const ApplyArgs &a)
+{
+    fused_pack<P, NV>(a);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        if (atomicAdd(a.pack_cnt, 1) == (int)gridDim.x - 1) {
+            __threadfence_system();
+#pragma unroll 1
+            for (int b = 0; b < 8; b++) {
+                if (!((a.wmask >> b) & 1)) continue;
+                unsigned long long *fl = a.pd.flag[b >> 1][b & 1];
+                asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(fl), "l"((unsigned long long)kPutCtas)
+                             : "memory");
+            }
+            atomicExch(a.pack_cnt, 0);   // the next fused launch is stream-ordered after this one
+        }
+    }
+}
+
+// Producer side: spin (acquire, system scope) until this exchange's halo has landed in this
+// rank's window; on timeout raise the context's error word and go on (never hang).
+__device__ __forceinline__ void wait_arrival(const ApplyArgs &a)
+{
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+#pragma unroll 1
+    for (int b = 0; b < 8; b++) {
+        if (!((a.wmask >> b) & 1)) continue;
+        for (;;) {
+            unsigned long long v;
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a.wflag + b) : "memory");
+            if (v >= a.wtarget) break;
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > a.wtimeout) {
+                atomicExch_system(a.werr, 1);
+                break;
+            }
+            __nanosleep(32);
+        }
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");   // generic-proxy arrival -> TMA reads
+}
+
+// Face index of x in the block of dim mu (the other three coordinates, lowest fastest).
+__device__ __forceinline__ int face_index(const KGeom &g, const int x[4], int mu)
+{
+    return mu == 0 ? (x[3] * g.L[2] + x[2]) * g.L[1] + x[1]
+         : mu == 1 ? (x[3] * g.L[2] + x[2]) * g.L[0] + x[0]
+         : mu == 2 ? (x[3] * g.L[1] + x[1]) * g.L[0] + x[0]
+                   : (x[2] * g.L[1] + x[1]) * g.L[0] + x[0];
+}
+
 // ------------------------------------------------------------------ RING variant
 // MPS = link matrices per ring stage.  A site's nine matrices are contiguous in HBM
 // ([site][k], k = 0..8), so a stage holding MPS of them is ONE bulk copy (plus the MPS vector
@@ -125,6 +233,10 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
     }
     __syncthreads();
     pdl_trigger();
+    if (a.fused) {   // split apply, peer transport: the halo pack + transfer is this kernel's prologue
+        pdl_wait();
+        fused_pack_and_signal<P, NV>(a);
+    }
 
     if (warp == RC::NCW) {
         // ===== producer: one elected lane takes sites from a global ticket counter (dynamic
@@ -139,7 +251,14 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
             // that kernel's tail (PDL).  Its vector records (`in`, written by the previous
             // kernel) follow the wait.  Later sites come from the ticket counter (site =
             // gridDim.x + ticket).
-            const bool pre = (G <= S) && (int)blockIdx.x < V;
+            const bool pre = !a.fused && (G <= S) && (int)blockIdx.x < V;
+            // fused split apply: tickets walk the interior sites first, the face sites last (their
+            // remote records have long landed by then)
+            auto order = [&](int t) -> int {
+                if (!a.fused) return t;
+                return t < a.n_interior ? __ldg(a.interior_sites + t) : __ldg(a.face_sites + (t - a.n_interior));
+            };
+            bool landed = false;
             if (pre) {
                 const int site = (int)blockIdx.x;
                 int x[4];
@@ -174,31 +293,52 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
             // first site goes through the loop like any other
             bool first = !pre && (int)blockIdx.x < V;
             for (;;) {
-                const int site = first ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(tickets, 1);
+                const int tk = first ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(tickets, 1);
                 first = false;
-                if (site >= V) {   // sentinel stage: tells the consumers to stop
+                if (tk >= V) {   // sentinel stage: tells the consumers to stop
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&full[stage], 4);
                     st_async_u32(&siteq[stage], 0xFFFFFFFFu, &full[stage]);
                     break;
                 }
+                const int site = order(tk);
                 int x[4];
                 decode(a.g, site, x);
                 const unsigned char *lsite = links + (size_t)site * 9 * Q::MREC;
+                constexpr int PREC = Q::F16 ? 4 * Q::N : 8 * Q::N;   // wire payload record
                 for (int gi = 0; gi < G; gi++) {
-                    int nvc = 0;
+                    uint32_t vbytes = 0;
 #pragma unroll
-                    for (int j = 0; j < MPS; j++) nvc += !(a.halo && remote_hop(a.g, x, gi * MPS + j));
+                    for (int j = 0; j < MPS; j++) {
+                        const bool rem = a.halo && remote_hop(a.g, x, gi * MPS + j);
+                        vbytes += !rem ? Q::VREC : (a.fused ? PREC + (Q::F16 ? 4 : 0) : 0);
+                    }
                     mbar_wait(&empty[stage], phase ^ 1);
                     unsigned char *st = stages + (size_t)stage * RC::STAGE;
                     // the site id travels like the data: an async store counted on the same barrier
-                    mbar_arrive_expect_tx(&full[stage], MPS * Q::MREC + nvc * Q::VREC + (gi == 0 ? 4 : 0));
+                    mbar_arrive_expect_tx(&full[stage], MPS * Q::MREC + vbytes + (gi == 0 ? 4 : 0));
                     if (gi == 0) st_async_u32(&siteq[stage], (uint32_t)site, &full[stage]);
                     bulk_g2s(st, lsite + (size_t)gi * MPS * Q::MREC, MPS * Q::MREC, &full[stage]);
 #pragma unroll
                     for (int j = 0; j < MPS; j++) {
                         const int k = gi * MPS + j;
-                        if (a.halo && remote_hop(a.g, x, k)) continue;
+                        if (a.halo && remote_hop(a.g, x, k)) {
+                            if (!a.fused) continue;   // unfused: the halo-term kernel adds this hop
+                            if (!landed) {
+                                wait_arrival(a);
+                                landed = true;
+                            }
+                            // a +mu hop reads block B (the +mu rank's x_mu = 0 face), a -mu hop block A
+                            const int mu = k >> 1, blk = (k & 1) ? 0 : 1;
+                            const int f = face_index(a.g, x, mu);
+                            const unsigned char *rb = static_cast<const unsigned char *>(a.recv) + a.g.blk_off[mu][blk];
+                            bulk_g2s(st + RC::VOFF + j * Q::VREC, rb + (size_t)f * PREC, PREC, &full[stage]);
+                            if constexpr (Q::F16)
+                                st_async_u32(st + RC::VOFF + j * Q::VREC + Q::VSCALE,
+                                             __ldcg(reinterpret_cast<const unsigned *>(rb + (size_t)sel4(a.g.F, mu) * PREC) + f),
+                                             &full[stage]);
+                            continue;
+                        }
                         bulk_g2s(st + RC::VOFF + j * Q::VREC, in + (size_t)neighbour(a.g, x, site, k) * Q::VREC,
                                  Q::VREC, &full[stage]);
                     }
@@ -265,7 +405,7 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
         };
         // only face sites of a split dim have remote hops; every other site takes the
         // straight-line path even when the context is split (the interior kernel of run_split)
-        const bool checked = a.halo && is_face<P, NV>(a.g, x);
+        const bool checked = a.halo && !a.fused && is_face<P, NV>(a.g, x);
         for (int gi = 0; gi < G; gi++) {
             if (gi > 0) mbar_wait(&full[stage], phase);
             const unsigned char *st = stages + (size_t)stage * RC::STAGE;
@@ -292,7 +432,7 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
             im += shfl_xor(im, m);
         }
         const bool owner = (d == 0);
-        if (a.halo && is_face<P, NV>(a.g, x)) {
+        if (checked) {
             if (owner) a.scratch[(size_t)site * Q::N + row] = make_float2(re, im);
         } else {
             const float sg = (a.dagger && row >= NV) ? -1.0f : 1.0f;
