@@ -1267,8 +1267,7 @@ static int do_apply(const cd_links *l, cd_field *out, const cd_field *in, void *
         a.wtimeout = c->peer_timeout_ns;
         a.werr = c->err_dev;
         a.pack_cnt = c->pack_cnt;
-        a.interior_sites = c->interior_sites;
-        a.n_interior = c->n_interior;
+        a.rot = (c->kg.split == 8) ? (int)(c->V / c->local[3]) : 0;
         CUDA_TRY(launch_next(c, l->prec, id, a, s, false), "fused split apply");
         return CD_OK;
     }

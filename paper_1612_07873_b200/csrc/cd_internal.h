@@ -235,8 +235,7 @@ struct ApplyArgs {
     unsigned long long wtimeout;         // ns
     int *werr;                           // host-mapped error word (timeout)
     int *pack_cnt;                       // CTAs done with their pack slice (last one resets it)
-    const int *interior_sites;           // site order: interior sites, then face_sites
-    int n_interior;
+    int rot;                             // ticket -> site rotation (T-only split: V / L3 puts the T faces last)
 };
 
 constexpr int CLUSTER_CHAIN_ID = 1000;   // apply_chain variant: whole lattice in one cluster

@@ -74,6 +74,75 @@ __device__ __forceinline__ void store_site(unsigned char *out, int site, int row
     }
 }
 
+// ------------------------------------------------------------------ halo pack (shared by the
+// halo_pack kernel and the fused ring prologue).  Face index f of block (mu, blk) -> site index
+// (the other three coordinates lexicographic, lowest fastest; x_mu = L-1 for block A, 0 for B).
+__device__ __forceinline__ int face_site(const KGeom &g, int mu, int blk, int f)
+{
+    const int xm = blk == 0 ? sel4(g.L, mu) - 1 : 0;
+    if (mu == 0) return f * g.L[0] + xm;
+    if (mu == 1) {
+        const int x0 = f % g.L[0], r = f / g.L[0];
+        return (r * g.L[1] + xm) * g.L[0] + x0;
+    }
+    if (mu == 2) {
+        const int A = g.L[0] * g.L[1];
+        const int lo = f % A, hi = f / A;
+        return (hi * g.L[2] + xm) * A + lo;
+    }
+    return f + xm * g.L[0] * g.L[1] * g.L[2];
+}
+
+// PackDst entries without dynamic indexing of a kernel parameter (which would force a stack copy)
+__device__ __forceinline__ unsigned char *pd_dst(const PackDst &d, int mu, int blk)
+{
+    unsigned char *a0 = blk ? d.dst[0][1] : d.dst[0][0], *a1 = blk ? d.dst[1][1] : d.dst[1][0];
+    unsigned char *a2 = blk ? d.dst[2][1] : d.dst[2][0], *a3 = blk ? d.dst[3][1] : d.dst[3][0];
+    return mu == 0 ? a0 : (mu == 1 ? a1 : (mu == 2 ? a2 : a3));
+}
+__device__ __forceinline__ unsigned long long *pd_flag(const PackDst &d, int mu, int blk)
+{
+    unsigned long long *a0 = blk ? d.flag[0][1] : d.flag[0][0], *a1 = blk ? d.flag[1][1] : d.flag[1][0];
+    unsigned long long *a2 = blk ? d.flag[2][1] : d.flag[2][0], *a3 = blk ? d.flag[3][1] : d.flag[3][0];
+    return mu == 0 ? a0 : (mu == 1 ? a1 : (mu == 2 ? a2 : a3));
+}
+
+// Elements [start, ...) with step `stride` of block (mu, blk): payload 16-B chunks (four loads in
+// flight per thread before their stores), then (fp16) the F scales and the zero padding to 16 B.
+template <cd_precision P, int NV>
+__device__ __forceinline__ void pack_block(const unsigned char *field, unsigned char *dst, const KGeom &g, int mu,
+                                           int blk, int start, int stride)
+{
+    using Q = Cfg<P, NV>;
+    constexpr int PREC = Q::F16 ? 4 * Q::N : 8 * Q::N;
+    constexpr int CPR = PREC / 16;
+    const int F = sel4(g.F, mu);
+    const int np = F * CPR;
+    for (int e0 = start; e0 < np; e0 += 4 * stride) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int e = e0 + u * stride;
+            if (e < np) {
+                const int f = e / CPR, ch = e - f * CPR;
+                v[u] = *reinterpret_cast<const uint4 *>(field + (size_t)face_site(g, mu, blk, f) * Q::VREC + ch * 16);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int e = e0 + u * stride;
+            if (e < np) *reinterpret_cast<uint4 *>(dst + (size_t)e * 16) = v[u];   // record f, chunk ch
+        }
+    }
+    if constexpr (Q::F16) {
+        const int npad = (4 - (F & 3)) & 3;
+        for (int e = start; e < F + npad; e += stride)
+            *reinterpret_cast<float *>(dst + (size_t)F * PREC + (size_t)e * 4) =
+                e < F ? *reinterpret_cast<const float *>(field + (size_t)face_site(g, mu, blk, e) * Q::VREC + Q::VSCALE)
+                      : 0.0f;
+    }
+}
+
 // ------------------------------------------------------------------ fused split apply helpers
 // (ring + peer transport).  The pack: every CTA of the persistent ring stores its
 // grid-stride slice of every face block (wire format R13: payload records, fp16 scales, zero
@@ -81,47 +150,13 @@ __device__ __forceinline__ void store_site(unsigned char *out, int site, int row
 template <cd_precision P, int NV>
 __device__ __forceinline__ void fused_pack(const ApplyArgs &a)
 {
-    using Q = Cfg<P, NV>;
-    constexpr int PREC = Q::F16 ? 4 * Q::N : 8 * Q::N;
-    constexpr int CPR = PREC / 16;
     const unsigned char *field = static_cast<const unsigned char *>(a.in);
-    const KGeom &g = a.g;
+    const int start = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
 #pragma unroll 1
     for (int mu = 0; mu < 4; mu++) {
-        if (!((g.split >> mu) & 1)) continue;
-        const int F = g.F[mu];
-        int o3[3], n = 0;
-        for (int nu = 0; nu < 4; nu++)
-            if (nu != mu) o3[n++] = nu;
-        const int npad = Q::F16 ? ((4 - (F & 3)) & 3) : 0;
-        const int total = F * CPR + (Q::F16 ? F + npad : 0);
-#pragma unroll 1
-        for (int blk = 0; blk < 2; blk++) {
-            unsigned char *dst = blk ? a.pd.dst[mu][1] : a.pd.dst[mu][0];
-            for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-                if (e >= F * CPR + F) {
-                    *reinterpret_cast<float *>(dst + (size_t)F * PREC + (size_t)(e - F * CPR) * 4) = 0.0f;
-                    continue;
-                }
-                const bool sc = e >= F * CPR;
-                const int f = sc ? e - F * CPR : e / CPR;
-                const int ch = sc ? 0 : e - f * CPR;
-                int x[4];
-                int t = f;
-                x[o3[0]] = t % g.L[o3[0]];
-                t /= g.L[o3[0]];
-                x[o3[1]] = t % g.L[o3[1]];
-                x[o3[2]] = t / g.L[o3[1]];
-                x[mu] = blk == 0 ? g.L[mu] - 1 : 0;
-                const unsigned char *rec = field + (size_t)encode(g, x) * Q::VREC;
-                if (!sc)
-                    *reinterpret_cast<uint4 *>(dst + (size_t)f * PREC + ch * 16) =
-                        *reinterpret_cast<const uint4 *>(rec + ch * 16);
-                else
-                    *reinterpret_cast<float *>(dst + (size_t)F * PREC + (size_t)f * 4) =
-                        *reinterpret_cast<const float *>(rec + Q::VSCALE);
-            }
-        }
+        if (!((a.g.split >> mu) & 1)) continue;
+        pack_block<P, NV>(field, pd_dst(a.pd, mu, 0), a.g, mu, 0, start, stride);
+        pack_block<P, NV>(field, pd_dst(a.pd, mu, 1), a.g, mu, 1, start, stride);
     }
 }
 
@@ -139,7 +174,7 @@ __device__ __forceinline__ void fused_pack_and_signal(const ApplyArgs &a)
 #pragma unroll 1
             for (int b = 0; b < 8; b++) {
                 if (!((a.wmask >> b) & 1)) continue;
-                unsigned long long *fl = a.pd.flag[b >> 1][b & 1];
+                unsigned long long *fl = pd_flag(a.pd, b >> 1, b & 1);
                 asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(fl), "l"((unsigned long long)kPutCtas)
                              : "memory");
             }
@@ -252,11 +287,14 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
             // kernel) follow the wait.  Later sites come from the ticket counter (site =
             // gridDim.x + ticket).
             const bool pre = !a.fused && (G <= S) && (int)blockIdx.x < V;
-            // fused split apply: tickets walk the interior sites first, the face sites last (their
-            // remote records have long landed by then)
+            // fused split apply: tickets walk the sites rotated by a.rot, which for a T-only split puts
+            // both T faces last (their remote records have long landed by then); otherwise a face
+            // site met early just waits for the arrival (once per CTA).  Arithmetic on purpose: the
+            // producer thread's per-site latency is the ring's critical path (an index-list load per
+            // site measured +22 % at 16^3x32).
             auto order = [&](int t) -> int {
-                if (!a.fused) return t;
-                return t < a.n_interior ? __ldg(a.interior_sites + t) : __ldg(a.face_sites + (t - a.n_interior));
+                const int u = t + a.rot;
+                return u < V ? u : u - V;
             };
             bool landed = false;
             if (pre) {
@@ -306,6 +344,26 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
                 decode(a.g, site, x);
                 const unsigned char *lsite = links + (size_t)site * 9 * Q::MREC;
                 constexpr int PREC = Q::F16 ? 4 * Q::N : 8 * Q::N;   // wire payload record
+                // fused split apply, fp16 face site: the remote records' scales are loaded before the
+                // stage wait and the link copy, so their latency hides behind both
+                unsigned rsc[9];   // set (and read) for the remote hops of a fused face site only
+                if constexpr (Q::F16) {
+                    if (a.fused && is_face<P, NV>(a.g, x)) {
+                        if (!landed) {
+                            wait_arrival(a);
+                            landed = true;
+                        }
+#pragma unroll
+                        for (int k = 0; k < 8; k++)
+                            if (remote_hop(a.g, x, k)) {
+                                const int mu = k >> 1, blk = (k & 1) ? 0 : 1;
+                                const unsigned char *rb = static_cast<const unsigned char *>(a.recv) + a.g.blk_off[mu][blk];
+                                rsc[k] = __ldcg(reinterpret_cast<const unsigned *>(rb + (size_t)sel4(a.g.F, mu) * PREC) +
+                                                face_index(a.g, x, mu));
+                            }
+                    }
+                }
+#pragma unroll
                 for (int gi = 0; gi < G; gi++) {
                     uint32_t vbytes = 0;
 #pragma unroll
@@ -333,10 +391,7 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
                             const int f = face_index(a.g, x, mu);
                             const unsigned char *rb = static_cast<const unsigned char *>(a.recv) + a.g.blk_off[mu][blk];
                             bulk_g2s(st + RC::VOFF + j * Q::VREC, rb + (size_t)f * PREC, PREC, &full[stage]);
-                            if constexpr (Q::F16)
-                                st_async_u32(st + RC::VOFF + j * Q::VREC + Q::VSCALE,
-                                             __ldcg(reinterpret_cast<const unsigned *>(rb + (size_t)sel4(a.g.F, mu) * PREC) + f),
-                                             &full[stage]);
+                            if constexpr (Q::F16) st_async_u32(st + RC::VOFF + j * Q::VREC + Q::VSCALE, rsc[k], &full[stage]);
                             continue;
                         }
                         bulk_g2s(st + RC::VOFF + j * Q::VREC, in + (size_t)neighbour(a.g, x, site, k) * Q::VREC,
@@ -2382,39 +2437,11 @@ __global__ void __launch_bounds__(32 * (2 * NV / Cfg<P, NV>::R)) dslash_halo(App
 template <cd_precision P, int NV>
 __global__ void halo_pack(const unsigned char *field, PackDst d, KGeom g, int4 pairs)
 {
-    using Q = Cfg<P, NV>;
-    constexpr int PREC = Q::F16 ? 4 * Q::N : 8 * Q::N;
-    constexpr int CPR = PREC / 16;
-    const int pid = (&pairs.x)[blockIdx.y >> 1];
-    const int mu = pid, blk = blockIdx.y & 1;
-    const int F = g.F[mu];
-    int o3[3], n = 0;
-    for (int nu = 0; nu < 4; nu++)
-        if (nu != mu) o3[n++] = nu;
-    unsigned char *dst = d.dst[mu][blk];
-    // fp16: F payload records, F scales, then zero padding of the block to 16 bytes (R13)
-    const int npad = Q::F16 ? ((4 - (F & 3)) & 3) : 0;
-    const int total = F * CPR + (Q::F16 ? F + npad : 0);
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-        if (e >= F * CPR + F) {
-            *reinterpret_cast<float *>(dst + (size_t)F * PREC + (size_t)(e - F * CPR) * 4) = 0.0f;
-            continue;
-        }
-        const bool sc = e >= F * CPR;
-        const int f = sc ? e - F * CPR : e / CPR;
-        const int ch = sc ? 0 : e - f * CPR;
-        int x[4];
-        int t = f;
-        x[o3[0]] = t % g.L[o3[0]];
-        t /= g.L[o3[0]];
-        x[o3[1]] = t % g.L[o3[1]];
-        x[o3[2]] = t / g.L[o3[1]];
-        x[mu] = blk == 0 ? g.L[mu] - 1 : 0;
-        const unsigned char *rec = field + (size_t)encode(g, x) * Q::VREC;
-        if (!sc) *reinterpret_cast<uint4 *>(dst + (size_t)f * PREC + ch * 16) = *reinterpret_cast<const uint4 *>(rec + ch * 16);
-        else *reinterpret_cast<float *>(dst + (size_t)F * PREC + (size_t)f * 4) = *reinterpret_cast<const float *>(rec + Q::VSCALE);
-    }
-    signal_block(d.flag[mu][blk]);
+    const int pi = blockIdx.y >> 1, blk = blockIdx.y & 1;
+    const int mu = pi == 0 ? pairs.x : (pi == 1 ? pairs.y : (pi == 2 ? pairs.z : pairs.w));
+    pack_block<P, NV>(field, pd_dst(d, mu, blk), g, mu, blk, blockIdx.x * blockDim.x + threadIdx.x,
+                      gridDim.x * blockDim.x);
+    signal_block(pd_flag(d, mu, blk));
 }
 
 // ------------------------------------------------------------------ variant table

@@ -1017,3 +1017,44 @@ def test_entry_points_restore_current_device():
     L.apply(b, a)
     b.export()
     assert torch.cuda.current_device() == dev0
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp16"])
+@pytest.mark.parametrize("mask", [0b1000, 0b1100])
+def test_fused_split_apply_is_one_launch(prec, mask):
+    """Ring variants on the peer transport run a split apply as ONE launch (pack in the prologue,
+    face sites read their remote records from the window in the same kernel, DESIGN.md §7);
+    CD_FUSE_SPLIT-independent result == the oracle; the unfused path launches pack + interior +
+    wait + halo-term kernels."""
+    dims, nvec = (4, 4, 4, 6), 24
+    N = 2 * nvec
+    Lh = synth.links(dims, N, scale_log2=-4)
+    v = synth.vector(dims, N)
+    ref = oracle.apply(dims, Lh, v)
+    ctx = cd.Context(dims, nvec)
+    ctx.set_option(cd.CD_OPT_HALO_SELF_MASK, mask)
+    ctx.peer_connect([ctx.peer_handle()])
+    ctx.set_transport("peer")
+    names = ctx.variants(prec)
+    rings = [i for i, n in enumerate(names) if n.startswith("ring")]
+    L = ctx.links_upload(Lh, prec)
+    fin, fout = ctx.field(prec), ctx.field(prec)
+    fin.import_(v)
+    for var in rings:
+        ctx.set_option(cd.CD_OPT_VARIANT, var)
+        L.apply(fout, fin)
+        torch.cuda.synchronize()
+        n0 = cd.cd_launch_count()
+        L.apply(fout, fin)
+        torch.cuda.synchronize()
+        assert cd.cd_launch_count() - n0 == 1, names[var]
+        assert rel_l2(fout.export(), ref) <= TOL[prec], names[var]
+    fg = [i for i, n in enumerate(names) if n.startswith("fg")][0]
+    ctx.set_option(cd.CD_OPT_VARIANT, fg)
+    L.apply(fout, fin)
+    torch.cuda.synchronize()
+    n0 = cd.cd_launch_count()
+    L.apply(fout, fin)
+    torch.cuda.synchronize()
+    assert cd.cd_launch_count() - n0 == 4    # pack, interior, arrival wait, halo term
+    assert rel_l2(fout.export(), ref) <= TOL[prec]
