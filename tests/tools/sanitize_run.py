@@ -48,8 +48,11 @@ for prec in ("fp32", "fp16"):
             Lh = h.links_generate(prec, kind="hermitian", scale_log2=-4)
             x, y = h.field(prec), h.field(prec)
             x.generate()
-            Lh.apply(y, x)
-            Lh.apply_dagger(x, y)
+            for v in (-1, 0):   # heuristic choice, and the ring (fused split apply on the peer transport)
+                h.set_option(cd.CD_OPT_VARIANT, v)
+                Lh.apply(y, x)
+                Lh.apply_dagger(x, y)
+            h.set_option(cd.CD_OPT_VARIANT, -1)
             h.halo_exchange(x)
             Ch, _ = Lh.compress_hermitian()
             Ch.apply(y, x)
