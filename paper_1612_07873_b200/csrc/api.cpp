@@ -1100,7 +1100,51 @@ static int resolve_variant(cd_context *c, cd_precision p, int dag, const ApplyAr
             // variant that overlaps its ramp with the previous launch's tail is timed as it will
             // run in a chain of applies); < 0 if it cannot run here
             const bool tpdl = c->pdl != 0;
+            // L2-resident lattices (the latency regime): eager back-to-back launches would time the
+            // host's launch rate, so r applies are captured in a CUDA graph on a private stream
+            // (PDL edges kept) and the graph's replay is timed -- how a solver runs them
+            const double lbytes = (double)c->V * 9.0 * (p == CD_FP32 ? 8.0 : 4.0) * c->N * c->N;
+            const bool graph_tune = lbytes <= 64e6 && !getenv("CD_TUNE_EAGER");
+            cudaStream_t ts = nullptr;
+            cudaEvent_t evs = nullptr;
+            if (graph_tune) {
+                if (cudaStreamCreateWithFlags(&ts, cudaStreamNonBlocking) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&evs, cudaEventDisableTiming) != cudaSuccess)
+                    return fail(CD_ERR_CUDA, "tuner stream");
+                cudaEventRecord(evs, s);
+                cudaStreamWaitEvent(ts, evs, 0);   // trials after the caller's prior work
+            }
+            auto timeit_graph = [&](int id2, int r) -> float {
+                cudaGraph_t gr = nullptr;
+                cudaGraphExec_t ge = nullptr;
+                if (cudaStreamBeginCapture(ts, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+                    cudaGetLastError();
+                    return -1.f;
+                }
+                cudaError_t e = cudaSuccess;
+                for (int rr = 0; rr < r && e == cudaSuccess; rr++) e = launch_next(c, p, id2, a, ts, tpdl);
+                cudaError_t e2 = cudaStreamEndCapture(ts, &gr);
+                if (e == cudaSuccess) e = e2;
+                if (e == cudaSuccess) e = cudaGraphInstantiate(&ge, gr, 0);
+                float ms = -1.f;
+                if (e == cudaSuccess) e = cudaGraphLaunch(ge, ts);   // warm-up
+                if (e == cudaSuccess) e = cudaEventRecord(e0, ts);
+                if (e == cudaSuccess) e = cudaGraphLaunch(ge, ts);
+                if (e == cudaSuccess) e = cudaEventRecord(e1, ts);
+                if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+                if (e == cudaSuccess) {
+                    cudaEventElapsedTime(&ms, e0, e1);
+                    ms /= r;
+                } else {
+                    cudaGetLastError();
+                    ms = -1.f;
+                }
+                if (ge) cudaGraphExecDestroy(ge);
+                if (gr) cudaGraphDestroy(gr);
+                return ms;
+            };
             auto timeit = [&](int id2, int r) -> float {
+                if (graph_tune) return timeit_graph(id2, std::max(r, 50));
                 cudaError_t e = cudaSuccess;
                 for (int w = 0; w < 2 && e == cudaSuccess; w++) e = launch_next(c, p, id2, a, s, tpdl);
                 if (e != cudaSuccess) {
@@ -1173,6 +1217,11 @@ static int resolve_variant(cd_context *c, cd_precision p, int dag, const ApplyAr
                     }
             cudaEventDestroy(e0);
             cudaEventDestroy(e1);
+            if (ts) {
+                cudaStreamSynchronize(ts);
+                cudaStreamDestroy(ts);
+            }
+            if (evs) cudaEventDestroy(evs);
             tune_file_store(ks, v, variant_name(p, c->nvec, v), best * 1000.f);
         }
     }
@@ -1268,7 +1317,7 @@ static int do_apply(const cd_links *l, cd_field *out, const cd_field *in, void *
         a.werr = c->err_dev;
         a.pack_cnt = c->pack_cnt;
         a.rot = (c->kg.split == 8) ? (int)(c->V / c->local[3]) : 0;
-        CUDA_TRY(launch_next(c, l->prec, id, a, s, false), "fused split apply");
+        CUDA_TRY(launch_next(c, l->prec, id, a, s, c->pdl != 0), "fused split apply");
         return CD_OK;
     }
     return run_split(

@@ -148,10 +148,9 @@ __device__ __forceinline__ void pack_block(const unsigned char *field, unsigned 
 // grid-stride slice of every face block (wire format R13: payload records, fp16 scales, zero
 // padding) straight into the neighbours' windows.
 template <cd_precision P, int NV>
-__device__ __forceinline__ void fused_pack(const ApplyArgs &a)
+__device__ __forceinline__ void fused_pack(const ApplyArgs &a, int start, int stride)
 {
     const unsigned char *field = static_cast<const unsigned char *>(a.in);
-    const int start = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
 #pragma unroll 1
     for (int mu = 0; mu < 4; mu++) {
         if (!((a.g.split >> mu) & 1)) continue;
@@ -160,14 +159,17 @@ __device__ __forceinline__ void fused_pack(const ApplyArgs &a)
     }
 }
 
-// All CTAs: pack, then the last CTA to finish releases kPutCtas per block to the receivers (the
+// Run by lanes 1..31 of the producer warp while lane 0 streams the stencil's records: this CTA's
+// slice of the pack, then the last CTA to finish releases kPutCtas per block to the receivers (the
 // same total a separate halo_pack launch signals, so ranks may mix fused and unfused applies).
 template <cd_precision P, int NV>
-__device__ __forceinline__ void fused_pack_and_signal(const ApplyArgs &a)
+__device__ __forceinline__ void fused_pack_lanes(const ApplyArgs &a, int lane)
 {
-    fused_pack<P, NV>(a);
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    constexpr unsigned kMask = 0xfffffffeu;   // lanes 1..31
+    pdl_wait();   // `in` is written by the previous kernel in the stream
+    fused_pack<P, NV>(a, (int)blockIdx.x * 31 + (lane - 1), (int)gridDim.x * 31);
+    __syncwarp(kMask);
+    if (lane == 1) {
         __threadfence_system();
         if (atomicAdd(a.pack_cnt, 1) == (int)gridDim.x - 1) {
             __threadfence_system();
@@ -178,7 +180,7 @@ __device__ __forceinline__ void fused_pack_and_signal(const ApplyArgs &a)
                 asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(fl), "l"((unsigned long long)kPutCtas)
                              : "memory");
             }
-            atomicExch(a.pack_cnt, 0);   // the next fused launch is stream-ordered after this one
+            atomicExch(a.pack_cnt, 0);   // the next fused launch packs only after this kernel completed
         }
     }
 }
@@ -268,11 +270,13 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
     }
     __syncthreads();
     pdl_trigger();
-    if (a.fused) {   // split apply, peer transport: the halo pack + transfer is this kernel's prologue
-        pdl_wait();
-        fused_pack_and_signal<P, NV>(a);
-    }
 
+    if (warp == RC::NCW && lane != 0) {
+        // fused split apply: the other 31 lanes of the producer warp pack this CTA's slice of the
+        // face records straight into the neighbours' windows, overlapped with the stencil
+        if (a.fused) fused_pack_lanes<P, NV>(a, lane);
+        return;
+    }
     if (warp == RC::NCW) {
         // ===== producer: one elected lane takes sites from a global ticket counter (dynamic
         // load balance across SMs) and streams their records into the ring.  Ticket slot
@@ -286,7 +290,6 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
             // that kernel's tail (PDL).  Its vector records (`in`, written by the previous
             // kernel) follow the wait.  Later sites come from the ticket counter (site =
             // gridDim.x + ticket).
-            const bool pre = !a.fused && (G <= S) && (int)blockIdx.x < V;
             // fused split apply: tickets walk the sites rotated by a.rot, which for a T-only split puts
             // both T faces last (their remote records have long landed by then); otherwise a face
             // site met early just waits for the arrival (once per CTA).  Arithmetic on purpose: the
@@ -296,11 +299,16 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
                 const int u = t + a.rot;
                 return u < V ? u : u - V;
             };
+            // The first site's links are prefetched before griddepcontrol.wait (PDL); a fused apply
+            // does so too unless that site is a face site (its remote records need the arrival wait)
+            const int site0 = order((int)blockIdx.x);
+            int x0[4];
+            decode(a.g, site0 < V ? site0 : 0, x0);
+            const bool pre = (G <= S) && (int)blockIdx.x < V && !(a.fused && is_face<P, NV>(a.g, x0));
             bool landed = false;
             if (pre) {
-                const int site = (int)blockIdx.x;
-                int x[4];
-                decode(a.g, site, x);
+                const int site = site0;
+                int x[4] = {x0[0], x0[1], x0[2], x0[3]};
                 const unsigned char *lsite = links + (size_t)site * 9 * Q::MREC;
                 for (int gi = 0; gi < G; gi++) {
                     int nvc = 0;
@@ -344,32 +352,13 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
                 decode(a.g, site, x);
                 const unsigned char *lsite = links + (size_t)site * 9 * Q::MREC;
                 constexpr int PREC = Q::F16 ? 4 * Q::N : 8 * Q::N;   // wire payload record
-                // fused split apply, fp16 face site: the remote records' scales are loaded before the
-                // stage wait and the link copy, so their latency hides behind both
-                unsigned rsc[9];   // set (and read) for the remote hops of a fused face site only
-                if constexpr (Q::F16) {
-                    if (a.fused && is_face<P, NV>(a.g, x)) {
-                        if (!landed) {
-                            wait_arrival(a);
-                            landed = true;
-                        }
-#pragma unroll
-                        for (int k = 0; k < 8; k++)
-                            if (remote_hop(a.g, x, k)) {
-                                const int mu = k >> 1, blk = (k & 1) ? 0 : 1;
-                                const unsigned char *rb = static_cast<const unsigned char *>(a.recv) + a.g.blk_off[mu][blk];
-                                rsc[k] = __ldcg(reinterpret_cast<const unsigned *>(rb + (size_t)sel4(a.g.F, mu) * PREC) +
-                                                face_index(a.g, x, mu));
-                            }
-                    }
-                }
 #pragma unroll
                 for (int gi = 0; gi < G; gi++) {
                     uint32_t vbytes = 0;
 #pragma unroll
                     for (int j = 0; j < MPS; j++) {
                         const bool rem = a.halo && remote_hop(a.g, x, gi * MPS + j);
-                        vbytes += !rem ? Q::VREC : (a.fused ? PREC + (Q::F16 ? 4 : 0) : 0);
+                        vbytes += !rem ? Q::VREC : (a.fused ? PREC + (Q::F16 ? 16 : 0) : 0);
                     }
                     mbar_wait(&empty[stage], phase ^ 1);
                     unsigned char *st = stages + (size_t)stage * RC::STAGE;
@@ -391,7 +380,12 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
                             const int f = face_index(a.g, x, mu);
                             const unsigned char *rb = static_cast<const unsigned char *>(a.recv) + a.g.blk_off[mu][blk];
                             bulk_g2s(st + RC::VOFF + j * Q::VREC, rb + (size_t)f * PREC, PREC, &full[stage]);
-                            if constexpr (Q::F16) st_async_u32(st + RC::VOFF + j * Q::VREC + Q::VSCALE, rsc[k], &full[stage]);
+                            // fp16: the 16-B aligned quad of wire scales holding this record's scale lands in
+                            // the record's scale slot (+ its 12 pad bytes); the consumer picks 4 * (f & 3) --
+                            // no dependent load on the producer thread (its latency is the ring's critical path)
+                            if constexpr (Q::F16)
+                                bulk_g2s(st + RC::VOFF + j * Q::VREC + Q::VSCALE,
+                                         rb + (size_t)sel4(a.g.F, mu) * PREC + (size_t)(f & ~3) * 4, 16, &full[stage]);
                             continue;
                         }
                         bulk_g2s(st + RC::VOFF + j * Q::VREC, in + (size_t)neighbour(a.g, x, site, k) * Q::VREC,
@@ -425,7 +419,18 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
         decode(a.g, site, x);
         float re = 0.0f, im = 0.0f;
         // one hop: row `row` of matrix j of stage `st` times its vector record
-        auto hop = [&](const unsigned char *st, int j) {
+        // fused split apply, fp16: a remote record's scale sits at 4 * (f & 3) in its scale slot
+        int sofs[9];
+#pragma unroll
+        for (int k = 0; k < 9; k++) sofs[k] = 0;
+        if constexpr (Q::F16) {
+            if (a.fused && is_face<P, NV>(a.g, x)) {
+#pragma unroll
+                for (int k = 0; k < 8; k++)
+                    if (remote_hop(a.g, x, k)) sofs[k] = 4 * (face_index(a.g, x, k >> 1) & 3);
+            }
+        }
+        auto hop = [&](const unsigned char *st, int j, int so) {
             const unsigned char *mrec = st + j * Q::MREC;
             const unsigned char *mrow = mrec + row * Q::ROWB;
             const unsigned char *vrec = st + RC::VOFF + j * Q::VREC;
@@ -453,7 +458,7 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
                     hmac4(lds128(mrow + q * 16), vq, ra, rb, ia, ib);
                 }
                 const float sc = *reinterpret_cast<const float *>(mrec + Q::MSCALE) *
-                                 *reinterpret_cast<const float *>(vrec + Q::VSCALE);
+                                 *reinterpret_cast<const float *>(vrec + Q::VSCALE + so);
                 re = fmaf(ra - rb, sc, re);
                 im = fmaf(ia + ib, sc, im);
             }
@@ -461,6 +466,7 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
         // only face sites of a split dim have remote hops; every other site takes the
         // straight-line path even when the context is split (the interior kernel of run_split)
         const bool checked = a.halo && !a.fused && is_face<P, NV>(a.g, x);
+#pragma unroll
         for (int gi = 0; gi < G; gi++) {
             if (gi > 0) mbar_wait(&full[stage], phase);
             const unsigned char *st = stages + (size_t)stage * RC::STAGE;
@@ -471,11 +477,11 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
                 // 16^3x32: 1.69 -> 1.55 ms, profiles/r02/ring_ilp_ab.txt).  Waiting for a whole
                 // site's stages before computing (more ILP for m1 / m3) measured slower for fp32.
 #pragma unroll
-                for (int j = 0; j < MPS; j++) hop(st, j);
+                for (int j = 0; j < MPS; j++) hop(st, j, sofs[gi * MPS + j]);
             } else {
 #pragma unroll
                 for (int j = 0; j < MPS; j++)
-                    if (!remote_hop(a.g, x, gi * MPS + j)) hop(st, j);
+                    if (!remote_hop(a.g, x, gi * MPS + j)) hop(st, j, 0);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
