@@ -258,11 +258,12 @@ def _rate(pm, nvec, prec, V, us, peak):
 
 
 def measure_config(cd, torch, pm, sampler, key, prec, peak):
-    """Hot and cold time of one coarse_dslash_apply for a BASELINE config.
-    hot: K chained applies (v -> y -> v), captured in one CUDA graph for the L2-resident sizes
-    (so launch gaps count, PDL edges kept), replayed R times, t = median / K.  cold: the same
-    K applies, each behind an L2 flush (256 MB written = 2 x L2), minus K flushes alone, both as
-    CUDA graphs (a single few-microsecond apply is below the event timer's resolution)."""
+    """Hot time of one coarse_dslash_apply for a BASELINE config: K chained
+    applies (v -> y -> v), captured in one CUDA graph for the L2-resident sizes (so launch gaps
+    count, PDL edges kept), replayed R times, t = median / K.  Returns (record, state); the cold
+    time is measured later by measure_cold(state) -- after every hot measurement, because an L2
+    flush leaves later L2-resident replays slower for the rest of the process
+    (profiles/m2_factors.py: 4^4 fp32 graph 5.42 -> 6.79 us per apply after one 256 MB flush)."""
     w = WORKLOADS[key]
     dims, nvec = w["dims"], w["nvec"]
     V = dims[0] * dims[1] * dims[2] * dims[3]
@@ -271,8 +272,6 @@ def measure_config(cd, torch, pm, sampler, key, prec, peak):
     a, b = ctx.field(prec), ctx.field(prec)
     a.generate()
     L.apply(b, a)   # autotune (excluded)
-    flush = 256 << 20
-    ctx.flush_l2(flush)   # allocates the flush buffer outside capture
     torch.cuda.synchronize()
     small = V <= 256
     K = {16: 400, 256: 200}.get(V, 20)
@@ -300,8 +299,30 @@ def measure_config(cd, torch, pm, sampler, key, prec, peak):
             for _ in range(R):
                 a.generate(stream=s)
                 hot.append(_events_us(torch, chained, K, s))
-        t1 = time.perf_counter()
-        KC = 40 if small else 10
+    t1 = time.perf_counter()
+    variant = ctx.variants(prec)[ctx.chosen_variant(prec)]
+    rec = {"workload": w["name"], "baseline_config": w["cfg"], "dims": list(dims), "nvec": nvec, "prec": prec,
+           "sites": V, "op": "coarse_dslash_apply", "variant": variant,
+           "hot": dict(_rate(pm, nvec, prec, V, statistics.median(hot), peak),
+                       protocol=(f"CUDA graph of {K} chained applies, median of {R} replays / {K}" if small else
+                                 f"{K} chained applies, median of {R} windows"),
+                       regime="L2-resident (effective rate under the BASELINE byte formula)" if small
+                       else "HBM streaming (inputs > L2)"),
+           "clocks": sampler.summary(t0, t1),
+           "ncu_traffic": ncu_traffic(f"{key}_{prec}", variant)}
+    return rec, (ctx, L, a, b, s, small, nvec, prec, V)
+
+
+def measure_cold(cd, torch, pm, sampler, rec, state, peak):
+    """cold: K applies, each behind an L2 flush (256 MB written = 2 x L2), minus K flushes alone,
+    both as CUDA graphs (a single few-microsecond apply is below the event timer's resolution)."""
+    ctx, L, a, b, s, small, nvec, prec, V = state
+    flush = 256 << 20
+    ctx.flush_l2(flush)   # allocates the flush buffer outside capture
+    torch.cuda.synchronize()
+    KC = 40 if small else 10
+    t0 = time.perf_counter()
+    with torch.cuda.stream(s):
         gf, gfa = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
         with torch.cuda.graph(gf, stream=s):
             for _ in range(KC):
@@ -314,20 +335,11 @@ def measure_config(cd, torch, pm, sampler, key, prec, peak):
         for _ in range(5):
             tf.append(_events_us(torch, lambda n: gf.replay(), 1, s))
             tfa.append(_events_us(torch, lambda n: gfa.replay(), 1, s))
-    t2 = time.perf_counter()
     cold_us = (statistics.median(tfa) - statistics.median(tf)) / KC
-    variant = ctx.variants(prec)[ctx.chosen_variant(prec)]
-    return {"workload": w["name"], "baseline_config": w["cfg"], "dims": list(dims), "nvec": nvec, "prec": prec,
-            "sites": V, "op": "coarse_dslash_apply", "variant": variant,
-            "hot": dict(_rate(pm, nvec, prec, V, statistics.median(hot), peak),
-                        protocol=(f"CUDA graph of {K} chained applies, median of {R} replays / {K}" if small else
-                                  f"{K} chained applies, median of {R} windows"),
-                        regime="L2-resident (effective rate under the BASELINE byte formula)" if small
-                        else "HBM streaming (inputs > L2)"),
-            "cold": dict(_rate(pm, nvec, prec, V, cold_us, peak),
-                         protocol=f"graph of {KC} x (256 MB L2 flush + apply) minus graph of {KC} flushes, / {KC}"),
-            "clocks": sampler.summary(t0, t2),
-            "ncu_traffic": ncu_traffic(f"{key}_{prec}", variant)}
+    rec["cold"] = dict(_rate(pm, nvec, prec, V, cold_us, peak),
+                       protocol=f"graph of {KC} x (256 MB L2 flush + apply) minus graph of {KC} flushes, / {KC}")
+    rec["clocks_cold"] = sampler.summary(t0, time.perf_counter())
+    return rec
 
 
 def measure_chain(cd, torch, pm, sampler):
@@ -806,9 +818,13 @@ def run_configs_only():
     sampler.start()
     time.sleep(1.0)   # idle: the latency-bound 2^4 chain first, at an unthrottled clock (reported)
     configs = {"M1_fp32_chain": measure_chain(cd, torch, pm, sampler)}
+    states = {}
     for key, prec_k in (("M1", "fp32"), ("M2", "fp32"), ("M2", "fp16"), ("M3", "fp32"), ("M3", "fp16"),
                         ("M4", "fp32"), ("M4", "fp16")):
-        configs[f"{key}_{prec_k}"] = measure_config(cd, torch, pm, sampler, key, prec_k, peak)
+        configs[f"{key}_{prec_k}"], states[f"{key}_{prec_k}"] = measure_config(cd, torch, pm, sampler, key, prec_k, peak)
+    for name, st in states.items():   # every cold (flushed) measurement after all the hot ones
+        measure_cold(cd, torch, pm, sampler, configs[name], st, peak)
+    del states
     configs["M5_fp16_self_halo_overlap"] = measure_overlap(cd, torch, pm, sampler)
     also = extras(cd, torch, pm, sampler)
     sampler.stop()
