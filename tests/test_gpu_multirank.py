@@ -270,7 +270,34 @@ def check_fullsize(rank, world, cfg, cd, oracle, synth, dev):
     return res
 
 
-CHECKS = {"operator": check_operator, "fullsize": check_fullsize}
+def check_timeout(rank, world, cfg, cd, oracle, synth, dev):
+    """A rank that stops calling the collective applies must not hang its neighbour: rank 1
+    connects and then never applies; rank 0's apply waits for rank 1's halo, times out after
+    CD_OPT_PEER_TIMEOUT_MS, and the NEXT call on its context reports CD_ERR_COMM."""
+    dims, nvec = cfg["dims"], cfg["nvec"]
+    ctx = _make_ctx(cd, cfg, rank, world, dev)
+    L = ctx.links_generate("fp32", scale_log2=-4)
+    a, b = ctx.field("fp32"), ctx.field("fp32")
+    a.generate()
+    out = {}
+    if rank == 0:
+        ctx.set_option(cd.CD_OPT_PEER_TIMEOUT_MS, 300)
+        t0 = time.time()
+        L.apply(b, a)
+        torch.cuda.synchronize()
+        out["waited_s"] = round(time.time() - t0, 3)
+        try:
+            L.apply(b, a)
+            out["code"] = 0
+        except cd.CDError as e:
+            out["code"] = e.code
+        assert out["code"] == cd.CD_ERR_COMM, out
+        assert out["waited_s"] < 30, out
+    dist.barrier()
+    return out
+
+
+CHECKS = {"operator": check_operator, "fullsize": check_fullsize, "timeout": check_timeout}
 
 
 def _worker(rank, world, port, cfg, q):
@@ -365,3 +392,10 @@ def test_multirank_fullsize_whole_field(world, dims, pgrid, nvec, prec, transpor
     cfg = {"check": "fullsize", "dims": dims, "pgrid": pgrid, "nvec": nvec, "precs": [prec], "transport": transport}
     res = _run(world, cfg, timeout=1500)
     print(world, dims, pgrid, transport, res[0])
+
+
+def test_peer_timeout_reports_comm_error():
+    cfg = {"check": "timeout", "dims": (4, 4, 4, 4), "pgrid": (1, 1, 1, 2), "nvec": 24, "precs": ["fp32"],
+           "transport": "peer"}
+    res = _run(2, cfg, timeout=300)
+    print(res[0])

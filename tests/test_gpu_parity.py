@@ -1020,13 +1020,15 @@ def test_entry_points_restore_current_device():
 
 
 @pytest.mark.parametrize("prec", ["fp32", "fp16"])
-@pytest.mark.parametrize("mask", [0b1000, 0b1100])
-def test_fused_split_apply_is_one_launch(prec, mask):
+@pytest.mark.parametrize("mask,dims", [(0b1000, (4, 4, 4, 6)), (0b1100, (4, 4, 4, 6)), (0b1000, (4, 3, 4, 1)),
+                                       (0b1001, (2, 4, 3, 2)), (0b1111, (3, 2, 2, 3))])
+def test_fused_split_apply_is_one_launch(prec, mask, dims):
     """Ring variants on the peer transport run a split apply as ONE launch (pack in the prologue,
     face sites read their remote records from the window in the same kernel, DESIGN.md §7);
     CD_FUSE_SPLIT-independent result == the oracle; the unfused path launches pack + interior +
-    wait + halo-term kernels."""
-    dims, nvec = (4, 4, 4, 6), 24
+    wait + halo-term kernels.  Includes local extent 1 (both hops of every site remote) and 2
+    (x+mu == x-mu)."""
+    nvec = 24
     N = 2 * nvec
     Lh = synth.links(dims, N, scale_log2=-4)
     v = synth.vector(dims, N)
