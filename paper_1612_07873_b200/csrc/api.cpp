@@ -108,6 +108,15 @@ cudaError_t launch_chain(cd_precision p, int id, const ApplyArgs &a, int n, unsi
                 launch_chain_f32_32(id, a, n, base, s, sms, nrb), launch_chain_f16_24(id, a, n, base, s, sms, nrb),
                 launch_chain_f16_32(id, a, n, base, s, sms, nrb));
 }
+cudaError_t launch_ringh_f32_24(const ApplyArgs &, cudaStream_t, bool, int, int);
+cudaError_t launch_ringh_f32_32(const ApplyArgs &, cudaStream_t, bool, int, int);
+cudaError_t launch_ringh_f16_24(const ApplyArgs &, cudaStream_t, bool, int, int);
+cudaError_t launch_ringh_f16_32(const ApplyArgs &, cudaStream_t, bool, int, int);
+cudaError_t launch_ringh(cd_precision p, const ApplyArgs &a, cudaStream_t s, bool pdl, int sms, int mps)
+{
+    return PICK(p, a.nvec, launch_ringh_f32_24(a, s, pdl, sms, mps), launch_ringh_f32_32(a, s, pdl, sms, mps),
+                launch_ringh_f16_24(a, s, pdl, sms, mps), launch_ringh_f16_32(a, s, pdl, sms, mps));
+}
 cudaError_t launch_fgh_f32_24(const ApplyArgs &, cudaStream_t, bool);
 cudaError_t launch_fgh_f32_32(const ApplyArgs &, cudaStream_t, bool);
 cudaError_t launch_fgh_f16_24(const ApplyArgs &, cudaStream_t, bool);
@@ -1266,6 +1275,16 @@ static int do_apply(const cd_links *l, cd_field *out, const cd_field *in, void *
         a.site_cnt = c->site_cnt;
         if (!halo) {
             a.g = c->kg;
+            // large lattices: the persistent TMA ring reading backward links transposed (HBM
+            // carries 5 matrices per site); small ones: the fine-grained fgh kernel
+            static const int comp_ring = getenv("CD_COMP_RING") ? atoi(getenv("CD_COMP_RING")) : 1;
+            if (comp_ring && c->V >= 4 * c->num_sms) {
+                a.work = c->work;
+                a.seq = c->seq++;
+                const int mps = (l->prec == CD_FP16 && c->nvec == 24) ? 9 : 3;
+                CUDA_TRY(launch_ringh(l->prec, a, s, c->pdl != 0, c->num_sms, mps), "compressed ring launch");
+                return CD_OK;
+            }
             CUDA_TRY(launch_fgh(l->prec, a, s, c->pdl != 0), "compressed dslash launch");
             return CD_OK;
         }

@@ -502,6 +502,179 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
     }
 }
 
+// ------------------------------------------------------------------ RING variant, compressed links
+// tau3-hermiticity-compressed links: a site stores X and its four forward links
+// ([site][5]); the backward hop k = 2mu+1 of x uses L_{2mu+1}(x) = tau3 L_{2mu}(x - mu)^H tau3, i.e.
+// the -mu neighbour's forward record read transposed.  The persistent TMA ring of dslash_ring with
+// one bulk copy per matrix: HBM carries 5 matrices per site (the neighbours' forward records come
+// back from L2: with tickets in site order they were streamed a few hundred sites earlier), the
+// consumers read a backward matrix by columns.  Unsplit contexts (a split one uses dslash_fgh).
+template <cd_precision P, int NV, int MPS>
+__global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ringh(ApplyArgs a, int slot)
+{
+    using Q = Cfg<P, NV>;
+    using RC = RingCfg<P, NV, MPS>;
+    constexpr int S = RC::S;
+    static_assert(S >= 2, "ring needs at least two stages");
+    constexpr int G = 9 / MPS;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem);
+    uint64_t *empty = full + RC::MAXS;
+    float *red = reinterpret_cast<float *>(smem + 16 * RC::MAXS);
+    int *siteq = reinterpret_cast<int *>(smem + 16 * RC::MAXS + 256);
+    unsigned char *stages = smem + RC::HDR;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned char *comp = static_cast<const unsigned char *>(a.links);
+    const unsigned char *in = static_cast<const unsigned char *>(a.in);
+    unsigned char *out = static_cast<unsigned char *>(a.out);
+    const int V = a.g.V;
+    int *tickets = a.work + 2 * slot;
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < S; st++) {
+            mbar_init(&full[st], 1);
+            mbar_init(&empty[st], RC::NCW);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    pdl_trigger();
+    if (warp == RC::NCW) {
+        if (lane == 0) {
+            pdl_wait();
+            int stage = 0;
+            uint32_t phase = 0;
+            bool first = (int)blockIdx.x < V;
+            for (;;) {
+                const int site = first ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(tickets, 1);
+                first = false;
+                if (site >= V) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], 4);
+                    st_async_u32(&siteq[stage], 0xFFFFFFFFu, &full[stage]);
+                    break;
+                }
+                int x[4];
+                decode(a.g, site, x);
+#pragma unroll
+                for (int gi = 0; gi < G; gi++) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    unsigned char *st = stages + (size_t)stage * RC::STAGE;
+                    mbar_arrive_expect_tx(&full[stage], MPS * (Q::MREC + Q::VREC) + (gi == 0 ? 4 : 0));
+                    if (gi == 0) st_async_u32(&siteq[stage], (uint32_t)site, &full[stage]);
+#pragma unroll
+                    for (int j = 0; j < MPS; j++) {
+                        const int k = gi * MPS + j;
+                        const int nb = neighbour(a.g, x, site, k);
+                        // X: record 0 of x; forward 2mu: record 1+mu of x; backward 2mu+1: record 1+mu of x-mu
+                        const int msite = (k == 8 || !(k & 1)) ? site : nb;
+                        const int crec = (k == 8) ? 0 : 1 + (k >> 1);
+                        bulk_g2s(st + j * Q::MREC, comp + ((size_t)msite * 5 + crec) * Q::MREC, Q::MREC, &full[stage]);
+                        bulk_g2s(st + RC::VOFF + j * Q::VREC, in + (size_t)nb * Q::VREC, Q::VREC, &full[stage]);
+                    }
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+            }
+            if (atomicAdd(tickets + 1, 1) == (int)gridDim.x - 1) {
+                tickets[0] = 0;
+                tickets[1] = 0;
+                __threadfence();
+            }
+        }
+        return;
+    }
+    pdl_wait();
+    const int r = lane / Q::D, d = lane % Q::D;
+    const int row = warp * Q::R + r;
+    const float srow = row >= NV ? -1.0f : 1.0f;   // s_i of the backward hops
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int it = 0;; ++it) {
+        mbar_wait(&full[stage], phase);
+        const int site = *reinterpret_cast<volatile int *>(&siteq[stage]);
+        if (site < 0) break;
+        float re = 0.0f, im = 0.0f;
+#pragma unroll
+        for (int gi = 0; gi < G; gi++) {
+            if (gi > 0) mbar_wait(&full[stage], phase);
+            const unsigned char *st = stages + (size_t)stage * RC::STAGE;
+#pragma unroll
+            for (int j = 0; j < MPS; j++) {
+                const int k = gi * MPS + j;
+                const bool bwd = (k != 8) && (k & 1);
+                const unsigned char *mrec = st + j * Q::MREC;
+                const unsigned char *vrec = st + RC::VOFF + j * Q::VREC;
+                if constexpr (P == CD_FP32) {
+                    float hr = 0.0f, hi = 0.0f;
+#pragma unroll
+                    for (int c = 0; c < Q::C; c++) {
+                        const int q = d + Q::D * c;
+                        uint4 vq = lds128(vrec + q * 16);
+                        if (!bwd) {
+                            if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<false>(vq);
+                            cmac2(lds128(mrec + row * Q::ROWB + q * 16), vq, hr, hi);
+                        } else {
+                            // s_j tau3-hermiticity sign, times the dagger's tau3: flip iff j >= NV && !dagger
+                            if (!a.dagger && q * Q::CPC >= NV) vq = neg_chunk<false>(vq);
+                            const float *vf = reinterpret_cast<const float *>(&vq);
+#pragma unroll
+                            for (int t = 0; t < Q::CPC; t++) {   // conj(M[j][row]) v_j
+                                const int jj = q * Q::CPC + t;
+                                const float2 m = *reinterpret_cast<const float2 *>(mrec + jj * Q::ROWB + row * 8);
+                                hr = fmaf(m.x, vf[2 * t], hr);
+                                hr = fmaf(m.y, vf[2 * t + 1], hr);
+                                hi = fmaf(m.x, vf[2 * t + 1], hi);
+                                hi = fmaf(-m.y, vf[2 * t], hi);
+                            }
+                        }
+                    }
+                    if (bwd) {
+                        hr *= srow;
+                        hi *= srow;
+                    }
+                    re += hr;
+                    im += hi;
+                } else {
+                    float ra = 0.f, rb = 0.f, ia = 0.f, ib = 0.f;
+#pragma unroll
+                    for (int c = 0; c < Q::C; c++) {
+                        const int q = d + Q::D * c;
+                        uint4 vq = lds128(vrec + q * 16);
+                        if (!bwd) {
+                            if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<true>(vq);
+                            hmac4(lds128(mrec + row * Q::ROWB + q * 16), vq, ra, rb, ia, ib);
+                        } else {
+                            if (!a.dagger && q * Q::CPC >= NV) vq = neg_chunk<true>(vq);
+                            const uint32_t *vw = &vq.x;
+#pragma unroll
+                            for (int t = 0; t < Q::CPC; t++) {
+                                const int jj = q * Q::CPC + t;
+                                hmac1(*reinterpret_cast<const uint32_t *>(mrec + jj * Q::ROWB + row * 4), vw[t], ra, rb,
+                                      ia, ib);
+                            }
+                        }
+                    }
+                    const float sc = *reinterpret_cast<const float *>(mrec + Q::MSCALE) *
+                                     *reinterpret_cast<const float *>(vrec + Q::VSCALE) * (bwd ? srow : 1.0f);
+                    // forward: (ra - rb, ia + ib); backward (conjugated matrix): (ra + rb, ia - ib)
+                    re = fmaf(bwd ? ra + rb : ra - rb, sc, re);
+                    im = fmaf(bwd ? ia - ib : ia + ib, sc, im);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+#pragma unroll
+        for (int m = Q::D / 2; m >= 1; m >>= 1) {
+            re += shfl_xor(re, m);
+            im += shfl_xor(im, m);
+        }
+        const bool owner = (d == 0);
+        const float sg = (a.dagger && row >= NV) ? -1.0f : 1.0f;
+        store_site<P, NV>(out, site, row, owner, sg * re, sg * im, red + 32 * (it & 1), 32 * RC::NCW, 1);
+    }
+}
+
 // ------------------------------------------------------------------ FG variant
 template <cd_precision P, int NV, int KW, int WR>
 struct FgCfg {
@@ -2554,6 +2727,40 @@ cudaError_t launch_ring(const ApplyArgs &a, cudaStream_t s, bool pdl, int num_sm
     return cudaLaunchKernelExC(&cfg, (const void *)dslash_ring<P, NV, MPS>, args);
 }
 
+template <cd_precision P, int NV, int MPS>
+cudaError_t launch_ringh(const ApplyArgs &a, cudaStream_t s, bool pdl, int num_sms)
+{
+    using RC = RingCfg<P, NV, MPS>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e =
+            cudaFuncSetAttribute(dslash_ringh<P, NV, MPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, RC::SMEM);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    int grid = a.g.V < num_sms ? a.g.V : num_sms;
+    grid = (grid + 1) & ~1;   // 2-CTA clusters: st.async (the site-id handoff)
+    ApplyArgs aa = a;
+    int slot = a.seq & (RC::SLOTS - 1);
+    void *args[] = {&aa, &slot};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(RC::THREADS);
+    cfg.dynamicSmemBytes = RC::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = 2;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    count_launch();
+    return cudaLaunchKernelExC(&cfg, (const void *)dslash_ringh<P, NV, MPS>, args);
+}
+
 template <cd_precision P, int NV, int KW, int WR>
 cudaError_t launch_fg(const ApplyArgs &a, cudaStream_t s, bool pdl)
 {
@@ -2669,6 +2876,14 @@ cudaError_t launch_pack_t(const void *field, const PackDst &d, const KGeom &g, c
         return dispatch_variant<P, NV, 0>(id, a, s, pdl, sms);                                                    \
     }                                                                                                             \
     cudaError_t launch_halo_##TAG(const ApplyArgs &a, cudaStream_t s) { return launch_halo_t<P, NV>(a, s); }      \
+    cudaError_t launch_ringh_##TAG(const ApplyArgs &a, cudaStream_t s, bool pdl, int sms, int mps)                \
+    {                                                                                                             \
+        if (mps == 9) {                                                                                           \
+            if constexpr (RingCfg<P, NV, 9>::S >= 2) return launch_ringh<P, NV, 9>(a, s, pdl, sms);                \
+            else return cudaErrorNotSupported;                                                                    \
+        }                                                                                                         \
+        return launch_ringh<P, NV, 3>(a, s, pdl, sms);                                                            \
+    }                                                                                                             \
     cudaError_t launch_fgh_##TAG(const ApplyArgs &a, cudaStream_t s, bool pdl)                                    \
     {                                                                                                             \
         ApplyArgs aa = a;                                                                                         \

@@ -83,6 +83,12 @@ for prec in ("fp32", "fp16"):
         ca.generate()
         Cc.apply(cb, ca)
         Cc.apply_dagger(ca, cb)
+        rc = cd.Context((8, 8, 4, 5), 24)   # V >= 4 x SMs: the compressed TMA ring (dslash_ringh)
+        Cr, _ = rc.links_generate(prec, kind="hermitian", scale_log2=-4).compress_hermitian()
+        ra, rb = rc.field(prec), rc.field(prec)
+        ra.generate()
+        Cr.apply(rb, ra)
+        Cr.apply_dagger(ra, rb)
     if which in ("all", "eo") and prec == "fp32":
         E = L.prepare_eo()
         xe, ye = ctx.field("fp32", parity=0), ctx.field("fp32", parity=0)
