@@ -1275,13 +1275,17 @@ static int do_apply(const cd_links *l, cd_field *out, const cd_field *in, void *
         a.site_cnt = c->site_cnt;
         if (!halo) {
             a.g = c->kg;
-            // large lattices: the persistent TMA ring reading backward links transposed (HBM
-            // carries 5 matrices per site); small ones: the fine-grained fgh kernel
-            static const int comp_ring = getenv("CD_COMP_RING") ? atoi(getenv("CD_COMP_RING")) : 1;
-            if (comp_ring && c->V >= 4 * c->num_sms) {
+            // fp16 on large lattices: the persistent TMA ring reading backward links transposed (HBM
+            // carries 5 matrices per site): 1.7x the fine-grained fgh16 kernel and 3-5 % faster than
+            // the full 9-matrix apply; fp32 (and small lattices): the fine-grained fgh kernel, which
+            // beats the ring there (81.6 vs 103.6 us at 8^4, profiles/r02/compressed_ring.txt)
+            static const int comp_ring = getenv("CD_COMP_RING") ? atoi(getenv("CD_COMP_RING")) : -1;
+            const bool use_ring = comp_ring > 0 || (comp_ring < 0 && l->prec == CD_FP16);
+            if (use_ring && c->V >= 4 * c->num_sms) {
                 a.work = c->work;
                 a.seq = c->seq++;
-                const int mps = (l->prec == CD_FP16 && c->nvec == 24) ? 9 : 3;
+                static const int mps_env = getenv("CD_COMP_MPS") ? atoi(getenv("CD_COMP_MPS")) : 3;
+                const int mps = (mps_env == 9 && l->prec == CD_FP16 && c->nvec == 24) ? 9 : 3;
                 CUDA_TRY(launch_ringh(l->prec, a, s, c->pdl != 0, c->num_sms, mps), "compressed ring launch");
                 return CD_OK;
             }

@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; s++) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], RC::NCW);
+            mbar_init(&empty[s], 32 * RC::NCW);   // every consumer thread releases (see below)
         }
         fence_mbar_init();
     }
@@ -483,8 +483,12 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
                 for (int j = 0; j < MPS; j++)
                     if (!remote_hop(a.g, x, gi * MPS + j)) hop(st, j, 0);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
+            // release the stage: every consumer thread arrives after its own reads returned (the
+            // accumulators depend on every load) -- no reliance on __syncwarp ordering the other
+            // lanes' reads before one elected arrive, so compute-sanitizer racecheck can verify
+            // the reuse of a stage (round 2; the elected-lane form was flagged)
+            asm volatile("" : "+f"(re), "+f"(im)::"memory");
+            mbar_arrive(&empty[stage]);
             if (++stage == S) { stage = 0; phase ^= 1; }
         }
 #pragma unroll
@@ -532,7 +536,7 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ringh(
     if (threadIdx.x == 0) {
         for (int st = 0; st < S; st++) {
             mbar_init(&full[st], 1);
-            mbar_init(&empty[st], RC::NCW);
+            mbar_init(&empty[st], 32 * RC::NCW);
         }
         fence_mbar_init();
     }
@@ -660,8 +664,10 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ringh(
                     im = fmaf(bwd ? ia - ib : ia + ib, sc, im);
                 }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
+            // the stage's shared-memory reads must have returned before it is released: pin the
+            // accumulators (which depend on every load) ahead of the arrive
+            asm volatile("" : "+f"(re), "+f"(im)::"memory");
+            mbar_arrive(&empty[stage]);   // every consumer thread (see dslash_ring)
             if (++stage == S) { stage = 0; phase ^= 1; }
         }
 #pragma unroll

@@ -1064,7 +1064,7 @@ def test_fused_split_apply_is_one_launch(prec, mask, dims):
 
 @pytest.mark.parametrize("prec", ["fp32", "fp16"])
 @pytest.mark.parametrize("dims,nvec", [((8, 8, 4, 5), 24), ((6, 5, 4, 6), 32), ((3, 8, 5, 6), 24)])
-def test_compressed_ring_matches_fine_grained(prec, dims, nvec):
+def test_compressed_ring_matches_fine_grained(prec, dims, nvec, monkeypatch):
     """Large lattices (V >= 4 x SMs) run compressed links on the persistent TMA ring
     (dslash_ringh: backward links read transposed from the neighbours' forward records);
     apply and dagger == the oracle on tau3-hermitian links and == the fine-grained compressed

@@ -12,7 +12,7 @@ SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitize
 
 
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
-@pytest.mark.parametrize("which", ["apply", "chain", "halo", "transport", "mrhs", "compressed", "eo", "transfer"])
+@pytest.mark.parametrize("which", ["apply", "ring", "chain", "halo", "transport", "mrhs", "compressed", "eo", "transfer"])
 def test_sanitizer(tool, which):
     if not os.path.exists(SAN):
         pytest.skip("compute-sanitizer not available")

@@ -60,7 +60,24 @@ for prec in ("fp32", "fp16"):
                 mx, my = h.field("fp16", nrhs=128), h.field("fp16", nrhs=128)
                 mx.generate()
                 Lh.apply_mrhs(my, mx)
+    if which in ("all", "ring"):
+        # every persistent ring variant with several sites per CTA (stage reuse across sites)
+        rr = cd.Context((8, 8, 4, 5), 24)
+        Lr = rr.links_generate(prec, scale_log2=-4)
+        ra, rb = rr.field(prec), rr.field(prec)
+        ra.generate()
+        for v, nm in enumerate(rr.variants(prec)):
+            if nm.startswith("ring"):
+                rr.set_option(cd.CD_OPT_VARIANT, v)
+                Lr.apply(rb, ra)
+                Lr.apply_dagger(ra, rb)
     if which in ("all", "mrhs") and prec == "fp16":
+        # 4^4 x 128 rhs: 256 items over 148 CTAs (ring stages and B slots reused)
+        mr = cd.Context((4, 4, 4, 4), 24)
+        ml4 = mr.links_generate("fp16", kind="hermitian", scale_log2=-4)
+        m4x, m4y = mr.field("fp16", nrhs=128), mr.field("fp16", nrhs=128)
+        m4x.generate()
+        ml4.apply_mrhs(m4y, m4x)
         x, y = ctx.field("fp16", nrhs=128), ctx.field("fp16", nrhs=128)
         x.generate()
         L.apply_mrhs(y, x)
