@@ -54,6 +54,20 @@ for prec in ("fp32", "fp16"):
                 Lh.apply_dagger(x, y)
             h.set_option(cd.CD_OPT_VARIANT, -1)
             h.halo_exchange(x)
+            # the fused split apply with several sites per CTA (stage reuse, face sites last)
+            fz = cd.Context((8, 8, 4, 5), 24)
+            fz.set_option(cd.CD_OPT_HALO_SELF_MASK, 0b1000)
+            if tr == "peer":
+                fz.peer_connect([fz.peer_handle()])
+            fz.set_transport(tr)
+            Lf = fz.links_generate(prec, kind="hermitian", scale_log2=-4)
+            fa, fb = fz.field(prec), fz.field(prec)
+            fa.generate()
+            for v, nm in enumerate(fz.variants(prec)):
+                if nm.startswith("ring"):
+                    fz.set_option(cd.CD_OPT_VARIANT, v)
+                    Lf.apply(fb, fa)
+                    Lf.apply_dagger(fa, fb)
             Ch, _ = Lh.compress_hermitian()
             Ch.apply(y, x)
             if prec == "fp16":
