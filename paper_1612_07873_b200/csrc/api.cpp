@@ -410,6 +410,7 @@ static void ctx_release(cd_context *c)
     if (c->ev_in) cudaEventDestroy(c->ev_in);
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
     peer_release(c);
+    if (c->err_host) cudaFreeHost(c->err_host);
     comm_destroy(c->comm);
     delete c;
 }
@@ -478,6 +479,13 @@ int cd_context_create(const cd_geometry *geom, int device, int nranks, int rank,
     if (e == cudaSuccess) e = cudaMalloc(&c->ysplit, sizeof(float2) * c->V * c->N);
     if (e == cudaSuccess) e = cudaMalloc(&c->site_cnt, sizeof(int) * c->V);
     if (e == cudaSuccess) e = cudaMemset(c->site_cnt, 0, sizeof(int) * c->V);
+    if (e == cudaSuccess) {   // host-mapped transport error word (in-kernel arrival-wait timeouts)
+        e = cudaHostAlloc(reinterpret_cast<void **>(&c->err_host), sizeof(int), cudaHostAllocMapped);
+        if (e == cudaSuccess) {
+            *c->err_host = 0;
+            e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->err_dev), c->err_host, 0);
+        }
+    }
     if (e == cudaSuccess) e = cudaMalloc(&c->pack_cnt, sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(c->pack_cnt, 0, sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc(&c->chain_cnt, sizeof(unsigned) * c->V);

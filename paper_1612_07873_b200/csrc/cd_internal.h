@@ -227,7 +227,7 @@ struct ApplyArgs {
     // CTA to finish signals kPutCtas per block), takes interior sites before face sites, and its
     // producer reads a face site's remote records from this rank's window after an in-kernel
     // arrival wait -- one launch per apply, no halo-term kernel, no partials
-    int fused;
+    int fused;                           // 1: fused split apply (peer transport)
     PackDst pd;                          // pack destinations + the peers' arrival counters
     const unsigned long long *wflag;     // this rank's arrival counters [mu][blk]
     unsigned wmask;                      // blocks to wait for (bit 2mu+blk)
@@ -253,6 +253,7 @@ cudaError_t launch_dslash(cd_precision p, int id, const ApplyArgs &a, cudaStream
 cudaError_t launch_halo(cd_precision p, const ApplyArgs &a, cudaStream_t s);
 cudaError_t launch_pack(cd_precision p, int nvec, const void *field, const PackDst &d, const KGeom &g, cudaStream_t s);
 cudaError_t launch_peer_wait(const PeerWait &w, cudaStream_t s);
+
 // bulk peer put of one chunk: for every block in `mask`, len[mu][blk] bytes from src[mu][blk] to
 // d.dst[mu][blk], then bump d.flag[mu][blk] once per CTA (kPutCtas CTAs per block)
 cudaError_t launch_peer_put(const unsigned char *const src[4][2], const int64_t len[4][2], unsigned mask,

@@ -132,8 +132,8 @@ int transport_of(const cd_context *c)
 int transport_check(cd_context *c, std::string &err)
 {
     if (c->err_host && *reinterpret_cast<volatile int *>(c->err_host)) {
-        err = "peer halo transport: a wait for a neighbour's halo timed out (a rank stopped calling the collective "
-              "applies, or the ranks issued them in different orders); the context's results are invalid";
+        err = "halo transport: an in-kernel wait for a neighbour's halo timed out (a rank stopped calling the "
+              "collective applies, or the ranks issued them in different orders); the context's results are invalid";
         return CD_ERR_COMM;
     }
     return comm_check(c->comm, err);
@@ -332,13 +332,6 @@ int peer_window_export(cd_context *ctx, size_t slot_bytes, unsigned char out[64]
         cudaError_t e = cudaMalloc(&w, kWinHeader + 2 * slot);
         if (e == cudaSuccess) e = cudaMemset(w, 0, kWinHeader + 2 * slot);
         if (e == cudaSuccess) e = cudaDeviceSynchronize();   // counters are zero before any peer can map them
-        if (e == cudaSuccess && !ctx->err_host) {
-            e = cudaHostAlloc(reinterpret_cast<void **>(&ctx->err_host), sizeof(int), cudaHostAllocMapped);
-            if (e == cudaSuccess) {
-                *ctx->err_host = 0;
-                e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&ctx->err_dev), ctx->err_host, 0);
-            }
-        }
         if (e != cudaSuccess) {
             if (w) cudaFree(w);
             err = std::string("peer window: ") + cudaGetErrorString(e);
@@ -398,9 +391,6 @@ void peer_release(cd_context *ctx)
     ctx->ipc_opened.clear();
     if (ctx->win) cudaFree(ctx->win);
     ctx->win = nullptr;
-    if (ctx->err_host) cudaFreeHost(ctx->err_host);
-    ctx->err_host = nullptr;
-    ctx->err_dev = nullptr;
     ctx->peer_ready = false;
 }
 

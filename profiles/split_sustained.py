@@ -24,6 +24,8 @@ ap.add_argument("--mask", type=int, default=8)
 ap.add_argument("--variant", type=int, default=10)
 ap.add_argument("--secs", type=float, default=1.0)
 ap.add_argument("--rounds", type=int, default=3)
+ap.add_argument("--nccl-reserve", type=int, nargs="*", default=[],
+                help="also time the (unfused) NCCL split with these SM reserves")
 a = ap.parse_args()
 rows = []
 proc = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm,power.draw", "--format=csv,noheader,nounits", "-i", "0",
@@ -42,13 +44,19 @@ def reader():
 threading.Thread(target=reader, daemon=True).start()
 dims = tuple(a.dims)
 runs = {}
-for name in ("unsplit", "unsplit_nopdl", "split_peer", "split_peer_unfused"):
+runs_wanted = ["unsplit", "unsplit_nopdl", "split_peer", "split_peer_unfused"] + \
+    [f"split_nccl_r{r}" for r in a.nccl_reserve]
+for name in runs_wanted:
     os.environ["CD_FUSE_SPLIT"] = "0" if name == "split_peer_unfused" else "1"   # read at context creation
     ctx = cd.Context(dims, a.nvec)
-    if name.startswith("split"):
+    if name.startswith("split_peer"):
         ctx.set_option(cd.CD_OPT_HALO_SELF_MASK, a.mask)
         ctx.peer_connect([ctx.peer_handle()])
         ctx.set_transport("peer")
+    if name.startswith("split_nccl"):
+        ctx.set_option(cd.CD_OPT_HALO_SELF_MASK, a.mask)
+        ctx.set_transport("nccl")
+        ctx.set_option(cd.CD_OPT_NCCL_SM_RESERVE, int(name.split("_r")[1]))
     if name == "unsplit_nopdl":
         ctx.set_option(cd.CD_OPT_PDL, 0)
     ctx.set_option(cd.CD_OPT_VARIANT, a.variant)
