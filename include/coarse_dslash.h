@@ -103,7 +103,11 @@ typedef enum {
                                     2 peer: the halo pack kernel stores the faces straight into the
                                       neighbours' CUDA-IPC-mapped receive windows over NVLink and
                                       signals arrival counters; the receiver waits on the device
-                                      (needs cd_context_peer_handle / cd_context_peer_connect);
+                                      (needs cd_context_peer_handle / cd_context_peer_connect); with
+                                      a persistent (ring) variant the whole split apply is ONE
+                                      launch that waits in-kernel for its neighbours -- one rank per
+                                      GPU (or time-sliced processes); with several ranks sharing a
+                                      GPU concurrently (MPS) set CD_FUSE_SPLIT=0;
                                     3 device copy (self exchanges only). */
     CD_OPT_NCCL_SM_RESERVE = 5,/* SMs the persistent interior kernel leaves free while an NCCL halo
                                   exchange is in flight (its kernels need SMs to progress); default 8 */
