@@ -958,6 +958,45 @@ def test_random_geometry_sweep(dims, nvec, prec, mask, vseed):
     assert rel_l2(fout.export(), oracle.adjoint(dims, Lh, v)) <= tol
 
 
+def _fuzz_split_cases(n=16, seed=20261018):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        dims = tuple(int(d) for d in rng.integers(2, 7, size=4))
+        prec = str(rng.choice(["fp32", "fp16"]))
+        mask = int(rng.integers(1, 16))
+        tr = str(rng.choice(["copy", "nccl", "peer", "peer"]))
+        out.append((dims, prec, mask, tr, int(rng.integers(0, 1 << 30))))
+    return out
+
+
+@pytest.mark.parametrize("dims,prec,mask,transport,vseed", _fuzz_split_cases())
+def test_random_split_sweep(dims, prec, mask, transport, vseed):
+    """Random lattices with several sites per CTA (extents 2-6), random halo masks routed through
+    a random transport, every ring variant (the peer transport runs them as the fused split apply)
+    and the tuned choice: apply and dagger vs the oracle."""
+    nvec = 24
+    N = 2 * nvec
+    Lh = synth.links(dims, N, kind="hermitian", seed=vseed)
+    v = synth.vector(dims, N, seed=vseed + 1)
+    ref, refd = oracle.apply(dims, Lh, v), oracle.adjoint(dims, Lh, v)
+    ctx = cd.Context(dims, nvec)
+    ctx.set_option(cd.CD_OPT_HALO_SELF_MASK, mask)
+    if transport == "peer":
+        ctx.peer_connect([ctx.peer_handle()])
+    ctx.set_transport(transport)
+    L = ctx.links_upload(Lh, prec)
+    fin, fout = ctx.field(prec), ctx.field(prec)
+    fin.import_(v)
+    names = ctx.variants(prec)
+    for var in [i for i, nm in enumerate(names) if nm.startswith("ring")] + [-1]:
+        ctx.set_option(cd.CD_OPT_VARIANT, var)
+        L.apply(fout, fin)
+        assert rel_l2(fout.export(), ref) <= TOL[prec], (names[var] if var >= 0 else "tuned")
+        L.apply_dagger(fout, fin)
+        assert rel_l2(fout.export(), refd) <= TOL[prec], (names[var] if var >= 0 else "tuned")
+
+
 # ---------------------------------------------------------------- link kinds (ADVICE r01: wrong kind -> CD_ERR_INVALID)
 def test_link_kinds_rejected_synchronously():
     """Calls given a link kind they do not support fail with CD_ERR_INVALID and enqueue nothing
