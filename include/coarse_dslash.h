@@ -110,7 +110,8 @@ typedef enum {
                                       GPU concurrently (MPS) set CD_FUSE_SPLIT=0;
                                     3 device copy (self exchanges only). */
     CD_OPT_NCCL_SM_RESERVE = 5,/* SMs the persistent interior kernel leaves free while an NCCL halo
-                                  exchange is in flight (its kernels need SMs to progress); default 8 */
+                                  exchange is in flight (its kernels need SMs to progress); default 4
+                                  (the library's communicators cap NCCL at CD_NCCL_MAX_CTAS = 4 CTAs) */
     CD_OPT_PEER_TIMEOUT_MS = 6 /* peer transport: give up waiting for a neighbour's halo after this
                                   long (the context then reports CD_ERR_COMM); default 60000 */
 } cd_option;

@@ -140,7 +140,7 @@ struct cd_context {
     cd::Comm *comm = nullptr;
     // halo transport
     int transport = 0;                // CD_OPT_TRANSPORT
-    int nccl_sm_reserve = 8;          // CD_OPT_NCCL_SM_RESERVE: SMs the interior leaves to NCCL's kernels
+    int nccl_sm_reserve = 4;          // CD_OPT_NCCL_SM_RESERVE: SMs the interior leaves to NCCL (capped at 4 CTAs)
     unsigned char *win = nullptr;     // own peer window (kWinHeader + 2 slots)
     size_t win_slot = 0;
     unsigned char *peer_win[4][2] = {};   // window of the rank at +mu (dir 0) / -mu (dir 1)

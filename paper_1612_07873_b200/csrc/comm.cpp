@@ -8,6 +8,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -21,6 +22,7 @@ struct NcclApi {
     void *h = nullptr;
     ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
     ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommInitRankConfig)(ncclComm_t *, int, ncclUniqueId, int, ncclConfig_t *) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;
     ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
@@ -49,6 +51,8 @@ static bool load_nccl(std::string &err)
     SYM(GetUniqueId, "ncclGetUniqueId");
     SYM(CommInitRank, "ncclCommInitRank");
     SYM(CommDestroy, "ncclCommDestroy");
+    // optional (NCCL >= 2.14): per-communicator CTA cap
+    *reinterpret_cast<void **>(&g_nccl.CommInitRankConfig) = dlsym(h, "ncclCommInitRankConfig");
     SYM(CommGetAsyncError, "ncclCommGetAsyncError");
     SYM(Send, "ncclSend");
     SYM(Recv, "ncclRecv");
@@ -84,7 +88,19 @@ int comm_create(const uint8_t id_bytes[128], int nranks, int rank, Comm **out, s
     ncclUniqueId id;
     memcpy(&id, id_bytes, 128);
     Comm *c = new Comm();
-    ncclResult_t r = g_nccl.CommInitRank(&c->comm, nranks, id, rank);
+    ncclResult_t r;
+    if (g_nccl.CommInitRankConfig) {
+        // cap NCCL's CTAs (CD_NCCL_MAX_CTAS, default 4) so its send/recv kernels fit in the SMs the
+        // persistent interior leaves free (CD_OPT_NCCL_SM_RESERVE, default 8): a halo of <= 1.6 MB
+        // per rank does not need more, and the stencil keeps the rest of the GPU
+        ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+        const char *ev = getenv("CD_NCCL_MAX_CTAS");
+        cfg.maxCTAs = ev ? atoi(ev) : 4;
+        cfg.minCTAs = 1;
+        r = g_nccl.CommInitRankConfig(&c->comm, nranks, id, rank, &cfg);
+    } else {
+        r = g_nccl.CommInitRank(&c->comm, nranks, id, rank);
+    }
     if (r != ncclSuccess) {
         err = std::string("ncclCommInitRank: ") + g_nccl.GetErrorString(r);
         delete c;
