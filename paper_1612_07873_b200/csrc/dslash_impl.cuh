@@ -733,17 +733,45 @@ __global__ void __launch_bounds__(FgCfg<P, NV, KW, WR>::THREADS) dslash_fg(Apply
             Lc[kk][c] = on[kk] ? ld_stream(m + row * Q::ROWB + (d + Q::D * c) * 16) : make_uint4(0, 0, 0, 0);
         sl[kk] = (Q::F16 && on[kk]) ? ld_nc_f32(m + Q::MSCALE) : 0.0f;
     }
+    // the latency regime (a grid of at most a few CTAs per SM): each lane loads the neighbour
+    // chunks it needs straight into registers -- no staging round trip through shared memory
+    // and no barrier between the vectors' arrival and the math (the floor of a dependent launch
+    // is ~0.82 us; this is on the path after griddepcontrol.wait, profiles/r02/launch_floor.txt)
+    // Measured (profiles/r02/fg_direct_ab.txt): 2^4 fp32 kw1_wr2 2.03 -> 1.62 us, fp16 kw1_wr1
+    // 4.84 -> 3.79 us; at 4^4 (>= 512 CTAs) the staged path is faster (6.80 vs 7.31 us), so the
+    // direct path is gated to grids of at most two CTAs per SM.
+    constexpr bool kDirect = KW == 1;   // registers: KW x C chunks more (kw3 would lose occupancy, kw9 spill)
+    constexpr int KD = kDirect ? KW : 1;
+    const bool direct = kDirect && a.g.V * F::NRB <= 2 * 148;
+    const unsigned char *nbrec[KD];
+#pragma unroll
+    for (int kk = 0; kk < KD; kk++) {
+        const int k = kseq(wk * KW + kk);
+        nbrec[kk] = in + (size_t)neighbour(a.g, x, site, k) * Q::VREC;
+    }
     pdl_trigger();
     pdl_wait();
 
-    // 2. the nine neighbour records -> shared memory (one 16-B chunk per thread-step)
-    for (int t = threadIdx.x; t < 9 * Q::VCH; t += F::THREADS) {
-        const int k = t / Q::VCH, e = t - k * Q::VCH;
-        if (a.halo && remote_hop(a.g, x, k)) continue;
-        const int nb = neighbour(a.g, x, site, k);
-        *reinterpret_cast<uint4 *>(vs + k * Q::VREC + e * 16) = ld_nc(in + (size_t)nb * Q::VREC + e * 16);
+    uint4 Vd[KD][Q::C];
+    float svd[KD];
+    if (direct) {
+#pragma unroll
+        for (int kk = 0; kk < KD; kk++) {
+#pragma unroll
+            for (int c = 0; c < Q::C; c++)
+                Vd[kk][c] = on[kk] ? ld_nc(nbrec[kk] + (d + Q::D * c) * 16) : make_uint4(0, 0, 0, 0);
+            svd[kk] = (Q::F16 && on[kk]) ? ld_nc_f32(nbrec[kk] + Q::VSCALE) : 0.0f;
+        }
+    } else {
+        // 2. the nine neighbour records -> shared memory (one 16-B chunk per thread-step)
+        for (int t = threadIdx.x; t < 9 * Q::VCH; t += F::THREADS) {
+            const int k = t / Q::VCH, e = t - k * Q::VCH;
+            if (a.halo && remote_hop(a.g, x, k)) continue;
+            const int nb = neighbour(a.g, x, site, k);
+            *reinterpret_cast<uint4 *>(vs + k * Q::VREC + e * 16) = ld_nc(in + (size_t)nb * Q::VREC + e * 16);
+        }
+        __syncthreads();
     }
-    __syncthreads();
 
     // 3. dot products (ILP: one accumulator pair per chunk, Listing 5)
     float re = 0.0f, im = 0.0f;
@@ -759,7 +787,7 @@ __global__ void __launch_bounds__(FgCfg<P, NV, KW, WR>::THREADS) dslash_fg(Apply
                 pr[c] = 0.0f;
                 pi[c] = 0.0f;
                 const int q = d + Q::D * c;
-                uint4 vq = lds128(vrec + q * 16);
+                uint4 vq = direct ? Vd[kDirect ? kk : 0][c] : lds128(vrec + q * 16);
                 if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<false>(vq);
                 cmac2(Lc[kk][c], vq, pr[c], pi[c]);
             }
@@ -770,11 +798,11 @@ __global__ void __launch_bounds__(FgCfg<P, NV, KW, WR>::THREADS) dslash_fg(Apply
 #pragma unroll
             for (int c = 0; c < Q::C; c++) {
                 const int q = d + Q::D * c;
-                uint4 vq = lds128(vrec + q * 16);
+                uint4 vq = direct ? Vd[kDirect ? kk : 0][c] : lds128(vrec + q * 16);
                 if (a.dagger && q * Q::CPC >= NV) vq = neg_chunk<true>(vq);
                 hmac4(Lc[kk][c], vq, ra, rb2, ia, ib);
             }
-            const float sc = sl[kk] * *reinterpret_cast<const float *>(vrec + Q::VSCALE);
+            const float sc = sl[kk] * (direct ? svd[kDirect ? kk : 0] : *reinterpret_cast<const float *>(vrec + Q::VSCALE));
             re = fmaf(ra - rb2, sc, re);
             im = fmaf(ia + ib, sc, im);
         }
