@@ -120,6 +120,11 @@ __device__ __forceinline__ void bulk_g2s_hint(void *dst_smem, const void *src, u
         ::"r"((uint32_t)__cvta_generic_to_shared(dst_smem)), "l"(src), "r"(bytes),
           "r"((uint32_t)__cvta_generic_to_shared(bar)), "l"(policy) : "memory");
 }
+// bulk prefetch of [src, src + bytes) into L2 (no shared-memory destination, no completion)
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 // 4-byte asynchronous shared-memory store whose completion is counted (4 tx bytes) on an
 // mbarrier: a value delivered exactly like TMA data, ordered by the barrier's phase.
 __device__ __forceinline__ void st_async_u32(void *dst_smem, uint32_t v, uint64_t *bar)

@@ -175,7 +175,7 @@ __device__ __forceinline__ float hop_scale(const unsigned char *links, const uns
 template <int NV, int NBS>
 __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
     dslash_mrhs(const unsigned char *__restrict__ links, const unsigned char *__restrict__ in, unsigned char *out,
-                KGeom g, int nrb, int dagger, const int *sites, int nsites, MrhsHalo hl, long long *trace)
+                KGeom g, int nrb, int dagger, const int *sites, int nsites, MrhsHalo hl, long long *trace, int pf)
 {
     using C = MrhsCfg<NV, NBS>;
     // optional diagnostic trace of CTA 0 (CD_MRHS_TRACE): trace[ev * 512 + index] = clock64()
@@ -236,6 +236,16 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
                 const int site = item_site(it, nrb, rb, sites);
                 int x[4];
                 decode(g, site, x);
+                // L2 prefetch of the next item's 9 link records (one contiguous run, read from DRAM
+                // once per apply): the ring's link copies then see L2 rather than DRAM latency.
+                // Nvec 32 (16 KB records): 147 -> 144 us at 6^3x12 x 128; Nvec 24: neutral to 1 %
+                // slower, off.  Prefetching the neighbour blocks too was slower for both
+                // (profiles/r02/mrhs_l2_prefetch_ab.txt).
+                if (pf && it + gridDim.x < items) {
+                    int rbp;
+                    const int sp = item_site(it + gridDim.x, nrb, rbp, sites);
+                    bulk_prefetch_l2(links + (size_t)sp * 9 * C::MREC, 9 * C::MREC);
+                }
                 for (int k = 0; k < 9; k++, h++) {
                     const int st = h % C::S;
                     mbar_wait(&empty[st], ((h / C::S) & 1) ^ 1);
@@ -458,6 +468,8 @@ static cudaError_t launch_mrhs_t(const void *links, const void *in, void *out, c
     MrhsHalo hl{};
     if (halo) hl = *halo;
     count_launch();
+    const char *pfe = getenv("CD_MRHS_PF");   // A/B switch: 0 / 1 override the per-Nvec default
+    const int pf = pfe ? atoi(pfe) : (NV == 32);
     long long *trace = nullptr;
     const char *tf = getenv("CD_MRHS_TRACE");   // diagnostic only: per-event clock64 of CTA 0
     if (tf) {
@@ -466,7 +478,7 @@ static cudaError_t launch_mrhs_t(const void *links, const void *in, void *out, c
     }
     dslash_mrhs<NV, NBS><<<(unsigned)(items < num_sms ? items : num_sms), C::THREADS, C::SMEM, s>>>(
         static_cast<const unsigned char *>(links), static_cast<const unsigned char *>(in),
-        static_cast<unsigned char *>(out), g, nrb, dagger, sites, nsites, hl, trace);
+        static_cast<unsigned char *>(out), g, nrb, dagger, sites, nsites, hl, trace, pf);
     cudaError_t e = cudaGetLastError();
     if (tf) {
         long long h[10 * 512];
