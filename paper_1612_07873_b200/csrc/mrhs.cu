@@ -175,7 +175,8 @@ __device__ __forceinline__ float hop_scale(const unsigned char *links, const uns
 template <int NV, int NBS>
 __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
     dslash_mrhs(const unsigned char *__restrict__ links, const unsigned char *__restrict__ in, unsigned char *out,
-                KGeom g, int nrb, int dagger, const int *sites, int nsites, MrhsHalo hl, long long *trace, int pf)
+                KGeom g, int nrb, int dagger, const int *sites, int nsites, MrhsHalo hl, long long *trace, int pf,
+                int smax, int exp)
 {
     using C = MrhsCfg<NV, NBS>;
     // optional diagnostic trace of CTA 0 (CD_MRHS_TRACE): trace[ev * 512 + index] = clock64()
@@ -247,16 +248,18 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
                     bulk_prefetch_l2(links + (size_t)sp * 9 * C::MREC, 9 * C::MREC);
                 }
                 for (int k = 0; k < 9; k++, h++) {
-                    const int st = h % C::S;
-                    mbar_wait(&empty[st], ((h / C::S) & 1) ^ 1);
-                    mbar_wait(&lempty[st], ((h / C::S) & 1) ^ 1);
+                    const int st = h % smax;
+                    mbar_wait(&empty[st], ((h / smax) & 1) ^ 1);
+                    mbar_wait(&lempty[st], ((h / smax) & 1) ^ 1);
                     unsigned char *dst = ring + st * C::STAGE;
-                    mbar_arrive_expect_tx(&full[st], C::BLK + C::MREC);
+                    mbar_arrive_expect_tx(&full[st], ((exp & 8) ? 0 : C::BLK) + ((exp & 4) ? 0 : C::MREC));
                     // vectors are re-read by 9 sites (keep them in L2), links are read once
-                    bulk_g2s_hint(dst, nbr_block<C::BLK>(g, hl, in, x, site, k, nrb, rb), C::BLK,
-                                  &full[st], pol_v);
-                    bulk_g2s_hint(dst + C::BLK, links + ((size_t)site * 9 + k) * C::MREC, C::MREC, &full[st],
-                                  pol_l);
+                    if (!(exp & 8))
+                        bulk_g2s_hint(dst, nbr_block<C::BLK>(g, hl, in, x, site, k, nrb, rb), C::BLK,
+                                      &full[st], pol_v);
+                    if (!(exp & 4))
+                        bulk_g2s_hint(dst + C::BLK, links + ((size_t)site * 9 + k) * C::MREC, C::MREC, &full[st],
+                                      pol_l);
                     TR(0, h)
                 }
             }
@@ -275,8 +278,8 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
                 const uint32_t d = tmem + acc * C::NB;
                 TR(9, t)
                 for (int k = 0; k < 9; k++, h++) {
-                    const int st = h % C::S, bs = h % C::NBS;
-                    mbar_wait(&full[st], (h / C::S) & 1);
+                    const int st = h % smax, bs = h % C::NBS;
+                    mbar_wait(&full[st], (h / smax) & 1);
                     TR(1, h)
                     mbar_wait(&bfull[bs], (h / C::NBS) & 1);
                     TR(2, h)
@@ -284,6 +287,7 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
                     const uint32_t a0 = ring0 + st * C::STAGE, b0 = bb0 + bs * C::B_BYTES;
 #pragma unroll
                     for (int s = 0; s < C::KSTEPS; s++) {
+                        if (exp & 2) break;
                         const uint64_t da = smem_desc(a0 + 2 * s * C::LBO_A, C::LBO_A, 128);
                         const uint64_t db = smem_desc(b0 + 2 * s * C::LBO_B, C::LBO_B, 128);
                         const uint32_t accum = (k > 0 || s > 0) ? 1u : 0u;
@@ -332,11 +336,17 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
             for (int k = 0; k < 9; k++) sref = fmaxf(sref, hsb[k]);
             const float isref = sref > 0.0f ? __frcp_rn(sref) : 0.0f;
             for (int k = 0; k < 9; k++, h++) {
-                const int st = h % C::S, bs = h % C::NBS;
+                const int st = h % smax, bs = h % C::NBS;
                 const uint32_t ratio = half2_bits(hsb[k] * isref);
                 mbar_wait(&bempty[bs], ((h / C::NBS) & 1) ^ 1);
                 if (bt == 0) TR(3, h)
-                mbar_wait(&full[st], (h / C::S) & 1);
+                mbar_wait(&full[st], (h / smax) & 1);
+                if (exp & 1) {
+                    mbar_arrive(&lempty[st]);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&bfull[bs]);
+                    continue;
+                }
                 if (bt == 0) TR(4, h)
                 const unsigned char *lraw = ring + st * C::STAGE + C::BLK;
                 unsigned char *Bs = bbuf + bs * C::B_BYTES;
@@ -470,6 +480,11 @@ static cudaError_t launch_mrhs_t(const void *links, const void *in, void *out, c
     count_launch();
     const char *pfe = getenv("CD_MRHS_PF");   // A/B switch: 0 / 1 override the per-Nvec default
     const int pf = pfe ? atoi(pfe) : (NV == 32);
+    // diagnostic knobs (timing experiments only; results are wrong with exp != 0): CD_MRHS_SMAX caps the
+    // ring stages, CD_MRHS_EXP bit 0 = builders skip the B build, 1 = no MMA, 2 = no link copy, 3 = no A copy
+    const char *sme = getenv("CD_MRHS_SMAX"), *exe = getenv("CD_MRHS_EXP");
+    const int smax = sme && atoi(sme) >= 2 && atoi(sme) < C::S ? atoi(sme) : C::S;
+    const int exp = exe ? atoi(exe) : 0;
     long long *trace = nullptr;
     const char *tf = getenv("CD_MRHS_TRACE");   // diagnostic only: per-event clock64 of CTA 0
     if (tf) {
@@ -478,7 +493,7 @@ static cudaError_t launch_mrhs_t(const void *links, const void *in, void *out, c
     }
     dslash_mrhs<NV, NBS><<<(unsigned)(items < num_sms ? items : num_sms), C::THREADS, C::SMEM, s>>>(
         static_cast<const unsigned char *>(links), static_cast<const unsigned char *>(in),
-        static_cast<unsigned char *>(out), g, nrb, dagger, sites, nsites, hl, trace, pf);
+        static_cast<unsigned char *>(out), g, nrb, dagger, sites, nsites, hl, trace, pf, smax, exp);
     cudaError_t e = cudaGetLastError();
     if (tf) {
         long long h[10 * 512];
@@ -493,10 +508,361 @@ static cudaError_t launch_mrhs_t(const void *links, const void *in, void *out, c
     return e;
 }
 
+// ===================================================================================== TS variant
+// The same product with the roles swapped (round 2): the LINK is the MMA's A operand, built by the
+// builder warps straight into tensor memory (tcgen05.st), and the stored neighbour block is the B
+// operand (N = 128 rhs, K-major exactly as stored: same descriptor as the A of the kernel above):
+//
+//     D[m][r] = sum_K A_k[m][K] v_r(nbr_k)[K],   A_k row 2i = ratio_k (L_i.re, -L_i.im),
+//                                                A_k row 2i+1 = ratio_k (L_i.im, L_i.re)
+//
+// so D lane 2i holds y_i.re and lane 2i+1 y_i.im for every rhs column (M = 128 lanes, 2N = 96 or
+// 128 of them used; with Nvec 24 lanes 96-127 are never written and never read).  No B slots in
+// shared memory: the ring gets one more stage (Nvec 24: 6, Nvec 32: 4) and a hop's link no longer
+// crosses shared memory twice more (B build write + MMA read).  The epilogue re-quantises through a
+// padded shared staging tile (pitch 2080 B per K chunk: conflict-free 32-bit stores) that leaves
+// with one bulk store per K chunk.
+template <int NV>
+struct MrhsTsCfg {
+    static constexpr int N = 2 * NV;
+    static constexpr int MR = 128;                          // rhs per block (MMA N)
+    static constexpr int KCH = N / 4;                       // 16-B K chunks per hop
+    static constexpr int KSTEPS = KCH / 2;                  // MMA K = 16 halves
+    static constexpr int LBO = MR * 16;                     // 2048
+    static constexpr int A_BYTES = KCH * LBO;
+    static constexpr int BLK = A_BYTES + 16;
+    static constexpr int MREC = 4 * N * N + 16;
+    static constexpr int STAGE = (BLK + MREC + 127) / 128 * 128;
+    static constexpr int ACOLS = N;                         // 32-bit TMEM columns of one A slot (2N halves)
+    static constexpr int NBS = 3;                           // A slots in TMEM
+    static constexpr int PITCH = LBO + 32;                  // staging pitch per K chunk
+    static constexpr int STG = KCH * PITCH;
+    static constexpr int HDR = 1024;
+    static constexpr int SMEM_MAX = 232448;
+    static constexpr int S = (SMEM_MAX - HDR - STG) / STAGE;
+    static constexpr int SMEM = HDR + STG + S * STAGE;
+    static constexpr int NBT = 128;                         // builder threads (warps 2-5)
+    static constexpr int THREADS = 320;                     // + epilogue warps 6-9
+    static constexpr int DCOL = 0, ACOL = 2 * MR;           // TMEM: two accumulators, then A slots
+    static_assert(S >= 2, "ring too small");
+    static_assert(ACOL + NBS * ACOLS <= 512, "TMEM columns");
+};
+
+__device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t *r)
+{
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(addr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+__device__ __forceinline__ void bulk_s2g_hint(void *dst, const void *src_smem, uint32_t bytes, uint64_t pol)
+{
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+                 "r"((uint32_t)__cvta_generic_to_shared(src_smem)), "r"(bytes), "l"(pol)
+                 : "memory");
+}
+
+template <int NV>
+__global__ void __launch_bounds__(MrhsTsCfg<NV>::THREADS, 1)
+    dslash_mrhs_ts(const unsigned char *__restrict__ links, const unsigned char *__restrict__ in, unsigned char *out,
+                   KGeom g, int nrb, int dagger, const int *sites, int nsites, MrhsHalo hl, int pf)
+{
+    using C = MrhsTsCfg<NV>;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem);       // [S]
+    uint64_t *empty = full + 16;                                 // [S]
+    uint64_t *lempty = full + 32;                                // [S]
+    uint64_t *bfull = full + 48;                                 // [NBS]
+    uint64_t *bempty = full + 52;                                // [NBS]
+    uint64_t *accfull = full + 56;                               // [2]
+    uint64_t *accempty = full + 58;                              // [2]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + 512);
+    float *red = reinterpret_cast<float *>(smem + 640);          // [4] epilogue max
+    float *hs = reinterpret_cast<float *>(smem + 704);           // [2][9] builder hop scales
+    float *es = reinterpret_cast<float *>(smem + 800);           // [9]    epilogue hop scales
+    unsigned char *stg = smem + C::HDR;                          // [KCH][PITCH] output staging
+    unsigned char *ring = stg + C::STG;                          // [S][STAGE]
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t items = (int64_t)(sites ? nsites : g.V) * nrb;
+
+    if (tid == 0) {
+        for (int j = 0; j < C::S; j++) {
+            mbar_init(&full[j], 1);
+            mbar_init(&empty[j], 1);            // the MMA commit (B = neighbour block consumed)
+            mbar_init(&lempty[j], C::NBT);      // every builder thread (raw link record read)
+        }
+        for (int j = 0; j < C::NBS; j++) {
+            mbar_init(&bfull[j], 4);            // one arrival per builder warp
+            mbar_init(&bempty[j], 1);
+        }
+        for (int j = 0; j < 2; j++) {
+            mbar_init(&accfull[j], 1);
+            mbar_init(&accempty[j], 4);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        const uint32_t a = (uint32_t)__cvta_generic_to_shared(tmem_slot);
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(a), "n"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ producer (as dslash_mrhs)
+        if (lane == 0) {
+            const uint64_t pol_v = l2_policy_evict_last(), pol_l = l2_policy_evict_first();
+            uint32_t h = 0;
+            for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+                int rb;
+                const int site = item_site(it, nrb, rb, sites);
+                int x[4];
+                decode(g, site, x);
+                if (pf && it + gridDim.x < items) {
+                    int rbp;
+                    const int sp = item_site(it + gridDim.x, nrb, rbp, sites);
+                    bulk_prefetch_l2(links + (size_t)sp * 9 * C::MREC, 9 * C::MREC);
+                }
+#pragma unroll 1
+                for (int k = 0; k < 9; k++, h++) {
+                    const int st = h % C::S;
+                    mbar_wait(&empty[st], ((h / C::S) & 1) ^ 1);
+                    mbar_wait(&lempty[st], ((h / C::S) & 1) ^ 1);
+                    unsigned char *dst = ring + st * C::STAGE;
+                    mbar_arrive_expect_tx(&full[st], C::BLK + C::MREC);
+                    bulk_g2s_hint(dst, nbr_block<C::BLK>(g, hl, in, x, site, k, nrb, rb), C::BLK, &full[st], pol_v);
+                    bulk_g2s_hint(dst + C::BLK, links + ((size_t)site * 9 + k) * C::MREC, C::MREC, &full[st], pol_l);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer (A in TMEM, B in smem)
+        if (lane == 0) {
+            // F32 accumulate, F16 A/B, both K-major, N = 128 (>> 3 at bit 17), M = 128 (>> 4 at bit 24)
+            const uint32_t idesc = (1u << 4) | ((uint32_t)(C::MR >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+            const uint32_t ring0 = (uint32_t)__cvta_generic_to_shared(ring);
+            uint32_t h = 0, t = 0;
+            for (int64_t it = blockIdx.x; it < items; it += gridDim.x, t++) {
+                const int acc = t & 1;
+                mbar_wait(&accempty[acc], ((t >> 1) & 1) ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t d = tmem + C::DCOL + acc * C::MR;
+#pragma unroll 1
+                for (int k = 0; k < 9; k++, h++) {
+                    const int st = h % C::S, bs = h % C::NBS;
+                    mbar_wait(&full[st], (h / C::S) & 1);
+                    mbar_wait(&bfull[bs], (h / C::NBS) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t b0 = ring0 + st * C::STAGE, a0 = tmem + C::ACOL + bs * C::ACOLS;
+#pragma unroll
+                    for (int s = 0; s < C::KSTEPS; s++) {
+                        const uint64_t db = smem_desc(b0 + 2 * s * C::LBO, C::LBO, 128);
+                        const uint32_t accum = (k > 0 || s > 0) ? 1u : 0u;
+                        asm volatile(
+                            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+                            "r"(a0 + 8 * s), "l"(db), "r"(idesc), "r"(accum));
+                    }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                     (uint32_t)__cvta_generic_to_shared(&empty[st]))
+                                 : "memory");
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                     (uint32_t)__cvta_generic_to_shared(&bempty[bs]))
+                                 : "memory");
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 (uint32_t)__cvta_generic_to_shared(&accfull[acc]))
+                             : "memory");
+            }
+        }
+    } else if (warp < 6) {
+        // ------------------------------------------------------------ A builders (warps 2-5)
+        // warp w may only reach TMEM lanes 32 (w % 4) .. + 31: this thread owns lane (= A row) m
+        const int bt = tid - 64, q = warp & 3, m = 32 * q + lane;
+        const bool live = m < 2 * C::N;
+        const int i = m >> 1, part = m & 1;
+        const uint32_t lrow = (uint32_t)(32 * q) << 16;
+        uint32_t h = 0, t = 0;
+        float nsl = 0.0f, nsv = 0.0f;
+        auto scale_of = [&](int64_t it) {
+            int rb;
+            const int site = item_site(it, nrb, rb, sites);
+            int x[4];
+            decode(g, site, x);
+            nsl = ld_nc_f32(links + ((size_t)site * 9 + bt) * C::MREC + 4 * C::N * C::N);
+            nsv = ld_nc_f32(nbr_block<C::BLK>(g, hl, in, x, site, bt, nrb, rb) + C::A_BYTES);
+        };
+        if (bt < 9 && (int64_t)blockIdx.x < items) scale_of(blockIdx.x);
+        for (int64_t it = blockIdx.x; it < items; it += gridDim.x, t++) {
+            float *hsb = hs + (t & 1) * 9;
+            if (bt < 9) {
+                hsb[bt] = nsl * nsv;   // == hop_scale (same fp32 product as the epilogue)
+                if (it + gridDim.x < items) scale_of(it + gridDim.x);
+            }
+            bar_named(1, C::NBT);
+            float sref = 0.0f;
+#pragma unroll
+            for (int k = 0; k < 9; k++) sref = fmaxf(sref, hsb[k]);
+            const float isref = sref > 0.0f ? __frcp_rn(sref) : 0.0f;
+#pragma unroll 1
+            for (int k = 0; k < 9; k++, h++) {
+                const int st = h % C::S, bs = h % C::NBS;
+                const uint32_t ratio = half2_bits(hsb[k] * isref);
+                mbar_wait(&bempty[bs], ((h / C::NBS) & 1) ^ 1);
+                mbar_wait(&full[st], (h / C::S) & 1);
+                if (live) {
+                    const unsigned char *lraw = ring + st * C::STAGE + C::BLK + (size_t)i * C::KCH * 16;
+                    uint32_t w[C::N];
+#pragma unroll
+                    for (int c = 0; c < C::KCH; c++) *reinterpret_cast<uint4 *>(&w[4 * c]) = lds128(lraw + c * 16);
+                    mbar_arrive(&lempty[st]);   // this thread is done with the stage's link record
+#pragma unroll
+                    for (int j = 0; j < C::N; j++) {
+                        const uint32_t flip = (dagger && j >= NV) ? 0x80008000u : 0u;   // tau3 on the input
+                        const uint32_t v = hmul2_u32(w[j] ^ flip, ratio);                // (re, im) * ratio
+                        w[j] = part ? __byte_perm(v, 0, 0x1032) : (v ^ 0x80000000u);     // (im, re) | (re, -im)
+                    }
+                    const uint32_t a0 = tmem + lrow + C::ACOL + bs * C::ACOLS;
+#pragma unroll
+                    for (int u = 0; u < C::ACOLS / 16; u++) tmem_st16(a0 + 16 * u, w + 16 * u);
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                } else {
+                    mbar_arrive(&lempty[st]);
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bfull[bs]);
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue (warps 6-9)
+        const int et = tid - 192, q = warp & 3, m = 32 * q + lane;
+        const bool live = 32 * q < 2 * C::N;
+        const int i = m >> 1, part = m & 1;
+        const uint64_t pol_o = l2_policy_evict_first();
+        const uint32_t lrow = (uint32_t)(32 * q) << 16;
+        unsigned char *srow = stg + (m >> 3) * C::PITCH + ((i & 3) << 2) + part * 16;
+        uint32_t t = 0;
+        for (int64_t it = blockIdx.x; it < items; it += gridDim.x, t++) {
+            int rb;
+            const int site = item_site(it, nrb, rb, sites);
+            int x[4];
+            decode(g, site, x);
+            if (et < 9) es[et] = hop_scale<NV>(links, in, g, hl, x, site, et, nrb, rb);
+            const int acc = t & 1;
+            mbar_wait(&accfull[acc], (t >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            bar_named(2, 128);                              // es[] visible
+            float sref = 0.0f;
+#pragma unroll
+            for (int k = 0; k < 9; k++) sref = fmaxf(sref, es[k]);
+            const float sg = (dagger && i >= NV) ? -sref : sref;
+            const uint32_t base = tmem + lrow + C::DCOL + acc * C::MR;
+            // pass 1: the block's max |y| (D read twice: tensor memory is cheap to re-read)
+            float mx = 0.0f;
+            if (live) {
+#pragma unroll
+                for (int cb = 0; cb < C::MR / 32; cb++) {
+                    uint32_t raw[32];
+                    tmem_ld16_nowait(base + 32 * cb, raw);
+                    tmem_ld16_nowait(base + 32 * cb + 16, raw + 16);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    reg_fence16(raw);
+                    reg_fence16(raw + 16);
+#pragma unroll
+                    for (int j = 0; j < 32; j++) mx = fmaxf(mx, fabsf(__uint_as_float(raw[j]) * sg));
+                }
+            }
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            if (lane == 0) red[q] = mx;
+            // the previous item's bulk stores must have read the staging tile
+            if (et == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            bar_named(2, 128);
+            const float mb = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+            const float im = mb > 0.0f ? __frcp_rn(mb) : 0.0f;
+            if (live) {
+#pragma unroll
+                for (int cb = 0; cb < C::MR / 32; cb++) {
+                    uint32_t raw[32];
+                    tmem_ld16_nowait(base + 32 * cb, raw);
+                    tmem_ld16_nowait(base + 32 * cb + 16, raw + 16);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    reg_fence16(raw);
+                    reg_fence16(raw + 16);
+#pragma unroll
+                    for (int p = 0; p < 16; p++) {
+                        // lane pair (re, im) of output row i: the even lane stores column 2p, the odd
+                        // lane column 2p + 1, each as one (re, im) half2 word
+                        const float a = __uint_as_float(raw[2 * p]) * sg * im;
+                        const float b = __uint_as_float(raw[2 * p + 1]) * sg * im;
+                        const float o = __shfl_xor_sync(0xffffffffu, part ? a : b, 1);
+                        __half2 hv = part ? __floats2half2_rn(o, b) : __floats2half2_rn(a, o);
+                        *reinterpret_cast<uint32_t *>(srow + (32 * cb + 2 * p) * 16) =
+                            *reinterpret_cast<uint32_t *>(&hv);
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&accempty[acc]);   // the MMA may reuse this accumulator
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bar_named(2, 128);
+            if (et == 0) {
+                unsigned char *blk = out + ((size_t)site * nrb + rb) * C::BLK;
+#pragma unroll 1
+                for (int c = 0; c < C::KCH; c++) bulk_s2g_hint(blk + c * C::LBO, stg + c * C::PITCH, C::LBO, pol_o);
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                *reinterpret_cast<float4 *>(blk + C::A_BYTES) = make_float4(mb, 0.f, 0.f, 0.f);
+            }
+        }
+        if (et == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+}
+
+template <int NV>
+static cudaError_t launch_mrhs_ts_t(const void *links, const void *in, void *out, const KGeom &g, int nrhs, int dagger,
+                                    cudaStream_t s, int num_sms, const int *sites, int nsites, const MrhsHalo *halo)
+{
+    using C = MrhsTsCfg<NV>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(dslash_mrhs_ts<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int nrb = nrhs / C::MR;
+    const int64_t items = (int64_t)(sites ? nsites : g.V) * nrb;
+    if (items == 0) return cudaSuccess;
+    MrhsHalo hl{};
+    if (halo) hl = *halo;
+    count_launch();
+    const char *pfe = getenv("CD_MRHS_PF");
+    const int pf = pfe ? atoi(pfe) : (NV == 32);
+    dslash_mrhs_ts<NV><<<(unsigned)(items < num_sms ? items : num_sms), C::THREADS, C::SMEM, s>>>(
+        static_cast<const unsigned char *>(links), static_cast<const unsigned char *>(in),
+        static_cast<unsigned char *>(out), g, nrb, dagger, sites, nsites, hl, pf);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_mrhs(int nvec, const void *links, const void *in, void *out, const KGeom &g, int nrhs, int dagger,
                         cudaStream_t s, int num_sms, const int *sites, int nsites, const MrhsHalo *halo)
 {
     if (nrhs % 128) return cudaErrorInvalidValue;
+    // A/B switch: CD_MRHS_TS=1 = links as the A operand in tensor memory (dslash_mrhs_ts).  Parity-green
+    // but 3-15 % slower than links as the shared-memory B operand (profiles/r02/mrhs_ts_ab.txt), so off.
+    const char *tse = getenv("CD_MRHS_TS");
+    if (tse && atoi(tse) == 1)
+        return nvec == 24 ? launch_mrhs_ts_t<24>(links, in, out, g, nrhs, dagger, s, num_sms, sites, nsites, halo)
+                          : launch_mrhs_ts_t<32>(links, in, out, g, nrhs, dagger, s, num_sms, sites, nsites, halo);
     // B slots: 3 for Nvec 24 (2 and 4 measured 1-3 % slower), 2 for Nvec 32 (shared memory)
     return nvec == 24 ? launch_mrhs_t<24, 3>(links, in, out, g, nrhs, dagger, s, num_sms, sites, nsites, halo)
                       : launch_mrhs_t<32, 2>(links, in, out, g, nrhs, dagger, s, num_sms, sites, nsites, halo);
