@@ -65,7 +65,7 @@ struct MrhsCfg {
     static constexpr int EPI0 = 2 + NBW;                    // first epilogue warp
     static constexpr int THREADS = 32 * (EPI0 + 4);
     static constexpr int TMEM_COLS = 2 * NB <= 256 ? 256 : 512;
-    static_assert(S >= 2, "ring too small");
+    static_assert(S >= 2 && S <= 6, "ring size (barrier slots)");
     static_assert(NB % 16 == 0 && NB <= 256, "MMA N");
 };
 
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
                 int smax, int exp)
 {
     using C = MrhsCfg<NV, NBS>;
-    // optional diagnostic trace of CTA 0 (CD_MRHS_TRACE): trace[ev * 512 + index] = clock64()
+    // optional diagnostic trace of CTA 0 (CD_MRHS_TRACE): trace[ev * 512 + index] = clock64(), 12 events
     const bool tr = trace != nullptr && blockIdx.x == 0;
 #define TR(ev, idx) \
     if (tr && (idx) < 512) trace[(ev) * 512 + (idx)] = clock64();
@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);       // [S]
     uint64_t *empty = full + 16;                                 // [S]
     uint64_t *lempty = full + 52;                                // [S]
+    uint64_t *lfull = full + 58;                                 // [S] link record landed (exp & 32)
     uint64_t *bfull = full + 32;                                 // [NBS]
     uint64_t *bempty = full + 40;                                // [NBS]
     uint64_t *accfull = full + 48;                               // [2]
@@ -205,7 +206,8 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
         for (int j = 0; j < C::S; j++) {
             mbar_init(&full[j], 1);
             mbar_init(&empty[j], 1);            // the MMA commit (A consumed by the tensor core)
-            mbar_init(&lempty[j], C::NBT);      // every builder thread (raw link record read)
+            mbar_init(&lempty[j], (exp & 16) ? C::NBW : C::NBT);   // builder threads (or warps) done with the link
+            mbar_init(&lfull[j], 1);
         }
         for (int j = 0; j < C::NBS; j++) {
             mbar_init(&bfull[j], C::NBW);
@@ -252,14 +254,25 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
                     mbar_wait(&empty[st], ((h / smax) & 1) ^ 1);
                     mbar_wait(&lempty[st], ((h / smax) & 1) ^ 1);
                     unsigned char *dst = ring + st * C::STAGE;
-                    mbar_arrive_expect_tx(&full[st], ((exp & 8) ? 0 : C::BLK) + ((exp & 4) ? 0 : C::MREC));
+                    TR(10, h)
                     // vectors are re-read by 9 sites (keep them in L2), links are read once
+                    if (exp & 32) {
+                        // link first, on its own barrier: the B build overlaps the neighbour block's flight
+                        mbar_arrive_expect_tx(&lfull[st], C::MREC);
+                        bulk_g2s_hint(dst + C::BLK, links + ((size_t)site * 9 + k) * C::MREC, C::MREC, &lfull[st],
+                                      pol_l);
+                        mbar_arrive_expect_tx(&full[st], C::BLK);
+                        bulk_g2s_hint(dst, nbr_block<C::BLK>(g, hl, in, x, site, k, nrb, rb), C::BLK, &full[st],
+                                      pol_v);
+                    } else {
+                    mbar_arrive_expect_tx(&full[st], ((exp & 8) ? 0 : C::BLK) + ((exp & 4) ? 0 : C::MREC));
                     if (!(exp & 8))
                         bulk_g2s_hint(dst, nbr_block<C::BLK>(g, hl, in, x, site, k, nrb, rb), C::BLK,
                                       &full[st], pol_v);
                     if (!(exp & 4))
                         bulk_g2s_hint(dst + C::BLK, links + ((size_t)site * 9 + k) * C::MREC, C::MREC, &full[st],
                                       pol_l);
+                    }
                     TR(0, h)
                 }
             }
@@ -340,9 +353,9 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
                 const uint32_t ratio = half2_bits(hsb[k] * isref);
                 mbar_wait(&bempty[bs], ((h / C::NBS) & 1) ^ 1);
                 if (bt == 0) TR(3, h)
-                mbar_wait(&full[st], (h / smax) & 1);
+                mbar_wait((exp & 32) ? &lfull[st] : &full[st], (h / smax) & 1);
                 if (exp & 1) {
-                    mbar_arrive(&lempty[st]);
+                    if (!(exp & 16) || lane == 0) mbar_arrive(&lempty[st]);
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&bfull[bs]);
                     continue;
@@ -365,7 +378,12 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
                     cc[u] = c >= C::KCH ? c - C::KCH : c;
                     if (e < C::BCH) w[u] = *reinterpret_cast<const uint4 *>(lraw + ((size_t)ii[u] * C::KCH + cc[u]) * 16);
                 }
-                mbar_arrive(&lempty[st]);   // this thread is done with the stage's link record
+                if (exp & 16) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&lempty[st]);   // the warp is done with the stage's link record
+                } else {
+                    mbar_arrive(&lempty[st]);   // this thread is done with the stage's link record
+                }
 #pragma unroll
                 for (int u = 0; u < UPT; u++) {
                     if (bt + u * C::NBT >= C::BCH) break;
@@ -484,19 +502,21 @@ static cudaError_t launch_mrhs_t(const void *links, const void *in, void *out, c
     // ring stages, CD_MRHS_EXP bit 0 = builders skip the B build, 1 = no MMA, 2 = no link copy, 3 = no A copy
     const char *sme = getenv("CD_MRHS_SMAX"), *exe = getenv("CD_MRHS_EXP");
     const int smax = sme && atoi(sme) >= 2 && atoi(sme) < C::S ? atoi(sme) : C::S;
-    const int exp = exe ? atoi(exe) : 0;
+    // default 32: the link record on its own barrier, issued before the neighbour block (B build overlaps
+    // the block's flight): 8^4 x 128 152 -> 149 us, 6^3x12 148 -> 143 us (profiles/r02/mrhs_release.txt)
+    const int exp = exe ? atoi(exe) : 32;
     long long *trace = nullptr;
     const char *tf = getenv("CD_MRHS_TRACE");   // diagnostic only: per-event clock64 of CTA 0
     if (tf) {
-        cudaMalloc(&trace, 10 * 512 * sizeof(long long));
-        cudaMemsetAsync(trace, 0, 10 * 512 * sizeof(long long), s);
+        cudaMalloc(&trace, 12 * 512 * sizeof(long long));
+        cudaMemsetAsync(trace, 0, 12 * 512 * sizeof(long long), s);
     }
     dslash_mrhs<NV, NBS><<<(unsigned)(items < num_sms ? items : num_sms), C::THREADS, C::SMEM, s>>>(
         static_cast<const unsigned char *>(links), static_cast<const unsigned char *>(in),
         static_cast<unsigned char *>(out), g, nrb, dagger, sites, nsites, hl, trace, pf, smax, exp);
     cudaError_t e = cudaGetLastError();
     if (tf) {
-        long long h[10 * 512];
+        long long h[12 * 512];
         cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
         cudaFree(trace);
@@ -534,7 +554,7 @@ struct MrhsTsCfg {
     static constexpr int MREC = 4 * N * N + 16;
     static constexpr int STAGE = (BLK + MREC + 127) / 128 * 128;
     static constexpr int ACOLS = N;                         // 32-bit TMEM columns of one A slot (2N halves)
-    static constexpr int NBS = 3;                           // A slots in TMEM
+    static constexpr int NBS = NV == 24 ? 5 : 4;            // A slots in TMEM (the builders run ahead)
     static constexpr int PITCH = LBO + 32;                  // staging pitch per K chunk
     static constexpr int STG = KCH * PITCH;
     static constexpr int HDR = 1024;
@@ -546,6 +566,7 @@ struct MrhsTsCfg {
     static constexpr int DCOL = 0, ACOL = 2 * MR;           // TMEM: two accumulators, then A slots
     static_assert(S >= 2, "ring too small");
     static_assert(ACOL + NBS * ACOLS <= 512, "TMEM columns");
+    static_assert(S <= 8 && NBS <= 8, "barrier slots");
 };
 
 __device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t *r)
@@ -574,9 +595,10 @@ __global__ void __launch_bounds__(MrhsTsCfg<NV>::THREADS, 1)
     uint64_t *empty = full + 16;                                 // [S]
     uint64_t *lempty = full + 32;                                // [S]
     uint64_t *bfull = full + 48;                                 // [NBS]
-    uint64_t *bempty = full + 52;                                // [NBS]
+    uint64_t *bempty = full + 40;                                // [NBS]
     uint64_t *accfull = full + 56;                               // [2]
     uint64_t *accempty = full + 58;                              // [2]
+    uint64_t *lfull = full + 24;                                 // [S] link record landed
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + 512);
     float *red = reinterpret_cast<float *>(smem + 640);          // [4] epilogue max
     float *hs = reinterpret_cast<float *>(smem + 704);           // [2][9] builder hop scales
@@ -592,6 +614,7 @@ __global__ void __launch_bounds__(MrhsTsCfg<NV>::THREADS, 1)
             mbar_init(&full[j], 1);
             mbar_init(&empty[j], 1);            // the MMA commit (B = neighbour block consumed)
             mbar_init(&lempty[j], C::NBT);      // every builder thread (raw link record read)
+            mbar_init(&lfull[j], 1);
         }
         for (int j = 0; j < C::NBS; j++) {
             mbar_init(&bfull[j], 4);            // one arrival per builder warp
@@ -634,9 +657,10 @@ __global__ void __launch_bounds__(MrhsTsCfg<NV>::THREADS, 1)
                     mbar_wait(&empty[st], ((h / C::S) & 1) ^ 1);
                     mbar_wait(&lempty[st], ((h / C::S) & 1) ^ 1);
                     unsigned char *dst = ring + st * C::STAGE;
-                    mbar_arrive_expect_tx(&full[st], C::BLK + C::MREC);
+                    mbar_arrive_expect_tx(&lfull[st], C::MREC);
+                    bulk_g2s_hint(dst + C::BLK, links + ((size_t)site * 9 + k) * C::MREC, C::MREC, &lfull[st], pol_l);
+                    mbar_arrive_expect_tx(&full[st], C::BLK);
                     bulk_g2s_hint(dst, nbr_block<C::BLK>(g, hl, in, x, site, k, nrb, rb), C::BLK, &full[st], pol_v);
-                    bulk_g2s_hint(dst + C::BLK, links + ((size_t)site * 9 + k) * C::MREC, C::MREC, &full[st], pol_l);
                 }
             }
         }
@@ -714,7 +738,7 @@ __global__ void __launch_bounds__(MrhsTsCfg<NV>::THREADS, 1)
                 const int st = h % C::S, bs = h % C::NBS;
                 const uint32_t ratio = half2_bits(hsb[k] * isref);
                 mbar_wait(&bempty[bs], ((h / C::NBS) & 1) ^ 1);
-                mbar_wait(&full[st], (h / C::S) & 1);
+                mbar_wait(&lfull[st], (h / C::S) & 1);
                 if (live) {
                     const unsigned char *lraw = ring + st * C::STAGE + C::BLK + (size_t)i * C::KCH * 16;
                     uint32_t w[C::N];
