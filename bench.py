@@ -446,9 +446,14 @@ def extras(cd, torch, pm, sampler):
     torch.cuda.synchronize()
     us = _events_us(torch, lambda n: [L.apply_mrhs(b, a) for _ in range(n)], 10)
     tf = pm.flops_per_site(nvec) * V * 128 / us / 1e6
+    N = 2 * nvec
+    comp = V * 9 * (4 * N * N + 16) + 2 * V * (128 * 4 * N + 16)   # links once + every block read and written
     out["8^4_fp16_mrhs128"] = {"us_per_apply": round(us, 1), "us_per_rhs": round(us / 128, 3),
                                "TFLOPS": round(tf, 1), "tensor_frac": round(tf / peak_tf, 3),
                                "tensor_peak_source": "MEASURED_PEAKS.json bf16_tflops (fp16 dense = bf16 dense)",
+                               "compulsory_bytes": comp, "hbm_GBs": round(comp / us / 1e3, 1),
+                               "hbm_frac": round(comp / us / 1e3 / peak_bw, 3),
+                               "limiter": "per-hop barrier hand-offs of the single-thread roles (DESIGN.md §6)",
                                "clocks": sampler.summary(t0, time.perf_counter())}
     del L, a, b, ctx
     # hermiticity-compressed links (5 matrices / site) and the even-odd Schur operator, fp32
