@@ -292,7 +292,9 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
                 TR(9, t)
                 for (int k = 0; k < 9; k++, h++) {
                     const int st = h % smax, bs = h % C::NBS;
-                    mbar_wait(&full[st], (h / smax) & 1);
+                    // merged hand-offs (exp & 64): the builders publish B only once the neighbour block
+                    // has landed too, so bfull alone gates the MMA
+                    if (!(exp & 64)) mbar_wait(&full[st], (h / smax) & 1);
                     TR(1, h)
                     mbar_wait(&bfull[bs], (h / C::NBS) & 1);
                     TR(2, h)
@@ -312,9 +314,10 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
                     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                                      (uint32_t)__cvta_generic_to_shared(&empty[st]))
                                  : "memory");
-                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                     (uint32_t)__cvta_generic_to_shared(&bempty[bs]))
-                                 : "memory");
+                    if (!(exp & 64))   // merged: the builders wait on the stage's empty barrier instead
+                        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                         (uint32_t)__cvta_generic_to_shared(&bempty[bs]))
+                                     : "memory");
                 }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                                  (uint32_t)__cvta_generic_to_shared(&accfull[acc]))
@@ -351,11 +354,21 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
             for (int k = 0; k < 9; k++, h++) {
                 const int st = h % smax, bs = h % C::NBS;
                 const uint32_t ratio = half2_bits(hsb[k] * isref);
-                mbar_wait(&bempty[bs], ((h / C::NBS) & 1) ^ 1);
+                if (exp & 64) {
+                    // B slot bs was last read by hop h - NBS, whose commit completes phase (h - NBS) / S of
+                    // that hop's stage barrier (it cannot be a later phase: hop h + S - NBS needs this B)
+                    if (h >= (uint32_t)C::NBS) {
+                        const uint32_t hp = h - C::NBS;
+                        mbar_wait(&empty[hp % smax], (hp / smax) & 1);
+                    }
+                } else {
+                    mbar_wait(&bempty[bs], ((h / C::NBS) & 1) ^ 1);
+                }
                 if (bt == 0) TR(3, h)
                 mbar_wait((exp & 32) ? &lfull[st] : &full[st], (h / smax) & 1);
                 if (exp & 1) {
                     if (!(exp & 16) || lane == 0) mbar_arrive(&lempty[st]);
+                    if (exp & 64) mbar_wait(&full[st], (h / smax) & 1);
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&bfull[bs]);
                     continue;
@@ -401,6 +414,7 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
                     const int i2 = ii[u] + C::N;
                     *reinterpret_cast<uint4 *>(Bs + c * C::LBO_B + (i2 >> 3) * 128 + (i2 & 7) * 16) = b2;
                 }
+                if (exp & 64) mbar_wait(&full[st], (h / smax) & 1);   // the neighbour block landed too
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bfull[bs]);
@@ -499,7 +513,9 @@ static cudaError_t launch_mrhs_t(const void *links, const void *in, void *out, c
     const char *pfe = getenv("CD_MRHS_PF");   // A/B switch: 0 / 1 override the per-Nvec default
     const int pf = pfe ? atoi(pfe) : (NV == 32);
     // diagnostic knobs (timing experiments only; results are wrong with exp != 0): CD_MRHS_SMAX caps the
-    // ring stages, CD_MRHS_EXP bit 0 = builders skip the B build, 1 = no MMA, 2 = no link copy, 3 = no A copy
+    // ring stages, CD_MRHS_EXP bit 0 = builders skip the B build, 1 = no MMA, 2 = no link copy, 3 = no A copy,
+    // 4 = per-warp link release (no change), 5 = link on its own barrier (the default), 6 = merged hand-offs
+    // (measured 4-11 % slower)
     const char *sme = getenv("CD_MRHS_SMAX"), *exe = getenv("CD_MRHS_EXP");
     const int smax = sme && atoi(sme) >= 2 && atoi(sme) < C::S ? atoi(sme) : C::S;
     // default 32: the link record on its own barrier, issued before the neighbour block (B build overlaps
