@@ -530,9 +530,27 @@ def run_ours(args):
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     ctx = cd.Context(gdims, nvec, pgrid, device=local, nranks=world, rank=rank, nccl_id=nccl_id)
+    fallback = None
     if world > 1:
         if args.transport == "peer":
-            ctx.connect_peers()
+            # every rank must agree on the transport: if any rank cannot open its neighbours' CUDA-IPC
+            # windows (a container without IPC between processes, GPUs without peer access), all
+            # fall back to NCCL rather than leave the scaling run without a line
+            import torch.distributed as dist
+            try:
+                ctx.connect_peers()
+                ok = 1
+            except Exception as e:   # noqa: BLE001 -- reported in the JSON line
+                ok, fallback = 0, f"peer connect failed on rank {rank}: {e}"[:300]
+            flag = torch.tensor([ok], device="cpu" if dist.get_backend() == "gloo" else f"cuda:{local}")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 0:
+                obj = [cd.cd_get_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(obj, src=0)
+                del ctx
+                ctx = cd.Context(gdims, nvec, pgrid, device=local, nranks=world, rank=rank, nccl_id=obj[0])
+                args.transport = "nccl"
+                fallback = fallback or "peer connect failed on another rank"
         ctx.set_transport(args.transport)
     ld = ctx.local_dims
     V_local = ctx.V
@@ -728,6 +746,7 @@ def run_ours(args):
                        "proc_grid": list(pgrid), "local_dims": list(ld), "nvec": nvec, "storage": prec,
                        "op": "apply (D v), chained v->y->v", "variant": variant,
                        "transport": args.transport if world > 1 else None,
+                       **({"transport_fallback": fallback} if fallback else {}),
                        "l2": "inputs larger than L2: links %.1f MB per GPU vs 126 MB L2" %
                              (V_local * 9 * (N * N * (8 if prec == 'fp32' else 4)) / 1e6),
                        "parallelism": f"proc grid {'x'.join(map(str, pgrid))} (T{'xZ' if pgrid[2] > 1 else ''} split)"
