@@ -1045,7 +1045,9 @@ static int check_objs(const cd_links *l, const cd_field *out, const cd_field *in
 static cudaError_t launch_next(cd_context *c, cd_precision p, int id, ApplyArgs a, cudaStream_t s, bool pdl)
 {
     a.seq = c->seq++;
-    const int sms = (a.halo && transport_of(c) == TR_NCCL) ? c->num_sms - c->nccl_sm_reserve : c->num_sms;
+    int sms = (a.halo && transport_of(c) == TR_NCCL) ? c->num_sms - c->nccl_sm_reserve : c->num_sms;
+    static const int cap = getenv("CD_RING_SMS") ? atoi(getenv("CD_RING_SMS")) : 0;   // diagnostic: persistent grid cap
+    if (cap > 0 && cap < sms) sms = cap;
     return launch_dslash(p, id, a, s, pdl, sms);
 }
 
