@@ -26,6 +26,8 @@
 
 #include "device_common.cuh"
 
+#include <cuda.h>   // CUtensorMap (TMA gather4 of the neighbour vector records)
+
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -227,26 +229,60 @@ __device__ __forceinline__ int face_index(const KGeom &g, const int x[4], int mu
 template <cd_precision P, int NV, int MPS>
 struct RingCfg {
     using Q = Cfg<P, NV>;
-    static constexpr int NCW = Q::N / Q::R;                         // consumer warps
+    // MPS = matrices per stage, + 100 per extra consumer group: MPS = 109 is nine matrices per stage
+    // with TWO consumer groups of N/R warps splitting each stage's hops (more warps per SM for the
+    // latency-bound FHFMA chains; group 1 hands its partial sums to group 0 through shared memory)
+    static constexpr int M = MPS % 100;                              // matrices per stage
+    static constexpr int HS = 1 + MPS / 100;                         // consumer groups
+    static constexpr int NCW1 = Q::N / Q::R;                         // consumer warps per group
+    static constexpr int NCW = HS * NCW1;                            // consumer warps
     static constexpr int THREADS = 32 * (NCW + 1);
-    static constexpr int VOFF = MPS * Q::MREC;                      // vector records after the matrices
-    static constexpr int STAGE = ((MPS * (Q::MREC + Q::VREC)) + 127) / 128 * 128;
-    static constexpr int HDR = 1024;                                // barriers + reduction scratch
+    // vector records after the matrices, 128-B aligned; with nine per stage they sit in blocks of four
+    // (each block 128-B aligned: the gather4 destinations) + one: record j at VOFF + vpos(j)
+    static constexpr int VOFF = (M * Q::MREC + 127) / 128 * 128;
+    static constexpr int VBLK = (4 * Q::VREC + 127) / 128 * 128;
+    static constexpr int VAREA = M == 9 ? 2 * VBLK + Q::VREC : M * Q::VREC;
+    static constexpr int STAGE = (VOFF + VAREA + 127) / 128 * 128;
+    __host__ __device__ static constexpr int vpos(int j) { return M == 9 ? (j >> 2) * VBLK + (j & 3) * Q::VREC : j * Q::VREC; }
+    static constexpr int HDR = HS == 1 ? 1024 : 2048;               // barriers + reduction scratch (+ partials)
+    static constexpr int PART = 1024;                                // group-1 partials [2][N] float2 (HS = 2)
     static constexpr int MAXS = 32;
     static constexpr int SMEM_BUDGET = 227 * 1024;                  // the ring is latency bound: all of it
     static constexpr int S = ((SMEM_BUDGET - HDR) / STAGE) > MAXS ? MAXS : ((SMEM_BUDGET - HDR) / STAGE);
     static constexpr int SMEM = HDR + S * STAGE;
     static constexpr int SLOTS = 4;                                  // ticket-counter slots (launch % 4)
-    static_assert(9 % MPS == 0, "MPS must divide 9");
+    static_assert(9 % M == 0, "M must divide 9");
+    static_assert(HS == 1 || (HS == 2 && M == 9), "two consumer groups only with one stage per site");
+    static_assert(HS == 1 || 2 * Q::N * 8 <= HDR - PART, "partials fit the header");
 };
 
-template <cd_precision P, int NV, int MPS>
-__global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(ApplyArgs a, int slot)
+
+// TMA gather4 (sm_100): four rows of a 2-D tensor map -- here four neighbours' vector records -- land
+// back to back in shared memory from ONE instruction (the ring producer's per-copy issue cost is
+// its critical path: nine vector copies per site become two gather4 + one bulk copy)
+__device__ __forceinline__ void gather4_g2s(void *dst_smem, const CUtensorMap *tm, int r0, int r1, int r2, int r3,
+                                            uint64_t *bar)
 {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"((uint32_t)__cvta_generic_to_shared(dst_smem)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+        "r"((uint32_t)__cvta_generic_to_shared(bar))
+        : "memory");
+}
+
+template <cd_precision P, int NV, int MPS>
+__global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(ApplyArgs a, int slotx, const __grid_constant__ CUtensorMap tmv)
+{
+    // slotx = ticket slot | diagnostic bits << 8 (CD_RING_EXP, timing experiments only: 1 = no vector
+    // copies, 2 = no consumer math; results are wrong with either)
+    const int slot = slotx & 0xff, rexp = (slotx >> 8) & 0xff;
+    const bool g4 = (slotx >> 16) & 1;   // tmv describes `in` as [V][VREC] bytes: gather4 the vector records
     using Q = Cfg<P, NV>;
     using RC = RingCfg<P, NV, MPS>;
+    constexpr int M = RC::M;                                         // matrices per stage
     constexpr int S = RC::S;
-    constexpr int G = 9 / MPS;                                       // stages per site
+    constexpr int G = 9 / M;                                       // stages per site
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
     uint64_t *empty = full + RC::MAXS;
@@ -313,20 +349,20 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
                 for (int gi = 0; gi < G; gi++) {
                     int nvc = 0;
 #pragma unroll
-                    for (int j = 0; j < MPS; j++) nvc += !(a.halo && remote_hop(a.g, x, gi * MPS + j));
+                    for (int j = 0; j < M; j++) nvc += !(a.halo && remote_hop(a.g, x, gi * M + j)) && !(rexp & 1);
                     unsigned char *st = stages + (size_t)gi * RC::STAGE;
-                    mbar_arrive_expect_tx(&full[gi], MPS * Q::MREC + nvc * Q::VREC + (gi == 0 ? 4 : 0));
+                    mbar_arrive_expect_tx(&full[gi], M * Q::MREC + nvc * Q::VREC + (gi == 0 ? 4 : 0));
                     if (gi == 0) st_async_u32(&siteq[gi], (uint32_t)site, &full[gi]);
-                    bulk_g2s(st, lsite + (size_t)gi * MPS * Q::MREC, MPS * Q::MREC, &full[gi]);
+                    bulk_g2s(st, lsite + (size_t)gi * M * Q::MREC, M * Q::MREC, &full[gi]);
                 }
                 pdl_wait();   // `in` is written by the previous kernel in the stream
                 for (int gi = 0; gi < G; gi++) {
                     unsigned char *st = stages + (size_t)gi * RC::STAGE;
 #pragma unroll
-                    for (int j = 0; j < MPS; j++) {
-                        const int k = gi * MPS + j;
-                        if (a.halo && remote_hop(a.g, x, k)) continue;
-                        bulk_g2s(st + RC::VOFF + j * Q::VREC, in + (size_t)neighbour(a.g, x, site, k) * Q::VREC,
+                    for (int j = 0; j < M; j++) {
+                        const int k = gi * M + j;
+                        if ((a.halo && remote_hop(a.g, x, k)) || (rexp & 1)) continue;
+                        bulk_g2s(st + RC::VOFF + RC::vpos(j), in + (size_t)neighbour(a.g, x, site, k) * Q::VREC,
                                  Q::VREC, &full[gi]);
                     }
                 }
@@ -356,19 +392,31 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
                 for (int gi = 0; gi < G; gi++) {
                     uint32_t vbytes = 0;
 #pragma unroll
-                    for (int j = 0; j < MPS; j++) {
-                        const bool rem = a.halo && remote_hop(a.g, x, gi * MPS + j);
-                        vbytes += !rem ? Q::VREC : (a.fused ? PREC + (Q::F16 ? 16 : 0) : 0);
+                    for (int j = 0; j < M; j++) {
+                        const bool rem = a.halo && remote_hop(a.g, x, gi * M + j);
+                        vbytes += !rem ? ((rexp & 1) ? 0 : Q::VREC) : (a.fused ? PREC + (Q::F16 ? 16 : 0) : 0);
                     }
                     mbar_wait(&empty[stage], phase ^ 1);
                     unsigned char *st = stages + (size_t)stage * RC::STAGE;
                     // the site id travels like the data: an async store counted on the same barrier
-                    mbar_arrive_expect_tx(&full[stage], MPS * Q::MREC + vbytes + (gi == 0 ? 4 : 0));
+                    mbar_arrive_expect_tx(&full[stage], M * Q::MREC + vbytes + (gi == 0 ? 4 : 0));
                     if (gi == 0) st_async_u32(&siteq[stage], (uint32_t)site, &full[stage]);
-                    bulk_g2s(st, lsite + (size_t)gi * MPS * Q::MREC, MPS * Q::MREC, &full[stage]);
+                    bulk_g2s(st, lsite + (size_t)gi * M * Q::MREC, M * Q::MREC, &full[stage]);
+                    if (M == 9 && g4 && !(rexp & 1) && !(a.halo && is_face<P, NV>(a.g, x))) {
+                        // a site with no remote hop: hops 0-3 and 4-7 by gather4, hop 8 by a bulk copy
+                        int n[9];
 #pragma unroll
-                    for (int j = 0; j < MPS; j++) {
-                        const int k = gi * MPS + j;
+                        for (int k = 0; k < 9; k++) n[k] = neighbour(a.g, x, site, k);
+                        unsigned char *vd = st + RC::VOFF;
+                        gather4_g2s(vd, &tmv, n[0], n[1], n[2], n[3], &full[stage]);
+                        gather4_g2s(vd + RC::vpos(4), &tmv, n[4], n[5], n[6], n[7], &full[stage]);
+                        bulk_g2s(vd + RC::vpos(8), in + (size_t)n[8] * Q::VREC, Q::VREC, &full[stage]);
+                        if (++stage == S) { stage = 0; phase ^= 1; }
+                        continue;
+                    }
+#pragma unroll
+                    for (int j = 0; j < M; j++) {
+                        const int k = gi * M + j;
                         if (a.halo && remote_hop(a.g, x, k)) {
                             if (!a.fused) continue;   // unfused: the halo-term kernel adds this hop
                             if (!landed) {
@@ -379,16 +427,17 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
                             const int mu = k >> 1, blk = (k & 1) ? 0 : 1;
                             const int f = face_index(a.g, x, mu);
                             const unsigned char *rb = static_cast<const unsigned char *>(a.recv) + a.g.blk_off[mu][blk];
-                            bulk_g2s(st + RC::VOFF + j * Q::VREC, rb + (size_t)f * PREC, PREC, &full[stage]);
+                            bulk_g2s(st + RC::VOFF + RC::vpos(j), rb + (size_t)f * PREC, PREC, &full[stage]);
                             // fp16: the 16-B aligned quad of wire scales holding this record's scale lands in
                             // the record's scale slot (+ its 12 pad bytes); the consumer picks 4 * (f & 3) --
                             // no dependent load on the producer thread (its latency is the ring's critical path)
                             if constexpr (Q::F16)
-                                bulk_g2s(st + RC::VOFF + j * Q::VREC + Q::VSCALE,
+                                bulk_g2s(st + RC::VOFF + RC::vpos(j) + Q::VSCALE,
                                          rb + (size_t)sel4(a.g.F, mu) * PREC + (size_t)(f & ~3) * 4, 16, &full[stage]);
                             continue;
                         }
-                        bulk_g2s(st + RC::VOFF + j * Q::VREC, in + (size_t)neighbour(a.g, x, site, k) * Q::VREC,
+                        if (rexp & 1) continue;
+                        bulk_g2s(st + RC::VOFF + RC::vpos(j), in + (size_t)neighbour(a.g, x, site, k) * Q::VREC,
                                  Q::VREC, &full[stage]);
                     }
                     if (++stage == S) { stage = 0; phase ^= 1; }
@@ -407,7 +456,9 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
     // ===== consumers: warp w owns rows [w*R, w*R + R) of the current site, all nine hops
     pdl_wait();   // order our stores after the previous kernel (it may still read `out`)
     const int r = lane / Q::D, d = lane % Q::D;
-    const int row = warp * Q::R + r;
+    const int grp = RC::HS == 1 ? 0 : warp / RC::NCW1;              // consumer group (HS = 2: hop halves)
+    const int row = (warp - grp * RC::NCW1) * Q::R + r;
+    constexpr int J1 = (M + 1) / 2;                                   // HS = 2: group 0 takes hops [0, J1)
     constexpr bool ROT = (Q::ROWB % 128 == 0) && (Q::D * 16 < 128);   // fp16 N=64: avoid 2-way bank conflict
     int stage = 0;
     uint32_t phase = 0;
@@ -433,7 +484,7 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
         auto hop = [&](const unsigned char *st, int j, int so) {
             const unsigned char *mrec = st + j * Q::MREC;
             const unsigned char *mrow = mrec + row * Q::ROWB;
-            const unsigned char *vrec = st + RC::VOFF + j * Q::VREC;
+            const unsigned char *vrec = st + RC::VOFF + RC::vpos(j);
             if constexpr (P == CD_FP32) {
                 float pr[Q::C], pi[Q::C];
 #pragma unroll
@@ -470,18 +521,27 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
         for (int gi = 0; gi < G; gi++) {
             if (gi > 0) mbar_wait(&full[stage], phase);
             const unsigned char *st = stages + (size_t)stage * RC::STAGE;
-            if (!checked) {
-                // straight-line stage (no per-hop branch): the compiler interleaves the MPS
+            if (rexp & 2) {
+            } else if (!checked) {
+                // straight-line stage (no per-hop branch): the compiler interleaves the M
                 // independent hops' loads and FMA chains -- one CTA per SM leaves few consumer
                 // warps, so this ILP is what keeps up with HBM at power-capped clocks (m9 fp16 at
                 // 16^3x32: 1.69 -> 1.55 ms, profiles/r02/ring_ilp_ab.txt).  Waiting for a whole
                 // site's stages before computing (more ILP for m1 / m3) measured slower for fp32.
+                if constexpr (RC::HS == 1) {
 #pragma unroll
-                for (int j = 0; j < MPS; j++) hop(st, j, sofs[gi * MPS + j]);
+                    for (int j = 0; j < M; j++) hop(st, j, sofs[gi * M + j]);
+                } else if (grp == 0) {
+#pragma unroll
+                    for (int j = 0; j < J1; j++) hop(st, j, sofs[gi * M + j]);
+                } else {
+#pragma unroll
+                    for (int j = J1; j < M; j++) hop(st, j, sofs[gi * M + j]);
+                }
             } else {
 #pragma unroll
-                for (int j = 0; j < MPS; j++)
-                    if (!remote_hop(a.g, x, gi * MPS + j)) hop(st, j, 0);
+                for (int j = 0; j < M; j++)
+                    if ((RC::HS == 1 || (j < J1) == (grp == 0)) && !remote_hop(a.g, x, gi * M + j)) hop(st, j, 0);
             }
             // release the stage: every consumer thread arrives after its own reads returned (the
             // accumulators depend on every load) -- no reliance on __syncwarp ordering the other
@@ -497,11 +557,23 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
             im += shfl_xor(im, m);
         }
         const bool owner = (d == 0);
+        if constexpr (RC::HS == 2) {
+            // group 1 hands its partial sums to group 0 (double-buffered by site parity), then moves on
+            float2 *part = reinterpret_cast<float2 *>(smem + RC::PART) + (it & 1) * Q::N;
+            if (grp == 1 && owner) part[row] = make_float2(re, im);
+            bar_named(2, 32 * RC::NCW);
+            if (grp == 1) continue;
+            if (owner) {
+                const float2 p = part[row];
+                re += p.x;
+                im += p.y;
+            }
+        }
         if (checked) {
             if (owner) a.scratch[(size_t)site * Q::N + row] = make_float2(re, im);
         } else {
             const float sg = (a.dagger && row >= NV) ? -1.0f : 1.0f;
-            store_site<P, NV>(out, site, row, owner, sg * re, sg * im, red + 32 * (it & 1), 32 * RC::NCW, 1);
+            store_site<P, NV>(out, site, row, owner, sg * re, sg * im, red + 32 * (it & 1), 32 * RC::NCW1, 1);
         }
     }
 }
@@ -2679,6 +2751,8 @@ struct Variants<CD_FP32, 32> {
 };
 template <>
 struct Variants<CD_FP16, 24> {
+    // {0, 109, 0} (ring m9 with two consumer groups, RingCfg HS = 2) is parity-green but measured 6 %
+    // slower at M5 under the power cap (profiles/r02/ring_g2_rejected.txt), so it is not a candidate
     static constexpr int n = 11;
     static constexpr VDesc v[n] = {{0, 1, 0}, {1, 3, 6}, {1, 9, 6}, {1, 1, 1}, {1, 1, 2}, {1, 3, 2},
                                    {1, 3, 3}, {1, 9, 2}, {1, 9, 3}, {0, 3, 0}, {0, 9, 0}};
@@ -2698,7 +2772,9 @@ inline const char *variant_name_t(int id)
     if (!init) {
         for (int i = 0; i < Variants<P, NV>::n; i++) {
             const VDesc &v = Variants<P, NV>::v[i];
-            if (v.kind == 0) snprintf(names[i], 48, "ring_tma_m%d_%s_nv%d", v.kw, P == CD_FP32 ? "f32" : "f16", NV);
+            if (v.kind == 0 && v.kw >= 100)
+                snprintf(names[i], 48, "ring_tma_m%dg%d_%s_nv%d", v.kw % 100, 1 + v.kw / 100, P == CD_FP32 ? "f32" : "f16", NV);
+            else if (v.kind == 0) snprintf(names[i], 48, "ring_tma_m%d_%s_nv%d", v.kw, P == CD_FP32 ? "f32" : "f16", NV);
             else snprintf(names[i], 48, "fg_kw%d_wr%d_%s_nv%d", v.kw, v.wr, P == CD_FP32 ? "f32" : "f16", NV);
         }
         init = true;
@@ -2725,6 +2801,32 @@ inline cudaError_t launch_ex(const void *fn, dim3 grid, dim3 block, size_t smem,
     return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
+// Host: a 2-D TMA tensor map over a field of V records of `rec` bytes (uint8 elements, one record per
+// row, box = one row) for the producer's gather4.  The driver entry point is looked up once through
+// the runtime (no link-time libcuda dependency); false if unavailable (the bulk-copy path is used).
+inline bool encode_rows_map(CUtensorMap *tm, const void *base, int rec, int V)
+{
+    typedef CUresult (*EncodeFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                 const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn fn = []() -> EncodeFn {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return nullptr;
+        return reinterpret_cast<EncodeFn>(p);
+    }();
+    if (!fn || V <= 0 || rec % 16 || rec > 256) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)rec, (cuuint64_t)V};
+    const cuuint64_t strides[1] = {(cuuint64_t)rec};
+    const cuuint32_t box[2] = {(cuuint32_t)rec, 1};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <cd_precision P, int NV, int MPS>
 cudaError_t launch_ring(const ApplyArgs &a, cudaStream_t s, bool pdl, int num_sms)
 {
@@ -2741,8 +2843,15 @@ cudaError_t launch_ring(const ApplyArgs &a, cudaStream_t s, bool pdl, int num_sm
     int grid = a.g.V < num_sms ? a.g.V : num_sms;
     grid = (grid + 1) & ~1;
     ApplyArgs aa = a;
-    int slot = a.seq & (RC::SLOTS - 1);
-    void *args[] = {&aa, &slot};
+    static const int rexp = getenv("CD_RING_EXP") ? atoi(getenv("CD_RING_EXP")) : 0;   // diagnostic only
+    // nine matrices per stage: a 2-D tensor map of `in` ([V][VREC] bytes) lets the producer gather four
+    // vector records per instruction for every site without remote hops (CD_RING_GATHER=0: nine bulk copies)
+    const bool gather_on = !(getenv("CD_RING_GATHER") && atoi(getenv("CD_RING_GATHER")) == 0);
+    CUtensorMap tmv;
+    memset(&tmv, 0, sizeof(tmv));
+    const bool g4 = RC::M == 9 && gather_on && encode_rows_map(&tmv, a.in, Cfg<P, NV>::VREC, a.g.V);
+    int slot = (a.seq & (RC::SLOTS - 1)) | (rexp << 8) | ((g4 ? 1 : 0) << 16);
+    void *args[] = {&aa, &slot, &tmv};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(RC::THREADS);

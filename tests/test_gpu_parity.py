@@ -169,6 +169,35 @@ def test_apply_all_variants(dims, nvec, prec):
     assert rel_l2(fout.export(), ref) <= TOL[prec]
 
 
+@pytest.mark.parametrize("dims", [(4, 4, 4, 4), (3, 4, 5, 2), (8, 8, 4, 6)])
+def test_ring_gather4_matches_bulk_copies(dims, monkeypatch):
+    """The nine-matrix ring's producer fetches the neighbour vector records with TMA gather4 (two
+    instructions for hops 0-7) or with nine bulk copies (CD_RING_GATHER=0): the same bytes reach the
+    same shared-memory slots, so both results are bit-identical, and match the oracle (apply, dagger)."""
+    nvec, prec = 24, "fp16"
+    N = 2 * nvec
+    Lh = synth.links(dims, N, kind="hermitian")
+    v = synth.vector(dims, N)
+    ctx = cd.Context(dims, nvec)
+    L = ctx.links_upload(Lh, prec)
+    fin, fout = ctx.field(prec), ctx.field(prec)
+    fin.import_(v)
+    names = ctx.variants(prec)
+    ring9 = [i for i, n in enumerate(names) if n.startswith("ring_tma_m9")]
+    assert ring9
+    for var in ring9:
+        ctx.set_option(cd.CD_OPT_VARIANT, var)
+        for dag, op in ((False, oracle.apply), (True, oracle.adjoint)):
+            got = {}
+            for g in ("1", "0"):
+                monkeypatch.setenv("CD_RING_GATHER", g)
+                (L.apply_dagger if dag else L.apply)(fout, fin)
+                got[g] = fout.export()
+            np.testing.assert_array_equal(got["1"], got["0"])
+            assert rel_l2(got["1"], op(dims, Lh, v)) <= TOL[prec], (names[var], dag)
+    ctx.set_option(cd.CD_OPT_VARIANT, -1)
+
+
 @pytest.mark.parametrize("dims,nvec", [((2, 2, 2, 2), 24), ((3, 2, 4, 3), 32), ((4, 4, 4, 4), 24)])
 @pytest.mark.parametrize("prec", ["fp32", "fp16"])
 def test_dagger_is_adjoint_on_hermitian_links(dims, nvec, prec):
