@@ -241,7 +241,7 @@ struct RingCfg {
     // (each block 128-B aligned: the gather4 destinations) + one: record j at VOFF + vpos(j)
     static constexpr int VOFF = (M * Q::MREC + 127) / 128 * 128;
     static constexpr int VBLK = (4 * Q::VREC + 127) / 128 * 128;
-    static constexpr int VAREA = M == 9 ? 2 * VBLK + Q::VREC : M * Q::VREC;
+    static constexpr int VAREA = M == 9 ? 2 * VBLK + Q::VREC : (M == 3 ? VBLK : M * Q::VREC);   // M = 3: + a spare slot
     static constexpr int STAGE = (VOFF + VAREA + 127) / 128 * 128;
     __host__ __device__ static constexpr int vpos(int j) { return M == 9 ? (j >> 2) * VBLK + (j & 3) * Q::VREC : j * Q::VREC; }
     static constexpr int HDR = HS == 1 ? 1024 : 2048;               // barriers + reduction scratch (+ partials)
@@ -389,8 +389,11 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
                 const unsigned char *lsite = links + (size_t)site * 9 * Q::MREC;
                 constexpr int PREC = Q::F16 ? 4 * Q::N : 8 * Q::N;   // wire payload record
 #pragma unroll
+                // TMA gather4 of the vector records (nine or three per stage) for a site without remote hops;
+                // with three per stage the fourth gathered row is a duplicate landing in the block's spare slot
+                const bool use_g4 = (M == 9 || M == 3) && g4 && !(rexp & 1) && !(a.halo && is_face<P, NV>(a.g, x));
                 for (int gi = 0; gi < G; gi++) {
-                    uint32_t vbytes = 0;
+                    uint32_t vbytes = (use_g4 && M == 3) ? Q::VREC : 0;
 #pragma unroll
                     for (int j = 0; j < M; j++) {
                         const bool rem = a.halo && remote_hop(a.g, x, gi * M + j);
@@ -402,15 +405,22 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
                     mbar_arrive_expect_tx(&full[stage], M * Q::MREC + vbytes + (gi == 0 ? 4 : 0));
                     if (gi == 0) st_async_u32(&siteq[stage], (uint32_t)site, &full[stage]);
                     bulk_g2s(st, lsite + (size_t)gi * M * Q::MREC, M * Q::MREC, &full[stage]);
-                    if (M == 9 && g4 && !(rexp & 1) && !(a.halo && is_face<P, NV>(a.g, x))) {
-                        // a site with no remote hop: hops 0-3 and 4-7 by gather4, hop 8 by a bulk copy
-                        int n[9];
-#pragma unroll
-                        for (int k = 0; k < 9; k++) n[k] = neighbour(a.g, x, site, k);
+                    if (use_g4) {
                         unsigned char *vd = st + RC::VOFF;
-                        gather4_g2s(vd, &tmv, n[0], n[1], n[2], n[3], &full[stage]);
-                        gather4_g2s(vd + RC::vpos(4), &tmv, n[4], n[5], n[6], n[7], &full[stage]);
-                        bulk_g2s(vd + RC::vpos(8), in + (size_t)n[8] * Q::VREC, Q::VREC, &full[stage]);
+                        if constexpr (M == 9) {
+                            // hops 0-3 and 4-7 by gather4, hop 8 by a bulk copy
+                            int n[9];
+#pragma unroll
+                            for (int k = 0; k < 9; k++) n[k] = neighbour(a.g, x, site, k);
+                            gather4_g2s(vd, &tmv, n[0], n[1], n[2], n[3], &full[stage]);
+                            gather4_g2s(vd + RC::vpos(4), &tmv, n[4], n[5], n[6], n[7], &full[stage]);
+                            bulk_g2s(vd + RC::vpos(8), in + (size_t)n[8] * Q::VREC, Q::VREC, &full[stage]);
+                        } else {
+                            const int k0 = gi * M;
+                            const int n2 = neighbour(a.g, x, site, k0 + 2);
+                            gather4_g2s(vd, &tmv, neighbour(a.g, x, site, k0), neighbour(a.g, x, site, k0 + 1), n2, n2,
+                                        &full[stage]);
+                        }
                         if (++stage == S) { stage = 0; phase ^= 1; }
                         continue;
                     }
@@ -2801,7 +2811,7 @@ inline cudaError_t launch_ex(const void *fn, dim3 grid, dim3 block, size_t smem,
     return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
-// Host: a 2-D TMA tensor map over a field of V records of `rec` bytes (uint8 elements, one record per
+// Host: a 2-D TMA tensor map over a field of V records of `rec` bytes (32-bit elements, one record per
 // row, box = one row) for the producer's gather4.  The driver entry point is looked up once through
 // the runtime (no link-time libcuda dependency); false if unavailable (the bulk-copy path is used).
 inline bool encode_rows_map(CUtensorMap *tm, const void *base, int rec, int V)
@@ -2817,12 +2827,12 @@ inline bool encode_rows_map(CUtensorMap *tm, const void *base, int rec, int V)
             return nullptr;
         return reinterpret_cast<EncodeFn>(p);
     }();
-    if (!fn || V <= 0 || rec % 16 || rec > 256) return false;
-    const cuuint64_t dims[2] = {(cuuint64_t)rec, (cuuint64_t)V};
+    if (!fn || V <= 0 || rec % 16 || rec > 1024) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)(rec / 4), (cuuint64_t)V};   // 32-bit elements: a row <= 256 of them
     const cuuint64_t strides[1] = {(cuuint64_t)rec};
-    const cuuint32_t box[2] = {(cuuint32_t)rec, 1};
+    const cuuint32_t box[2] = {(cuuint32_t)(rec / 4), 1};
     const cuuint32_t estr[2] = {1, 1};
-    return fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(base), dims, strides, box, estr,
+    return fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void *>(base), dims, strides, box, estr,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -2849,7 +2859,7 @@ cudaError_t launch_ring(const ApplyArgs &a, cudaStream_t s, bool pdl, int num_sm
     const bool gather_on = !(getenv("CD_RING_GATHER") && atoi(getenv("CD_RING_GATHER")) == 0);
     CUtensorMap tmv;
     memset(&tmv, 0, sizeof(tmv));
-    const bool g4 = RC::M == 9 && gather_on && encode_rows_map(&tmv, a.in, Cfg<P, NV>::VREC, a.g.V);
+    const bool g4 = (RC::M == 9 || RC::M == 3) && gather_on && encode_rows_map(&tmv, a.in, Cfg<P, NV>::VREC, a.g.V);
     int slot = (a.seq & (RC::SLOTS - 1)) | (rexp << 8) | ((g4 ? 1 : 0) << 16);
     void *args[] = {&aa, &slot, &tmv};
     cudaLaunchConfig_t cfg = {};

@@ -169,12 +169,13 @@ def test_apply_all_variants(dims, nvec, prec):
     assert rel_l2(fout.export(), ref) <= TOL[prec]
 
 
+@pytest.mark.parametrize("prec,nvec", [("fp16", 24), ("fp32", 24), ("fp16", 32), ("fp32", 32)])
 @pytest.mark.parametrize("dims", [(4, 4, 4, 4), (3, 4, 5, 2), (8, 8, 4, 6)])
-def test_ring_gather4_matches_bulk_copies(dims, monkeypatch):
-    """The nine-matrix ring's producer fetches the neighbour vector records with TMA gather4 (two
-    instructions for hops 0-7) or with nine bulk copies (CD_RING_GATHER=0): the same bytes reach the
-    same shared-memory slots, so both results are bit-identical, and match the oracle (apply, dagger)."""
-    nvec, prec = 24, "fp16"
+def test_ring_gather4_matches_bulk_copies(dims, prec, nvec, monkeypatch):
+    """The nine- and three-matrix rings' producer fetches the neighbour vector records with TMA
+    gather4 (nine per stage: two gather4 + one bulk copy; three: one gather4 with a duplicate fourth
+    row) or with one bulk copy per record (CD_RING_GATHER=0): the same bytes reach the same shared-
+    memory slots, so both results are bit-identical, and match the oracle (apply, dagger)."""
     N = 2 * nvec
     Lh = synth.links(dims, N, kind="hermitian")
     v = synth.vector(dims, N)
@@ -183,9 +184,9 @@ def test_ring_gather4_matches_bulk_copies(dims, monkeypatch):
     fin, fout = ctx.field(prec), ctx.field(prec)
     fin.import_(v)
     names = ctx.variants(prec)
-    ring9 = [i for i, n in enumerate(names) if n.startswith("ring_tma_m9")]
-    assert ring9
-    for var in ring9:
+    rings = [i for i, n in enumerate(names) if n.startswith(("ring_tma_m9", "ring_tma_m3"))]
+    assert rings
+    for var in rings:
         ctx.set_option(cd.CD_OPT_VARIANT, var)
         for dag, op in ((False, oracle.apply), (True, oracle.adjoint)):
             got = {}
