@@ -275,7 +275,7 @@ template <cd_precision P, int NV, int MPS>
 __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(ApplyArgs a, int slotx, const __grid_constant__ CUtensorMap tmv)
 {
     // slotx = ticket slot | diagnostic bits << 8 (CD_RING_EXP, timing experiments only: 1 = no vector
-    // copies, 2 = no consumer math; results are wrong with either)
+    // copies, 2 = no consumer math (results wrong with either), 4 = static round-robin sites) | gather4 << 16
     const int slot = slotx & 0xff, rexp = (slotx >> 8) & 0xff;
     const bool g4 = (slotx >> 16) & 1;   // tmv describes `in` as [V][VREC] bytes: gather4 the vector records
     using Q = Cfg<P, NV>;
@@ -374,8 +374,12 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
             // without the prefetch (a site needs more stages than the ring holds) the static
             // first site goes through the loop like any other
             bool first = !pre && (int)blockIdx.x < V;
+            int nstatic = 0;
             for (;;) {
-                const int tk = first ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(tickets, 1);
+                // (rexp & 4, diagnostic: static round-robin sites instead of tickets)
+                const int tk = first ? (int)blockIdx.x
+                                     : ((rexp & 4) ? (int)blockIdx.x + (++nstatic) * (int)gridDim.x
+                                                   : (int)gridDim.x + atomicAdd(tickets, 1));
                 first = false;
                 if (tk >= V) {   // sentinel stage: tells the consumers to stop
                     mbar_wait(&empty[stage], phase ^ 1);
@@ -595,9 +599,15 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
 // one bulk copy per matrix: HBM carries 5 matrices per site (the neighbours' forward records come
 // back from L2: with tickets in site order they were streamed a few hundred sites earlier), the
 // consumers read a backward matrix by columns.  Unsplit contexts (a split one uses dslash_fgh).
+// compressed ring stage slot p -> hop: X (k = 8), the forward hops 0, 2, 4, 6 (records 0-4 of the site,
+// contiguous), then the backward hops 1, 3, 5, 7
+__host__ __device__ constexpr int kperm(int p) { return p == 0 ? 8 : (p < 5 ? 2 * (p - 1) : 2 * (p - 5) + 1); }
+
 template <cd_precision P, int NV, int MPS>
-__global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ringh(ApplyArgs a, int slot)
+__global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ringh(ApplyArgs a, int slotx, const __grid_constant__ CUtensorMap tmv)
 {
+    const int slot = slotx & 0xff;
+    const bool g4 = (slotx >> 16) & 1;   // tmv describes `in` as [V][VREC]: gather4 the vector records
     using Q = Cfg<P, NV>;
     using RC = RingCfg<P, NV, MPS>;
     constexpr int S = RC::S;
@@ -643,19 +653,41 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ringh(
                 decode(a.g, site, x);
 #pragma unroll
                 for (int gi = 0; gi < G; gi++) {
+                    // stage slots p = gi * MPS + j hold hop kperm(p): the site's own five records (X and the
+                    // forward hops, contiguous in `comp`) first -- ONE copy per stage for that run -- then the
+                    // backward hops (record 1 + mu of x - mu); vectors by gather4 (MPS = 9: two + one bulk
+                    // copy; MPS = 3: one, its fourth row a duplicate into the spare slot)
+                    const int p0 = gi * MPS;
+                    const int nown = p0 < 5 ? (MPS < 5 - p0 ? MPS : 5 - p0) : 0;
+                    const int nvrec = g4 ? (MPS == 3 ? 4 : MPS) : MPS;
                     mbar_wait(&empty[stage], phase ^ 1);
                     unsigned char *st = stages + (size_t)stage * RC::STAGE;
-                    mbar_arrive_expect_tx(&full[stage], MPS * (Q::MREC + Q::VREC) + (gi == 0 ? 4 : 0));
+                    mbar_arrive_expect_tx(&full[stage], MPS * Q::MREC + nvrec * Q::VREC + (gi == 0 ? 4 : 0));
                     if (gi == 0) st_async_u32(&siteq[stage], (uint32_t)site, &full[stage]);
+                    if (nown > 0)
+                        bulk_g2s(st, comp + ((size_t)site * 5 + p0) * Q::MREC, nown * Q::MREC, &full[stage]);
+                    int n[MPS];
+#pragma unroll
+                    for (int j = 0; j < MPS; j++) n[j] = neighbour(a.g, x, site, kperm(p0 + j));
 #pragma unroll
                     for (int j = 0; j < MPS; j++) {
-                        const int k = gi * MPS + j;
-                        const int nb = neighbour(a.g, x, site, k);
-                        // X: record 0 of x; forward 2mu: record 1+mu of x; backward 2mu+1: record 1+mu of x-mu
-                        const int msite = (k == 8 || !(k & 1)) ? site : nb;
-                        const int crec = (k == 8) ? 0 : 1 + (k >> 1);
-                        bulk_g2s(st + j * Q::MREC, comp + ((size_t)msite * 5 + crec) * Q::MREC, Q::MREC, &full[stage]);
-                        bulk_g2s(st + RC::VOFF + j * Q::VREC, in + (size_t)nb * Q::VREC, Q::VREC, &full[stage]);
+                        if (j < nown) continue;
+                        const int mu = p0 + j - 5;   // backward hop 2mu+1: record 1 + mu of x - mu
+                        bulk_g2s(st + j * Q::MREC, comp + ((size_t)n[j] * 5 + 1 + mu) * Q::MREC, Q::MREC, &full[stage]);
+                    }
+                    unsigned char *vd = st + RC::VOFF;
+                    if (g4) {
+                        if constexpr (MPS == 9) {
+                            gather4_g2s(vd, &tmv, n[0], n[1], n[2], n[3], &full[stage]);
+                            gather4_g2s(vd + RC::vpos(4), &tmv, n[4], n[5], n[6], n[7], &full[stage]);
+                            bulk_g2s(vd + RC::vpos(8), in + (size_t)n[8] * Q::VREC, Q::VREC, &full[stage]);
+                        } else {
+                            gather4_g2s(vd, &tmv, n[0], n[1], n[2], n[2], &full[stage]);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < MPS; j++)
+                            bulk_g2s(vd + RC::vpos(j), in + (size_t)n[j] * Q::VREC, Q::VREC, &full[stage]);
                     }
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
@@ -685,10 +717,10 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ringh(
             const unsigned char *st = stages + (size_t)stage * RC::STAGE;
 #pragma unroll
             for (int j = 0; j < MPS; j++) {
-                const int k = gi * MPS + j;
+                const int k = kperm(gi * MPS + j);
                 const bool bwd = (k != 8) && (k & 1);
                 const unsigned char *mrec = st + j * Q::MREC;
-                const unsigned char *vrec = st + RC::VOFF + j * Q::VREC;
+                const unsigned char *vrec = st + RC::VOFF + RC::vpos(j);
                 if constexpr (P == CD_FP32) {
                     float hr = 0.0f, hi = 0.0f;
 #pragma unroll
@@ -2894,8 +2926,12 @@ cudaError_t launch_ringh(const ApplyArgs &a, cudaStream_t s, bool pdl, int num_s
     int grid = a.g.V < num_sms ? a.g.V : num_sms;
     grid = (grid + 1) & ~1;   // 2-CTA clusters: st.async (the site-id handoff)
     ApplyArgs aa = a;
-    int slot = a.seq & (RC::SLOTS - 1);
-    void *args[] = {&aa, &slot};
+    const bool gather_on = !(getenv("CD_RING_GATHER") && atoi(getenv("CD_RING_GATHER")) == 0);
+    CUtensorMap tmv;
+    memset(&tmv, 0, sizeof(tmv));
+    const bool g4 = (MPS == 9 || MPS == 3) && gather_on && encode_rows_map(&tmv, a.in, Cfg<P, NV>::VREC, a.g.V);
+    int slot = (a.seq & (RC::SLOTS - 1)) | ((g4 ? 1 : 0) << 16);
+    void *args[] = {&aa, &slot, &tmv};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(RC::THREADS);

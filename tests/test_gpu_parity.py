@@ -1165,3 +1165,11 @@ def test_compressed_ring_matches_fine_grained(prec, dims, nvec, monkeypatch):
     assert rel_l2(fout.export(), fref.export()) <= (1e-6 if prec == "fp32" else 2e-3)
     C.apply_dagger(fout, fin)
     assert rel_l2(fout.export(), oracle.adjoint(dims, Lh, v)) <= TOL[prec]
+    # the producer's vector records by TMA gather4 or by one bulk copy each: bit-identical
+    for dag in (False, True):
+        got = {}
+        for g in ("1", "0"):
+            monkeypatch.setenv("CD_RING_GATHER", g)
+            (C.apply_dagger if dag else C.apply)(fout, fin)
+            got[g] = fout.export()
+        np.testing.assert_array_equal(got["1"], got["0"])
