@@ -395,12 +395,21 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
 #pragma unroll
                 // TMA gather4 of the vector records (nine or three per stage) for a site without remote hops;
                 // with three per stage the fourth gathered row is a duplicate landing in the block's spare slot
-                const bool use_g4 = (M == 9 || M == 3) && g4 && !(rexp & 1) && !(a.halo && is_face<P, NV>(a.g, x));
+                const bool gsite = (M == 9 || M == 3) && g4 && !(rexp & 1);
                 for (int gi = 0; gi < G; gi++) {
-                    uint32_t vbytes = (use_g4 && M == 3) ? Q::VREC : 0;
+                    // TMA gather4 of the vector records by blocks of four slots (M = 9: slots 0-3 and 4-7, slot 8
+                    // by a bulk copy; M = 3: slots 0-2 with a duplicate fourth row into the spare slot) for every
+                    // block without a remote hop; a face site's block holding its remote hop(s) keeps per-record copies
+                    uint32_t rmask = 0;
+#pragma unroll
+                    for (int j = 0; j < M; j++)
+                        if (a.halo && remote_hop(a.g, x, gi * M + j)) rmask |= 1u << j;
+                    const bool gb0 = gsite && !(rmask & (M == 9 ? 0xFu : 0x7u));
+                    const bool gb1 = gsite && M == 9 && !(rmask & 0xF0u);
+                    uint32_t vbytes = (gb0 && M == 3) ? Q::VREC : 0;
 #pragma unroll
                     for (int j = 0; j < M; j++) {
-                        const bool rem = a.halo && remote_hop(a.g, x, gi * M + j);
+                        const bool rem = (rmask >> j) & 1;
                         vbytes += !rem ? ((rexp & 1) ? 0 : Q::VREC) : (a.fused ? PREC + (Q::F16 ? 16 : 0) : 0);
                     }
                     mbar_wait(&empty[stage], phase ^ 1);
@@ -409,29 +418,21 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
                     mbar_arrive_expect_tx(&full[stage], M * Q::MREC + vbytes + (gi == 0 ? 4 : 0));
                     if (gi == 0) st_async_u32(&siteq[stage], (uint32_t)site, &full[stage]);
                     bulk_g2s(st, lsite + (size_t)gi * M * Q::MREC, M * Q::MREC, &full[stage]);
-                    if (use_g4) {
-                        unsigned char *vd = st + RC::VOFF;
-                        if constexpr (M == 9) {
-                            // hops 0-3 and 4-7 by gather4, hop 8 by a bulk copy
-                            int n[9];
-#pragma unroll
-                            for (int k = 0; k < 9; k++) n[k] = neighbour(a.g, x, site, k);
-                            gather4_g2s(vd, &tmv, n[0], n[1], n[2], n[3], &full[stage]);
-                            gather4_g2s(vd + RC::vpos(4), &tmv, n[4], n[5], n[6], n[7], &full[stage]);
-                            bulk_g2s(vd + RC::vpos(8), in + (size_t)n[8] * Q::VREC, Q::VREC, &full[stage]);
-                        } else {
-                            const int k0 = gi * M;
-                            const int n2 = neighbour(a.g, x, site, k0 + 2);
-                            gather4_g2s(vd, &tmv, neighbour(a.g, x, site, k0), neighbour(a.g, x, site, k0 + 1), n2, n2,
-                                        &full[stage]);
-                        }
-                        if (++stage == S) { stage = 0; phase ^= 1; }
-                        continue;
+                    unsigned char *vd = st + RC::VOFF;
+                    const int k0 = gi * M;
+                    if (gb0) {
+                        const int n2 = neighbour(a.g, x, site, k0 + 2);
+                        gather4_g2s(vd, &tmv, neighbour(a.g, x, site, k0), neighbour(a.g, x, site, k0 + 1), n2,
+                                    M == 9 ? neighbour(a.g, x, site, k0 + 3) : n2, &full[stage]);
                     }
+                    if (gb1)
+                        gather4_g2s(vd + RC::vpos(4), &tmv, neighbour(a.g, x, site, 4), neighbour(a.g, x, site, 5),
+                                    neighbour(a.g, x, site, 6), neighbour(a.g, x, site, 7), &full[stage]);
 #pragma unroll
                     for (int j = 0; j < M; j++) {
+                        if ((gb0 && j < (M == 9 ? 4 : 3)) || (gb1 && j >= 4 && j < 8)) continue;   // gathered
                         const int k = gi * M + j;
-                        if (a.halo && remote_hop(a.g, x, k)) {
+                        if ((rmask >> j) & 1) {
                             if (!a.fused) continue;   // unfused: the halo-term kernel adds this hop
                             if (!landed) {
                                 wait_arrival(a);
