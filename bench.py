@@ -570,6 +570,15 @@ def run_ours(args):
     # warm-up (the first call autotunes; excluded, as the paper excludes its tuning solve)
     steps(max(args.warmup, 3))
     torch.cuda.synchronize()
+    if world > 1:
+        # every rank runs rank 0's tuned variant: per-rank tuning on noisy timings could otherwise pick
+        # kernels with different split protocols (fused one-launch ring vs pack + halo-term kernels)
+        import torch.distributed as dist
+        obj = [ctx.chosen_variant(prec)]
+        dist.broadcast_object_list(obj, src=0)
+        ctx.set_option(cd.CD_OPT_VARIANT, int(obj[0]))
+        steps(2)
+        torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
     t_end = time.perf_counter() + 0.5       # settle clocks under load before the timed region
