@@ -581,10 +581,25 @@ def run_ours(args):
         torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
-    t_end = time.perf_counter() + 0.5       # settle clocks under load before the timed region
-    while time.perf_counter() < t_end:
-        steps(8)
+    # settle clocks under load (~0.5 s) before the timed region.  Every apply is collective when
+    # N > 1, so all ranks must run the SAME number: rank 0's per-step time sets the count (a
+    # time-based loop per rank let the ranks' apply counts diverge and the last applies wait
+    # forever for a neighbour that had already stopped)
+    if world > 1:
+        import torch.distributed as dist
+        t_s = time.perf_counter()
+        steps(4)
         torch.cuda.synchronize()
+        obj = [(time.perf_counter() - t_s) / 4]
+        dist.broadcast_object_list(obj, src=0)
+        for _ in range(max(1, min(2000, int(0.5 / max(8 * float(obj[0]), 1e-6))))):
+            steps(8)
+            torch.cuda.synchronize()
+    else:
+        t_end = time.perf_counter() + 0.5
+        while time.perf_counter() < t_end:
+            steps(8)
+            torch.cuda.synchronize()
     a.generate(seed=0x7873, tag=2)
     barrier(world)
     torch.cuda.synchronize()
