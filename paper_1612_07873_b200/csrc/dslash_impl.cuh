@@ -229,13 +229,8 @@ __device__ __forceinline__ int face_index(const KGeom &g, const int x[4], int mu
 template <cd_precision P, int NV, int MPS>
 struct RingCfg {
     using Q = Cfg<P, NV>;
-    // MPS = matrices per stage, + 100 per extra consumer group: MPS = 109 is nine matrices per stage
-    // with TWO consumer groups of N/R warps splitting each stage's hops (more warps per SM for the
-    // latency-bound FHFMA chains; group 1 hands its partial sums to group 0 through shared memory)
-    static constexpr int M = MPS % 100;                              // matrices per stage
-    static constexpr int HS = 1 + MPS / 100;                         // consumer groups
-    static constexpr int NCW1 = Q::N / Q::R;                         // consumer warps per group
-    static constexpr int NCW = HS * NCW1;                            // consumer warps
+    static constexpr int M = MPS;                                    // matrices per stage
+    static constexpr int NCW = Q::N / Q::R;                          // consumer warps
     static constexpr int THREADS = 32 * (NCW + 1);
     // vector records after the matrices, 128-B aligned; with nine per stage they sit in blocks of four
     // (each block 128-B aligned: the gather4 destinations) + one: record j at VOFF + vpos(j)
@@ -244,16 +239,13 @@ struct RingCfg {
     static constexpr int VAREA = M == 9 ? 2 * VBLK + Q::VREC : (M == 3 ? VBLK : M * Q::VREC);   // M = 3: + a spare slot
     static constexpr int STAGE = (VOFF + VAREA + 127) / 128 * 128;
     __host__ __device__ static constexpr int vpos(int j) { return M == 9 ? (j >> 2) * VBLK + (j & 3) * Q::VREC : j * Q::VREC; }
-    static constexpr int HDR = HS == 1 ? 1024 : 2048;               // barriers + reduction scratch (+ partials)
-    static constexpr int PART = 1024;                                // group-1 partials [2][N] float2 (HS = 2)
+    static constexpr int HDR = 1024;                                // barriers + reduction scratch
     static constexpr int MAXS = 32;
     static constexpr int SMEM_BUDGET = 227 * 1024;                  // the ring is latency bound: all of it
     static constexpr int S = ((SMEM_BUDGET - HDR) / STAGE) > MAXS ? MAXS : ((SMEM_BUDGET - HDR) / STAGE);
     static constexpr int SMEM = HDR + S * STAGE;
     static constexpr int SLOTS = 4;                                  // ticket-counter slots (launch % 4)
     static_assert(9 % M == 0, "M must divide 9");
-    static_assert(HS == 1 || (HS == 2 && M == 9), "two consumer groups only with one stage per site");
-    static_assert(HS == 1 || 2 * Q::N * 8 <= HDR - PART, "partials fit the header");
 };
 
 
@@ -471,9 +463,7 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
     // ===== consumers: warp w owns rows [w*R, w*R + R) of the current site, all nine hops
     pdl_wait();   // order our stores after the previous kernel (it may still read `out`)
     const int r = lane / Q::D, d = lane % Q::D;
-    const int grp = RC::HS == 1 ? 0 : warp / RC::NCW1;              // consumer group (HS = 2: hop halves)
-    const int row = (warp - grp * RC::NCW1) * Q::R + r;
-    constexpr int J1 = (M + 1) / 2;                                   // HS = 2: group 0 takes hops [0, J1)
+    const int row = warp * Q::R + r;
     constexpr bool ROT = (Q::ROWB % 128 == 0) && (Q::D * 16 < 128);   // fp16 N=64: avoid 2-way bank conflict
     int stage = 0;
     uint32_t phase = 0;
@@ -543,20 +533,12 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
                 // warps, so this ILP is what keeps up with HBM at power-capped clocks (m9 fp16 at
                 // 16^3x32: 1.69 -> 1.55 ms, profiles/r02/ring_ilp_ab.txt).  Waiting for a whole
                 // site's stages before computing (more ILP for m1 / m3) measured slower for fp32.
-                if constexpr (RC::HS == 1) {
 #pragma unroll
-                    for (int j = 0; j < M; j++) hop(st, j, sofs[gi * M + j]);
-                } else if (grp == 0) {
-#pragma unroll
-                    for (int j = 0; j < J1; j++) hop(st, j, sofs[gi * M + j]);
-                } else {
-#pragma unroll
-                    for (int j = J1; j < M; j++) hop(st, j, sofs[gi * M + j]);
-                }
+                for (int j = 0; j < M; j++) hop(st, j, sofs[gi * M + j]);
             } else {
 #pragma unroll
                 for (int j = 0; j < M; j++)
-                    if ((RC::HS == 1 || (j < J1) == (grp == 0)) && !remote_hop(a.g, x, gi * M + j)) hop(st, j, 0);
+                    if (!remote_hop(a.g, x, gi * M + j)) hop(st, j, 0);
             }
             // release the stage: every consumer thread arrives after its own reads returned (the
             // accumulators depend on every load) -- no reliance on __syncwarp ordering the other
@@ -572,23 +554,11 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
             im += shfl_xor(im, m);
         }
         const bool owner = (d == 0);
-        if constexpr (RC::HS == 2) {
-            // group 1 hands its partial sums to group 0 (double-buffered by site parity), then moves on
-            float2 *part = reinterpret_cast<float2 *>(smem + RC::PART) + (it & 1) * Q::N;
-            if (grp == 1 && owner) part[row] = make_float2(re, im);
-            bar_named(2, 32 * RC::NCW);
-            if (grp == 1) continue;
-            if (owner) {
-                const float2 p = part[row];
-                re += p.x;
-                im += p.y;
-            }
-        }
         if (checked) {
             if (owner) a.scratch[(size_t)site * Q::N + row] = make_float2(re, im);
         } else {
             const float sg = (a.dagger && row >= NV) ? -1.0f : 1.0f;
-            store_site<P, NV>(out, site, row, owner, sg * re, sg * im, red + 32 * (it & 1), 32 * RC::NCW1, 1);
+            store_site<P, NV>(out, site, row, owner, sg * re, sg * im, red + 32 * (it & 1), 32 * RC::NCW, 1);
         }
     }
 }
@@ -2794,8 +2764,8 @@ struct Variants<CD_FP32, 32> {
 };
 template <>
 struct Variants<CD_FP16, 24> {
-    // {0, 109, 0} (ring m9 with two consumer groups, RingCfg HS = 2) is parity-green but measured 6 %
-    // slower at M5 under the power cap (profiles/r02/ring_g2_rejected.txt), so it is not a candidate
+    // (a ring m9 with two consumer groups splitting each stage's hops was parity-green but measured 6 %
+    // slower at M5 under the power cap and removed: profiles/r02/ring_g2_rejected.txt)
     static constexpr int n = 11;
     static constexpr VDesc v[n] = {{0, 1, 0}, {1, 3, 6}, {1, 9, 6}, {1, 1, 1}, {1, 1, 2}, {1, 3, 2},
                                    {1, 3, 3}, {1, 9, 2}, {1, 9, 3}, {0, 3, 0}, {0, 9, 0}};
@@ -2815,9 +2785,7 @@ inline const char *variant_name_t(int id)
     if (!init) {
         for (int i = 0; i < Variants<P, NV>::n; i++) {
             const VDesc &v = Variants<P, NV>::v[i];
-            if (v.kind == 0 && v.kw >= 100)
-                snprintf(names[i], 48, "ring_tma_m%dg%d_%s_nv%d", v.kw % 100, 1 + v.kw / 100, P == CD_FP32 ? "f32" : "f16", NV);
-            else if (v.kind == 0) snprintf(names[i], 48, "ring_tma_m%d_%s_nv%d", v.kw, P == CD_FP32 ? "f32" : "f16", NV);
+            if (v.kind == 0) snprintf(names[i], 48, "ring_tma_m%d_%s_nv%d", v.kw, P == CD_FP32 ? "f32" : "f16", NV);
             else snprintf(names[i], 48, "fg_kw%d_wr%d_%s_nv%d", v.kw, v.wr, P == CD_FP32 ? "f32" : "f16", NV);
         }
         init = true;
