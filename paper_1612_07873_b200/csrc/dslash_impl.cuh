@@ -770,7 +770,8 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ringh(
         }
         const bool owner = (d == 0);
         const float sg = (a.dagger && row >= NV) ? -1.0f : 1.0f;
-        store_site<P, NV>(out, site, row, owner, sg * re, sg * im, red + 32 * (it & 1), 32 * RC::NCW, 1);
+        store_site<P, NV>(out, site, row, owner, sg * re, sg * im, red + 32 * (it & 1), 32 * RC::NCW, 1,
+                          true);   // x * (1/s) as dslash_ring (R12)
     }
 }
 
