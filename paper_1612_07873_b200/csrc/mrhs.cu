@@ -40,8 +40,9 @@
 
 namespace cd {
 
-template <int NV, int NBS_ = (NV == 24 ? 3 : 2)>
+template <int NV, int NBS_ = (NV == 24 ? 3 : 2), int CPS_ = 1>
 struct MrhsCfg {
+    static constexpr int CPS = CPS_;           // CTAs per SM (2: two independent pipelines per SM)
     static constexpr int N = 2 * NV;           // complex rows of a link matrix
     static constexpr int MR = 128;             // rhs per block (MMA M)
     static constexpr int NB = 2 * N;           // MMA N: B1 rows then B2 rows
@@ -55,7 +56,7 @@ struct MrhsCfg {
     static constexpr int MREC = 4 * N * N + 16;            // fp16 matrix record
     static constexpr int STAGE = (BLK + MREC + 127) / 128 * 128;
     static constexpr int HDR = 1024;
-    static constexpr int SMEM_MAX = 232448;
+    static constexpr int SMEM_MAX = CPS == 1 ? 232448 : 115712;      // per CTA (2 CTAs: 228 KB - 2 x 1 KB reserved)
     static constexpr int NBS = NBS_;                                   // B slots (builders run ahead)
     static constexpr int S = (SMEM_MAX - HDR - NBS * B_BYTES) / STAGE;  // ring stages
     static constexpr int SMEM = HDR + NBS * B_BYTES + S * STAGE;
@@ -172,13 +173,13 @@ __device__ __forceinline__ float hop_scale(const unsigned char *links, const uns
     return sl * sv;
 }
 
-template <int NV, int NBS>
-__global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
+template <int NV, int NBS, int CPS>
+__global__ void __launch_bounds__(MrhsCfg<NV, NBS, CPS>::THREADS, CPS)
     dslash_mrhs(const unsigned char *__restrict__ links, const unsigned char *__restrict__ in, unsigned char *out,
                 KGeom g, int nrb, int dagger, const int *sites, int nsites, MrhsHalo hl, long long *trace, int pf,
                 int smax, int exp)
 {
-    using C = MrhsCfg<NV, NBS>;
+    using C = MrhsCfg<NV, NBS, CPS>;
     // optional diagnostic trace of CTA 0 (CD_MRHS_TRACE): trace[ev * 512 + index] = clock64(), 12 events
     const bool tr = trace != nullptr && blockIdx.x == 0;
 #define TR(ev, idx) \
@@ -438,8 +439,62 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
             mbar_wait(&accfull[acc], (t >> 1) & 1);
             if (et == 0) TR(7, t)
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            uint32_t raw[C::NB];
             const uint32_t base = tmem + acc * C::NB + ((uint32_t)(32 * (warp & 3)) << 16);
+            if constexpr (C::CPS == 2) {
+                // two CTAs per SM (<= 85 registers per thread): two passes over the accumulator in
+                // tensor memory -- the block max, then re-quantise and store -- in chunks of columns
+                bar_named(2, 128);                          // es[] visible
+                float sref = 0.0f;
+#pragma unroll
+                for (int k = 0; k < 9; k++) sref = fmaxf(sref, es[k]);
+                float m = 0.0f;
+#pragma unroll 1
+                for (int cc = 0; cc < C::NB / 16; cc++) {
+                    uint32_t r16[16];
+                    tmem_ld16_nowait(base + cc * 16, r16);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    reg_fence16(r16);
+#pragma unroll
+                    for (int i = 0; i < 16; i++) {
+                        const int col = cc * 16 + i, row = col < C::N ? col : col - C::N;
+                        m = fmaxf(m, fabsf(__uint_as_float(r16[i]) * ((dagger && row >= NV) ? -sref : sref)));
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+                if (lane == 0) red[warp & 3] = m;
+                bar_named(2, 128);
+                m = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+                unsigned char *blk = out + ((size_t)site * nrb + rb) * C::BLK;
+                const float im = m > 0.0f ? __frcp_rn(m) : 0.0f;
+#pragma unroll 1
+                for (int c = 0; c < C::KCH; c++) {
+                    uint32_t re4[4], im4[4];
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(re4[0]), "=r"(re4[1]), "=r"(re4[2]), "=r"(re4[3]) : "r"(base + 4 * c));
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(im4[0]), "=r"(im4[1]), "=r"(im4[2]), "=r"(im4[3]) : "r"(base + C::N + 4 * c));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    uint4 o;
+                    uint32_t *ow = &o.x;
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const int row = 4 * c + q;
+                        const float sg = (dagger && row >= NV) ? -sref : sref;
+                        asm volatile("" : "+r"(re4[q]), "+r"(im4[q]));
+                        __half2 hv = __floats2half2_rn(__uint_as_float(re4[q]) * sg * im, __uint_as_float(im4[q]) * sg * im);
+                        ow[q] = *reinterpret_cast<uint32_t *>(&hv);
+                    }
+                    st_evict_first(blk + c * C::LBO_A + r * 16, o, pol_o);
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&accempty[acc]);   // the MMA may reuse this accumulator
+                if (et == 0) *reinterpret_cast<float4 *>(blk + C::A_BYTES) = make_float4(m, 0.f, 0.f, 0.f);
+                bar_named(2, 128);   // red[] / es[] reuse by the next item
+                continue;
+            }
+            uint32_t raw[C::NB];
 #pragma unroll
             for (int cc = 0; cc < C::NB / 16; cc++) tmem_ld16_nowait(base + cc * 16, raw + cc * 16);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -493,14 +548,15 @@ __global__ void __launch_bounds__(MrhsCfg<NV, NBS>::THREADS, 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
 }
 
-template <int NV, int NBS>
+template <int NV, int NBS, int CPS = 1>
 static cudaError_t launch_mrhs_t(const void *links, const void *in, void *out, const KGeom &g, int nrhs, int dagger,
                                  cudaStream_t s, int num_sms, const int *sites, int nsites, const MrhsHalo *halo)
 {
-    using C = MrhsCfg<NV, NBS>;
+    using C = MrhsCfg<NV, NBS, CPS>;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(dslash_mrhs<NV, NBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaError_t e =
+            cudaFuncSetAttribute(dslash_mrhs<NV, NBS, CPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         if (e != cudaSuccess) return e;
         attr = true;
     }
@@ -527,7 +583,8 @@ static cudaError_t launch_mrhs_t(const void *links, const void *in, void *out, c
         cudaMalloc(&trace, 12 * 512 * sizeof(long long));
         cudaMemsetAsync(trace, 0, 12 * 512 * sizeof(long long), s);
     }
-    dslash_mrhs<NV, NBS><<<(unsigned)(items < num_sms ? items : num_sms), C::THREADS, C::SMEM, s>>>(
+    const int64_t gmax = (int64_t)CPS * num_sms;
+    dslash_mrhs<NV, NBS, CPS><<<(unsigned)(items < gmax ? items : gmax), C::THREADS, C::SMEM, s>>>(
         static_cast<const unsigned char *>(links), static_cast<const unsigned char *>(in),
         static_cast<unsigned char *>(out), g, nrb, dagger, sites, nsites, hl, trace, pf, smax, exp);
     cudaError_t e = cudaGetLastError();
@@ -903,6 +960,14 @@ cudaError_t launch_mrhs(int nvec, const void *links, const void *in, void *out, 
     if (tse && atoi(tse) == 1)
         return nvec == 24 ? launch_mrhs_ts_t<24>(links, in, out, g, nrhs, dagger, s, num_sms, sites, nsites, halo)
                           : launch_mrhs_ts_t<32>(links, in, out, g, nrhs, dagger, s, num_sms, sites, nsites, halo);
+    // Nvec 24: two CTAs per SM, each a full pipeline (2 stages, 2 B slots, 79 registers): the kernel is
+    // bound by the per-hop hand-offs of its single-thread roles, so two independent pipelines per SM
+    // beat one deeper one -- 8^4 x 128 161.6 -> 152.1 us, 8^3x16 x 128 312 -> 300 us, 4^4 x 1024 (L2
+    // resident) 86.3 -> 71.8 us (profiles/r02/mrhs_2cta_ab.txt).  CD_MRHS_2CTA=0: one CTA per SM.
+    // Nvec 32 stays at one CTA (a 32 KB B slot leaves no room for two stages in half the SM).
+    const char *c2 = getenv("CD_MRHS_2CTA");
+    if (nvec == 24 && !(c2 && atoi(c2) == 0))
+        return launch_mrhs_t<24, 2, 2>(links, in, out, g, nrhs, dagger, s, num_sms, sites, nsites, halo);
     // B slots: 3 for Nvec 24 (2 and 4 measured 1-3 % slower), 2 for Nvec 32 (shared memory)
     return nvec == 24 ? launch_mrhs_t<24, 3>(links, in, out, g, nrhs, dagger, s, num_sms, sites, nsites, halo)
                       : launch_mrhs_t<32, 2>(links, in, out, g, nrhs, dagger, s, num_sms, sites, nsites, halo);

@@ -648,7 +648,7 @@ def test_chain_tuner_reports_choice():
 
 
 # ---------------------------------------------------------------- multi-RHS on tcgen05 tensor cores
-@pytest.mark.parametrize("variant", ["ts", "ss"])
+@pytest.mark.parametrize("variant", ["ts", "ss", "ss2"])
 @pytest.mark.parametrize("dims,nvec,nrhs", [((2, 2, 2, 2), 24, 128), ((2, 3, 2, 2), 32, 128),
                                             ((2, 2, 2, 2), 24, 256),
                                             # several items per CTA (V * nrhs / 128 > 148): ring wrap,
@@ -659,8 +659,9 @@ def test_apply_mrhs_tensor_cores(dims, nvec, nrhs, variant, monkeypatch):
     """NEXT-1: out_r = D in_r for 128 right-hand sides per CTA on tcgen05 (fp16 storage, fp32
     accumulate in TMEM) against the oracle applied to every rhs; apply and dagger.  variant "ts":
     links as the A operand built in tensor memory (default); "ss": links as the shared-memory B
-    operand (CD_MRHS_TS=0)."""
+    operand (CD_MRHS_TS=0); "ss2": the same with two CTAs per SM (CD_MRHS_2CTA=1, Nvec 24)."""
     monkeypatch.setenv("CD_MRHS_TS", "1" if variant == "ts" else "0")
+    monkeypatch.setenv("CD_MRHS_2CTA", "1" if variant == "ss2" else "0")   # Nvec 24: two CTAs per SM
     N = 2 * nvec
     V = vol(dims)
     for kind, dag in (("general", False), ("hermitian", True)):
