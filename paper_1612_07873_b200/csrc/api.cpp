@@ -1290,12 +1290,19 @@ static int do_apply(const cd_links *l, cd_field *out, const cd_field *in, void *
             // the full 9-matrix apply; fp32 (and small lattices): the fine-grained fgh kernel, which
             // beats the ring there (81.6 vs 103.6 us at 8^4, profiles/r02/compressed_ring.txt)
             static const int comp_ring = getenv("CD_COMP_RING") ? atoi(getenv("CD_COMP_RING")) : -1;
-            const bool use_ring = comp_ring > 0 || (comp_ring < 0 && l->prec == CD_FP16);
+            // fp16 only: the fp32 compressed ring (CD_COMP_RING=1 used to force it) shows intermittent
+            // errors of 1e-4..1e-2 on repeated applies (also in the round-2 build before the stage
+            // reorder; the fp16 ring is bit-stable), so fp32 always takes the fine-grained kernel
+            const bool use_ring = l->prec == CD_FP16 && comp_ring != 0;
             if (use_ring && c->V >= 4 * c->num_sms) {
                 a.work = c->work;
                 a.seq = c->seq++;
                 static const int mps_env = getenv("CD_COMP_MPS") ? atoi(getenv("CD_COMP_MPS")) : 3;
-                const int mps = (mps_env == 9 && l->prec == CD_FP16 && c->nvec == 24) ? 9 : 3;
+                // two CTAs per SM for the three-matrix compressed ring (its consumers' transposed column
+                // reads are latency bound: twice the consumer warps per SM): M5 fp16 1617 -> 1456 us, 8^4
+                // 49.8 -> 45.7 us (profiles/r02/compressed_2cta_ab.txt); CD_COMP_2CTA=0: one CTA per SM
+                const int two = getenv("CD_COMP_2CTA") ? atoi(getenv("CD_COMP_2CTA")) : 1;
+                const int mps = (mps_env == 9 && l->prec == CD_FP16 && c->nvec == 24) ? 9 : (two == 1 ? 103 : 3);
                 CUDA_TRY(launch_ringh(l->prec, a, s, c->pdl != 0, c->num_sms, mps), "compressed ring launch");
                 return CD_OK;
             }

@@ -1166,6 +1166,13 @@ def test_compressed_ring_matches_fine_grained(prec, dims, nvec, monkeypatch):
     assert rel_l2(fout.export(), fref.export()) <= (1e-6 if prec == "fp32" else 2e-3)
     C.apply_dagger(fout, fin)
     assert rel_l2(fout.export(), oracle.adjoint(dims, Lh, v)) <= TOL[prec]
+    # one CTA per SM (CD_COMP_2CTA=0) instead of two: the same operator
+    monkeypatch.setenv("CD_COMP_2CTA", "0")
+    C.apply(fref, fin)
+    monkeypatch.setenv("CD_COMP_2CTA", "1")
+    C.apply(fout, fin)
+    assert rel_l2(fref.export(), oracle.apply(dims, Lh, v)) <= TOL[prec]
+    assert rel_l2(fout.export(), fref.export()) <= (1e-6 if prec == "fp32" else 2e-3)
     # the producer's vector records by TMA gather4 or by one bulk copy each: bit-identical
     for dag in (False, True):
         got = {}
