@@ -233,7 +233,9 @@ __device__ __forceinline__ int face_index(const KGeom &g, const int x[4], int mu
 template <cd_precision P, int NV, int MPS>
 struct RingCfg {
     using Q = Cfg<P, NV>;
-    static constexpr int M = MPS;                                    // matrices per stage
+    // MPS = matrices per stage, + 100 for two CTAs per SM (MPS = 103)
+    static constexpr int M = MPS % 100;                              // matrices per stage
+    static constexpr int CPS = 1 + MPS / 100;                        // CTAs per SM
     static constexpr int NCW = Q::N / Q::R;                          // consumer warps
     static constexpr int THREADS = 32 * (NCW + 1);
     // vector records after the matrices, 128-B aligned; with nine per stage they sit in blocks of four
@@ -245,11 +247,12 @@ struct RingCfg {
     __host__ __device__ static constexpr int vpos(int j) { return M == 9 ? (j >> 2) * VBLK + (j & 3) * Q::VREC : j * Q::VREC; }
     static constexpr int HDR = 1024;                                // barriers + reduction scratch
     static constexpr int MAXS = 32;
-    static constexpr int SMEM_BUDGET = 227 * 1024;                  // the ring is latency bound: all of it
+    static constexpr int SMEM_BUDGET = CPS == 1 ? 227 * 1024 : 115712;   // latency bound: all of it (per CTA)
     static constexpr int S = ((SMEM_BUDGET - HDR) / STAGE) > MAXS ? MAXS : ((SMEM_BUDGET - HDR) / STAGE);
     static constexpr int SMEM = HDR + S * STAGE;
     static constexpr int SLOTS = 4;                                  // ticket-counter slots (launch % 4)
     static_assert(9 % M == 0, "M must divide 9");
+    static_assert(CPS == 1 || MPS == 103, "two CTAs per SM: three matrices per stage");
 };
 
 
@@ -268,7 +271,7 @@ __device__ __forceinline__ void gather4_g2s(void *dst_smem, const CUtensorMap *t
 }
 
 template <cd_precision P, int NV, int MPS>
-__global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(ApplyArgs a, int slotx, const __grid_constant__ CUtensorMap tmv)
+__global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, RingCfg<P, NV, MPS>::CPS) dslash_ring(ApplyArgs a, int slotx, const __grid_constant__ CUtensorMap tmv)
 {
     // slotx = ticket slot | diagnostic bits << 8 (CD_RING_EXP, timing experiments only: 1 = no vector
     // copies, 2 = no consumer math (results wrong with either), 4 = static round-robin sites, 8 = IEEE
@@ -583,15 +586,16 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ring(A
 __host__ __device__ constexpr int kperm(int p) { return p == 0 ? 8 : (p < 5 ? 2 * (p - 1) : 2 * (p - 5) + 1); }
 
 template <cd_precision P, int NV, int MPS>
-__global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ringh(ApplyArgs a, int slotx, const __grid_constant__ CUtensorMap tmv)
+__global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, RingCfg<P, NV, MPS>::CPS) dslash_ringh(ApplyArgs a, int slotx, const __grid_constant__ CUtensorMap tmv)
 {
     const int slot = slotx & 0xff;
     const bool g4 = (slotx >> 16) & 1;   // tmv describes `in` as [V][VREC]: gather4 the vector records
     using Q = Cfg<P, NV>;
     using RC = RingCfg<P, NV, MPS>;
+    constexpr int MM = RC::M;   // matrices per stage
     constexpr int S = RC::S;
     static_assert(S >= 2, "ring needs at least two stages");
-    constexpr int G = 9 / MPS;
+    constexpr int G = 9 / MM;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
     uint64_t *empty = full + RC::MAXS;
@@ -632,31 +636,31 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ringh(
                 decode(a.g, site, x);
 #pragma unroll
                 for (int gi = 0; gi < G; gi++) {
-                    // stage slots p = gi * MPS + j hold hop kperm(p): the site's own five records (X and the
+                    // stage slots p = gi * MM + j hold hop kperm(p): the site's own five records (X and the
                     // forward hops, contiguous in `comp`) first -- ONE copy per stage for that run -- then the
-                    // backward hops (record 1 + mu of x - mu); vectors by gather4 (MPS = 9: two + one bulk
-                    // copy; MPS = 3: one, its fourth row a duplicate into the spare slot)
-                    const int p0 = gi * MPS;
-                    const int nown = p0 < 5 ? (MPS < 5 - p0 ? MPS : 5 - p0) : 0;
-                    const int nvrec = g4 ? (MPS == 3 ? 4 : MPS) : MPS;
+                    // backward hops (record 1 + mu of x - mu); vectors by gather4 (MM = 9: two + one bulk
+                    // copy; MM = 3: one, its fourth row a duplicate into the spare slot)
+                    const int p0 = gi * MM;
+                    const int nown = p0 < 5 ? (MM < 5 - p0 ? MM : 5 - p0) : 0;
+                    const int nvrec = g4 ? (MM == 3 ? 4 : MM) : MM;
                     mbar_wait(&empty[stage], phase ^ 1);
                     unsigned char *st = stages + (size_t)stage * RC::STAGE;
-                    mbar_arrive_expect_tx(&full[stage], MPS * Q::MREC + nvrec * Q::VREC + (gi == 0 ? 4 : 0));
+                    mbar_arrive_expect_tx(&full[stage], MM * Q::MREC + nvrec * Q::VREC + (gi == 0 ? 4 : 0));
                     if (gi == 0) st_async_u32(&siteq[stage], (uint32_t)site, &full[stage]);
                     if (nown > 0)
                         bulk_g2s(st, comp + ((size_t)site * 5 + p0) * Q::MREC, nown * Q::MREC, &full[stage]);
-                    int n[MPS];
+                    int n[MM];
 #pragma unroll
-                    for (int j = 0; j < MPS; j++) n[j] = neighbour(a.g, x, site, kperm(p0 + j));
+                    for (int j = 0; j < MM; j++) n[j] = neighbour(a.g, x, site, kperm(p0 + j));
 #pragma unroll
-                    for (int j = 0; j < MPS; j++) {
+                    for (int j = 0; j < MM; j++) {
                         if (j < nown) continue;
                         const int mu = p0 + j - 5;   // backward hop 2mu+1: record 1 + mu of x - mu
                         bulk_g2s(st + j * Q::MREC, comp + ((size_t)n[j] * 5 + 1 + mu) * Q::MREC, Q::MREC, &full[stage]);
                     }
                     unsigned char *vd = st + RC::VOFF;
                     if (g4) {
-                        if constexpr (MPS == 9) {
+                        if constexpr (MM == 9) {
                             gather4_g2s(vd, &tmv, n[0], n[1], n[2], n[3], &full[stage]);
                             gather4_g2s(vd + RC::vpos(4), &tmv, n[4], n[5], n[6], n[7], &full[stage]);
                             bulk_g2s(vd + RC::vpos(8), in + (size_t)n[8] * Q::VREC, Q::VREC, &full[stage]);
@@ -665,7 +669,7 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ringh(
                         }
                     } else {
 #pragma unroll
-                        for (int j = 0; j < MPS; j++)
+                        for (int j = 0; j < MM; j++)
                             bulk_g2s(vd + RC::vpos(j), in + (size_t)n[j] * Q::VREC, Q::VREC, &full[stage]);
                     }
                     if (++stage == S) { stage = 0; phase ^= 1; }
@@ -695,8 +699,8 @@ __global__ void __launch_bounds__(RingCfg<P, NV, MPS>::THREADS, 1) dslash_ringh(
             if (gi > 0) mbar_wait(&full[stage], phase);
             const unsigned char *st = stages + (size_t)stage * RC::STAGE;
 #pragma unroll
-            for (int j = 0; j < MPS; j++) {
-                const int k = kperm(gi * MPS + j);
+            for (int j = 0; j < MM; j++) {
+                const int k = kperm(gi * MM + j);
                 const bool bwd = (k != 8) && (k & 1);
                 const unsigned char *mrec = st + j * Q::MREC;
                 const unsigned char *vrec = st + RC::VOFF + RC::vpos(j);
@@ -2775,9 +2779,9 @@ template <>
 struct Variants<CD_FP16, 24> {
     // (a ring m9 with two consumer groups splitting each stage's hops was parity-green but measured 6 %
     // slower at M5 under the power cap and removed: profiles/r02/ring_g2_rejected.txt)
-    static constexpr int n = 11;
+    static constexpr int n = 12;
     static constexpr VDesc v[n] = {{0, 1, 0}, {1, 3, 6}, {1, 9, 6}, {1, 1, 1}, {1, 1, 2}, {1, 3, 2},
-                                   {1, 3, 3}, {1, 9, 2}, {1, 9, 3}, {0, 3, 0}, {0, 9, 0}};
+                                   {1, 3, 3}, {1, 9, 2}, {1, 9, 3}, {0, 3, 0}, {0, 9, 0}, {0, 103, 0}};
 };
 template <>
 struct Variants<CD_FP16, 32> {
@@ -2794,7 +2798,9 @@ inline const char *variant_name_t(int id)
     if (!init) {
         for (int i = 0; i < Variants<P, NV>::n; i++) {
             const VDesc &v = Variants<P, NV>::v[i];
-            if (v.kind == 0) snprintf(names[i], 48, "ring_tma_m%d_%s_nv%d", v.kw, P == CD_FP32 ? "f32" : "f16", NV);
+            if (v.kind == 0 && v.kw > 100)   // two CTAs per SM
+                snprintf(names[i], 48, "ring_tma_m%dx2_%s_nv%d", v.kw % 100, P == CD_FP32 ? "f32" : "f16", NV);
+            else if (v.kind == 0) snprintf(names[i], 48, "ring_tma_m%d_%s_nv%d", v.kw, P == CD_FP32 ? "f32" : "f16", NV);
             else snprintf(names[i], 48, "fg_kw%d_wr%d_%s_nv%d", v.kw, v.wr, P == CD_FP32 ? "f32" : "f16", NV);
         }
         init = true;
@@ -2860,7 +2866,7 @@ cudaError_t launch_ring(const ApplyArgs &a, cudaStream_t s, bool pdl, int num_sm
         attr = true;
     }
     // 2-CTA clusters (148 SMs = 74 TPC pairs): st.async (the site-id handoff) needs a cluster of >= 2
-    int grid = a.g.V < num_sms ? a.g.V : num_sms;
+    int grid = a.g.V < RC::CPS * num_sms ? a.g.V : RC::CPS * num_sms;
     grid = (grid + 1) & ~1;
     ApplyArgs aa = a;
     static const int rexp = getenv("CD_RING_EXP") ? atoi(getenv("CD_RING_EXP")) : 0;   // diagnostic only
@@ -2901,13 +2907,13 @@ cudaError_t launch_ringh(const ApplyArgs &a, cudaStream_t s, bool pdl, int num_s
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    int grid = a.g.V < num_sms ? a.g.V : num_sms;
+    int grid = a.g.V < RC::CPS * num_sms ? a.g.V : RC::CPS * num_sms;
     grid = (grid + 1) & ~1;   // 2-CTA clusters: st.async (the site-id handoff)
     ApplyArgs aa = a;
     const bool gather_on = !(getenv("CD_RING_GATHER") && atoi(getenv("CD_RING_GATHER")) == 0);
     CUtensorMap tmv;
     memset(&tmv, 0, sizeof(tmv));
-    const bool g4 = (MPS == 9 || MPS == 3) && gather_on && encode_rows_map(&tmv, a.in, Cfg<P, NV>::VREC, a.g.V);
+    const bool g4 = (RC::M == 9 || RC::M == 3) && gather_on && encode_rows_map(&tmv, a.in, Cfg<P, NV>::VREC, a.g.V);
     int slot = (a.seq & (RC::SLOTS - 1)) | ((g4 ? 1 : 0) << 16);
     void *args[] = {&aa, &slot, &tmv};
     cudaLaunchConfig_t cfg = {};
@@ -3048,6 +3054,10 @@ cudaError_t launch_pack_t(const void *field, const PackDst &d, const KGeom &g, c
         if (mps == 9) {                                                                                           \
             if constexpr (RingCfg<P, NV, 9>::S >= 2) return launch_ringh<P, NV, 9>(a, s, pdl, sms);                \
             else return cudaErrorNotSupported;                                                                    \
+        }                                                                                                         \
+        if (mps == 103) {                                                                                         \
+            if constexpr (RingCfg<P, NV, 103>::S >= 2) return launch_ringh<P, NV, 103>(a, s, pdl, sms);            \
+            else return launch_ringh<P, NV, 3>(a, s, pdl, sms);                                                   \
         }                                                                                                         \
         return launch_ringh<P, NV, 3>(a, s, pdl, sms);                                                            \
     }                                                                                                             \
