@@ -21,7 +21,8 @@
 // scalar: ratio_k = s_L(x,k) s_v(nbr_k) / s_ref, s_ref = max_k of the same products, folded into
 // B (ratio <= 1: no fp16 overflow), restored in the epilogue, which re-quantises the block.
 //
-// Persistent warp-specialised kernel, one CTA per SM, items = (site, rhs block):
+// Persistent warp-specialised kernel, one CTA per SM (two for Nvec 24: CPS = 2, a complete pipeline
+// each in half the SM), items = (site, rhs block):
 //   warp 0     producer: per hop one bulk copy of the neighbour block (A) + one of the link record
 //              into an S-stage ring (mbarrier full/empty);
 //   warp 1     MMA issuer (one thread): tcgen05.mma kind::f16 into a double-buffered TMEM
